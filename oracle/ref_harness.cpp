@@ -1,0 +1,502 @@
+// ref_harness.cpp -- drives the UNMODIFIED reference library as a checker.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle_abi.h).  This file is compiled by
+// oracle/Makefile together with the reference sources *where they lie* under
+// /root/reference/proj/src/core (nothing is copied into this repo) into
+// oracle/_ref/libramlt_ref.so (timing build) and libramlt_ref_log.so (decision
+// logging build).
+//
+// The logging build observes the reference's own hot loop, run_chain_span
+// (core/driver.cpp:109-173), without modifying it: the linker redirects the
+// cross-object calls driver.o makes (suitability, mh_accept, lens_perturb,
+// multichain_perturb, large_step, KernelController::tallies) and the ray casts
+// path.o / mutations.o make (SceneModel::intersect / visible) to __wrap_*
+// shims below (-Wl,--wrap=<mangled name>).
+//
+//  * A step starts when suitability() is called on the chain's own path
+//    (core/driver.cpp:115).  The first suitability() call a worker thread makes
+//    is always that one, so its argument address identifies the chain.
+//  * a = the value the step's mh_accept() returned (core/driver.cpp:138, 161),
+//    0 when mh_accept was not reached.
+//  * accepted <=> chain.path's vertex buffer changed between two step starts
+//    (core/driver.cpp:169 moves the proposal's buffer into chain.path).
+//  * Chains are std::vector<ChainState> elements (core/driver.cpp:220), so the
+//    address order of &chain.path is the chain index order.
+#include "driver.hpp"
+#include "sampling.hpp"
+#include "scene.hpp"
+#include "camera.hpp"
+#include "adaptation.hpp"
+#include "partition.hpp"
+
+#include "oracle_abi.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+void copy_err(char *err, int errlen, const char *msg) {
+    if (!err || errlen <= 0)
+        return;
+    std::strncpy(err, msg, static_cast<size_t>(errlen) - 1);
+    err[errlen - 1] = '\0';
+}
+
+ramlt::RenderConfig to_config(const oracle_config *c) {
+    ramlt::RenderConfig cfg;
+    static const ramlt::StrategyVariant kStrat[] = {
+        ramlt::StrategyVariant::Fixed, ramlt::StrategyVariant::Global,
+        ramlt::StrategyVariant::RaGrid, ramlt::StrategyVariant::RaQuadtree};
+    if (c->strategy < 0 || c->strategy > 3)
+        throw std::invalid_argument("harness: bad strategy");
+    cfg.strategy = kStrat[c->strategy];
+    cfg.perturbation = c->perturbation == 0 ? ramlt::PerturbationKind::Lens
+                                            : ramlt::PerturbationKind::MultiChain;
+    cfg.mutations = c->mutations;
+    cfg.chains = c->chains;
+    cfg.adaptation.batch_size = c->batch_size;
+    cfg.adaptation.gamma_max = c->gamma_max;
+    cfg.adaptation.gamma_scale = c->gamma_scale;
+    cfg.adaptation.target_acceptance = c->target_acceptance;
+    cfg.adaptation.lambda_init = c->lambda_init;
+    cfg.adaptation.lambda_min = c->lambda_min;
+    cfg.adaptation.sigma2_ratio = c->sigma2_ratio;
+    cfg.n_top = c->n_top;
+    cfg.n_bottom = c->n_bottom;
+    cfg.m_split = c->m_split;
+    cfg.m_refine = c->m_refine;
+    cfg.b_samples = c->b_samples;
+    cfg.seed = c->seed;
+    cfg.width = c->width;
+    cfg.height = c->height;
+    cfg.max_vertices = c->max_vertices;
+    cfg.metrics_interval = c->metrics_interval;
+    cfg.trace_enabled = c->trace_enabled != 0;
+    return cfg;
+}
+
+#ifdef RAMLT_REF_LOG
+struct ChainLog {
+    std::vector<double> a;
+    std::vector<uint8_t> flags;
+};
+
+std::mutex g_mu;
+std::map<const void *, ChainLog *> g_logs;
+std::atomic<bool> g_enabled{false};
+std::atomic<uint64_t> g_rays_closest{0}, g_rays_vis{0};
+uint32_t g_max_steps = 0;
+
+struct ThreadState {
+    const ramlt::Path *chain_path = nullptr;
+    ChainLog *log = nullptr;
+    const void *prev_data = nullptr;
+    bool in_step = false;
+    double a = 0.0;
+    uint8_t kind = 0;
+    uint64_t rays_c = 0, rays_v = 0;
+
+    void finalize() {
+        if (in_step && log) {
+            bool accepted = static_cast<const void *>(chain_path->vertices.data()) != prev_data;
+            if (log->a.size() < g_max_steps) {
+                log->a.push_back(a);
+                log->flags.push_back(static_cast<uint8_t>((accepted ? 1 : 0) | (kind ? 2 : 0) | 4));
+            }
+        }
+        in_step = false;
+        g_rays_closest.fetch_add(rays_c);
+        g_rays_vis.fetch_add(rays_v);
+        rays_c = rays_v = 0;
+    }
+    void reset() {
+        chain_path = nullptr;
+        log = nullptr;
+        in_step = false;
+        rays_c = rays_v = 0;
+    }
+    ~ThreadState() {
+        if (g_enabled.load())
+            finalize();
+    }
+};
+thread_local ThreadState tls;
+#endif
+
+} // namespace
+
+#ifdef RAMLT_REF_LOG
+extern "C" {
+double __real__ZN5ramlt9mh_acceptEdddddd(double, double, double, double, double, double);
+double __wrap__ZN5ramlt9mh_acceptEdddddd(double pc, double pp, double tf, double tr, double sf,
+                                         double sr) {
+    double a = __real__ZN5ramlt9mh_acceptEdddddd(pc, pp, tf, tr, sf, sr);
+    tls.a = a;
+    return a;
+}
+
+double __real__ZN5ramlt11suitabilityERKNS_4PathENS_8StrategyE(const ramlt::Path &, ramlt::Strategy);
+double __wrap__ZN5ramlt11suitabilityERKNS_4PathENS_8StrategyE(const ramlt::Path &p,
+                                                               ramlt::Strategy s) {
+    if (g_enabled.load(std::memory_order_relaxed)) {
+        if (!tls.chain_path) {
+            tls.chain_path = &p;
+            std::lock_guard<std::mutex> lock(g_mu);
+            auto it = g_logs.find(&p);
+            if (it == g_logs.end())
+                it = g_logs.emplace(&p, new ChainLog()).first;
+            tls.log = it->second;
+        }
+        if (&p == tls.chain_path) {
+            if (tls.in_step) {
+                bool accepted = static_cast<const void *>(p.vertices.data()) != tls.prev_data;
+                if (tls.log->a.size() < g_max_steps) {
+                    tls.log->a.push_back(tls.a);
+                    tls.log->flags.push_back(
+                        static_cast<uint8_t>((accepted ? 1 : 0) | (tls.kind ? 2 : 0) | 4));
+                }
+            }
+            tls.prev_data = p.vertices.data();
+            tls.a = 0.0;
+            tls.kind = 0;
+            tls.in_step = true;
+        }
+    }
+    return __real__ZN5ramlt11suitabilityERKNS_4PathENS_8StrategyE(p, s);
+}
+
+std::optional<ramlt::Proposal> __real__ZN5ramlt12lens_perturbERKNS_10SceneModelERKNS_4PathERKNS_9SigmaPairERNS_14RandomSequenceE(
+    const ramlt::SceneModel &, const ramlt::Path &, const ramlt::SigmaPair &, ramlt::RandomSequence &);
+std::optional<ramlt::Proposal> __wrap__ZN5ramlt12lens_perturbERKNS_10SceneModelERKNS_4PathERKNS_9SigmaPairERNS_14RandomSequenceE(
+    const ramlt::SceneModel &sc, const ramlt::Path &p, const ramlt::SigmaPair &s, ramlt::RandomSequence &r) {
+    tls.kind = 1;
+    return __real__ZN5ramlt12lens_perturbERKNS_10SceneModelERKNS_4PathERKNS_9SigmaPairERNS_14RandomSequenceE(sc, p, s, r);
+}
+
+std::optional<ramlt::Proposal> __real__ZN5ramlt18multichain_perturbERKNS_10SceneModelERKNS_4PathERKNS_9SigmaPairERNS_14RandomSequenceE(
+    const ramlt::SceneModel &, const ramlt::Path &, const ramlt::SigmaPair &, ramlt::RandomSequence &);
+std::optional<ramlt::Proposal> __wrap__ZN5ramlt18multichain_perturbERKNS_10SceneModelERKNS_4PathERKNS_9SigmaPairERNS_14RandomSequenceE(
+    const ramlt::SceneModel &sc, const ramlt::Path &p, const ramlt::SigmaPair &s, ramlt::RandomSequence &r) {
+    tls.kind = 1;
+    return __real__ZN5ramlt18multichain_perturbERKNS_10SceneModelERKNS_4PathERKNS_9SigmaPairERNS_14RandomSequenceE(sc, p, s, r);
+}
+
+std::optional<ramlt::Intersection> __real__ZNK5ramlt10SceneModel9intersectERKNS_4Vec3ES3_(
+    const ramlt::SceneModel *, const ramlt::Vec3 &, const ramlt::Vec3 &);
+std::optional<ramlt::Intersection> __wrap__ZNK5ramlt10SceneModel9intersectERKNS_4Vec3ES3_(
+    const ramlt::SceneModel *self, const ramlt::Vec3 &o, const ramlt::Vec3 &d) {
+    if (tls.in_step)
+        ++tls.rays_c;
+    return __real__ZNK5ramlt10SceneModel9intersectERKNS_4Vec3ES3_(self, o, d);
+}
+
+bool __real__ZNK5ramlt10SceneModel7visibleERKNS_4Vec3ES3_(const ramlt::SceneModel *,
+                                                          const ramlt::Vec3 &, const ramlt::Vec3 &);
+bool __wrap__ZNK5ramlt10SceneModel7visibleERKNS_4Vec3ES3_(const ramlt::SceneModel *self,
+                                                          const ramlt::Vec3 &a, const ramlt::Vec3 &b) {
+    if (tls.in_step)
+        ++tls.rays_v;
+    return __real__ZNK5ramlt10SceneModel7visibleERKNS_4Vec3ES3_(self, a, b);
+}
+
+std::vector<ramlt::KernelController::Tally> __real__ZNK5ramlt16KernelController7talliesEv(
+    const ramlt::KernelController *);
+std::vector<ramlt::KernelController::Tally> __wrap__ZNK5ramlt16KernelController7talliesEv(
+    const ramlt::KernelController *self) {
+    // Called once after the span loop (core/driver.cpp:332): the 1-chain run's
+    // last step is still open in this (main) thread and chain.path is alive.
+    if (g_enabled.load())
+        tls.finalize();
+    return __real__ZNK5ramlt16KernelController7talliesEv(self);
+}
+} // extern "C"
+#endif
+
+extern "C" {
+
+int ref_has_log(void) {
+#ifdef RAMLT_REF_LOG
+    return 1;
+#else
+    return 0;
+#endif
+}
+
+// run_render through the reference's public API (core/driver.hpp:80).
+// Returns 0 on success; 1 runtime_error, 2 logic_error, 3 invalid_argument,
+// 4 other exception.  err receives e.what().
+int ref_render(const char *scene_text, const oracle_config *c, oracle_stats *st, oracle_log *lg,
+               oracle_outputs *out, char *err, int errlen) {
+    try {
+        ramlt::SceneModel scene = ramlt::parse_scene(scene_text, "<scene>");
+        ramlt::RenderConfig cfg = to_config(c);
+        cfg.dump_partition = out && out->dump && out->cap_dump > 0;
+#ifdef RAMLT_REF_LOG
+        for (auto &kv : g_logs)
+            delete kv.second;
+        g_logs.clear();
+        tls.reset();
+        g_rays_closest = 0;
+        g_rays_vis = 0;
+        g_max_steps = lg ? lg->steps : 0;
+        g_enabled = lg != nullptr;
+#endif
+        ramlt::RenderResult r = ramlt::run_render(scene, cfg);
+#ifdef RAMLT_REF_LOG
+        g_enabled = false;
+#endif
+        if (st) {
+            std::memset(st, 0, sizeof(*st));
+            st->b = r.b.b;
+            st->b_stderr = r.b.stderr_;
+            st->b_samples = r.b.samples;
+            st->total_mutations = r.total_mutations;
+            st->perturbation_proposals = r.perturbation_proposals;
+            st->large_step_proposals = r.large_step_proposals;
+            st->mean_acceptance = r.mean_acceptance;
+            st->film_luminance = r.film_luminance;
+            st->identity_residual = r.identity_residual;
+            st->region_count = r.region_count;
+            st->loop_time_s = r.metrics.empty() ? 0.0 : r.metrics.back().time_s;
+#ifdef RAMLT_REF_LOG
+            st->rays_closest = g_rays_closest.load();
+            st->rays_visibility = g_rays_vis.load();
+#endif
+            st->n_tallies = r.tallies.size();
+            st->n_trace = r.trace.size();
+            st->n_metrics = r.metrics.size();
+        }
+        if (out) {
+            if (out->image)
+                std::memcpy(out->image, r.image.data.data(), r.image.data.size() * sizeof(float));
+            for (size_t i = 0; i < r.tallies.size() && i < out->cap_tallies; ++i) {
+                if (out->tally_accept)
+                    out->tally_accept[i] = r.tallies[i].accept_sum;
+                if (out->tally_visits)
+                    out->tally_visits[i] = r.tallies[i].visits;
+            }
+            for (size_t i = 0; i < r.trace.size() && i < out->cap_trace && out->trace; ++i) {
+                out->trace[i].mutation_index = r.trace[i].mutation_index;
+                out->trace[i].region = r.trace[i].event.region;
+                out->trace[i].n = r.trace[i].event.n;
+                out->trace[i].lambda = r.trace[i].event.lambda;
+                out->trace[i].alpha_hat = r.trace[i].event.alpha_hat;
+            }
+            if (out->dump && out->cap_dump > 0) {
+                std::strncpy(out->dump, r.partition_dump.c_str(), out->cap_dump - 1);
+                out->dump[out->cap_dump - 1] = '\0';
+            }
+            for (size_t i = 0; i < r.metrics.size() && i < out->cap_metrics && out->metrics; ++i) {
+                out->metrics[i * 4 + 0] = r.metrics[i].time_s;
+                out->metrics[i * 4 + 1] = static_cast<double>(r.metrics[i].mutations);
+                out->metrics[i * 4 + 2] = r.metrics[i].rrmse;
+                out->metrics[i * 4 + 3] = r.metrics[i].mean_acceptance;
+            }
+        }
+#ifdef RAMLT_REF_LOG
+        if (lg) {
+            std::vector<const void *> keys;
+            for (auto &kv : g_logs)
+                keys.push_back(kv.first);
+            std::sort(keys.begin(), keys.end());
+            size_t chains = static_cast<size_t>(c->chains);
+            std::memset(lg->flags, 0, chains * lg->steps);
+            for (size_t i = 0; i < chains * lg->steps; ++i)
+                lg->a[i] = 0.0;
+            for (size_t ci = 0; ci < keys.size() && ci < chains; ++ci) {
+                ChainLog *l = g_logs[keys[ci]];
+                for (size_t j = 0; j < l->a.size() && j < lg->steps; ++j) {
+                    lg->a[ci * lg->steps + j] = l->a[j];
+                    lg->flags[ci * lg->steps + j] = l->flags[j];
+                }
+            }
+        }
+#endif
+        return 0;
+    } catch (const std::invalid_argument &e) {
+        copy_err(err, errlen, e.what());
+        return 3;
+    } catch (const std::logic_error &e) {
+        copy_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::runtime_error &e) {
+        copy_err(err, errlen, e.what());
+        return 1;
+    } catch (const std::exception &e) {
+        copy_err(err, errlen, e.what());
+        return 4;
+    }
+}
+
+// ---- reference primitives, exported for function-level pinning --------------
+
+double ref_normal_quantile(double p) { return ramlt::normal_quantile(p); }
+double ref_normal_cdf(double x) { return ramlt::normal_cdf(x); }
+
+// AngularKernel (core/sampling.cpp:62-92): pdf and pdf_solid_angle.
+int ref_angular_pdf(double sigma, double theta, double *pdf, double *pdf_sa) {
+    try {
+        ramlt::AngularKernel k(sigma);
+        *pdf = k.pdf(theta);
+        *pdf_sa = k.pdf_solid_angle(theta);
+        return 0;
+    } catch (...) {
+        return 3;
+    }
+}
+
+// n draws of AngularKernel::sample from RandomSequence(seed, stream).
+int ref_angular_sample(double sigma, uint64_t seed, uint64_t stream, uint64_t n, double *out) {
+    try {
+        ramlt::AngularKernel k(sigma);
+        ramlt::RandomSequence rng(seed, stream);
+        for (uint64_t i = 0; i < n; ++i)
+            out[i] = k.sample(rng);
+        return 0;
+    } catch (...) {
+        return 3;
+    }
+}
+
+void ref_rng_u32(uint64_t seed, uint64_t stream, uint64_t n, uint32_t *out) {
+    ramlt::RandomSequence rng(seed, stream);
+    for (uint64_t i = 0; i < n; ++i)
+        out[i] = rng.next_u32();
+}
+
+void ref_perturb_direction(const double *omega, double sigma, uint64_t seed, uint64_t stream,
+                           uint64_t n, double *out) {
+    ramlt::AngularKernel k(sigma);
+    ramlt::RandomSequence rng(seed, stream);
+    ramlt::Vec3 w(omega[0], omega[1], omega[2]);
+    for (uint64_t i = 0; i < n; ++i) {
+        ramlt::Vec3 r = ramlt::perturb_direction(w, k, rng);
+        out[3 * i + 0] = r.x;
+        out[3 * i + 1] = r.y;
+        out[3 * i + 2] = r.z;
+    }
+}
+
+void ref_cylindrical(const double *omega, double *uv) {
+    auto p = ramlt::cylindrical_coords(ramlt::Vec3(omega[0], omega[1], omega[2]));
+    uv[0] = p.u;
+    uv[1] = p.v;
+}
+
+double ref_step_size(double gamma_max, double gamma_scale, uint64_t n) {
+    ramlt::AdaptationConfig cfg;
+    cfg.gamma_max = gamma_max;
+    cfg.gamma_scale = gamma_scale;
+    return ramlt::step_size(cfg, n);
+}
+
+double ref_update_lambda(double lambda, double alpha_hat, uint64_t n, double target,
+                         double lambda_min) {
+    ramlt::AdaptationConfig cfg;
+    cfg.target_acceptance = target;
+    cfg.lambda_min = lambda_min;
+    return ramlt::update_lambda(lambda, alpha_hat, n, cfg);
+}
+
+// sigma_for of a Global controller after feeding `n` acceptances.
+double ref_controller_feed(const double *a, uint64_t n, int *updates_out) {
+    ramlt::AdaptationConfig cfg;
+    ramlt::KernelController ctl(ramlt::ControllerKind::Global, cfg);
+    int updates = 0;
+    for (uint64_t i = 0; i < n; ++i)
+        if (ctl.record_acceptance(0, a[i]))
+            ++updates;
+    if (updates_out)
+        *updates_out = updates;
+    return ctl.lambda_of(0);
+}
+
+int ref_grid_cell(int n, double u, double v) {
+    ramlt::Grid2D g(n);
+    return g.cell_of({u, v});
+}
+
+double ref_mh_accept(double pc, double pp, double tf, double tr, double sf, double sr, int *status) {
+    try {
+        *status = 0;
+        return ramlt::mh_accept(pc, pp, tf, tr, sf, sr);
+    } catch (...) {
+        *status = 3;
+        return 0.0;
+    }
+}
+
+double ref_fresnel(double cos_i, double ior) { return ramlt::fresnel_dielectric(cos_i, ior); }
+
+// Camera round trip rp(primary(u,v)) (core/camera.cpp:32-49) and pdfs.
+int ref_camera(const double *cam /*pos3 look3 up3 fov*/, int w, int h, double u, double v,
+               double *dir3, double *uv2, double *importance, double *dir_pdf) {
+    try {
+        ramlt::Camera c(ramlt::Vec3(cam[0], cam[1], cam[2]), ramlt::Vec3(cam[3], cam[4], cam[5]),
+                        ramlt::Vec3(cam[6], cam[7], cam[8]), cam[9]);
+        c.configure_image(w, h);
+        ramlt::Vec3 d = c.primary_direction(u, v);
+        dir3[0] = d.x;
+        dir3[1] = d.y;
+        dir3[2] = d.z;
+        auto rp = c.raster_position(d);
+        uv2[0] = rp ? rp->u : -1.0;
+        uv2[1] = rp ? rp->v : -1.0;
+        *importance = c.importance(d);
+        *dir_pdf = c.direction_pdf(d);
+        return 0;
+    } catch (...) {
+        return 3;
+    }
+}
+
+// parse_scene (core/scene.cpp:114-234): 0 ok, 1 runtime_error (message in err).
+int ref_parse(const char *text, int *counts /* materials spheres triangles emitters */, char *err,
+              int errlen) {
+    try {
+        ramlt::SceneModel s = ramlt::parse_scene(text, "<scene>");
+        counts[0] = static_cast<int>(s.materials.size());
+        counts[1] = static_cast<int>(s.spheres.size());
+        counts[2] = static_cast<int>(s.triangles.size());
+        counts[3] = static_cast<int>(s.emitters.size());
+        return 0;
+    } catch (const std::runtime_error &e) {
+        copy_err(err, errlen, e.what());
+        return 1;
+    } catch (const std::exception &e) {
+        copy_err(err, errlen, e.what());
+        return 4;
+    }
+}
+
+// Quadtree::refine (core/partition.cpp:68-100): visit a point list, refine,
+// and return the leaf list (region u0 v0 u1 v1 visits) as text.
+int ref_quadtree(const double *uv, uint64_t n, uint64_t m_split, int rounds, char *out, int cap) {
+    ramlt::AdaptationConfig cfg;
+    ramlt::KernelController ctl(ramlt::ControllerKind::Regional, cfg);
+    ramlt::Quadtree tree(ctl);
+    int splits = 0;
+    for (int r = 0; r < rounds; ++r) {
+        for (uint64_t i = 0; i < n; ++i)
+            tree.record_visit(tree.classify({uv[2 * i], uv[2 * i + 1]}));
+        splits += tree.refine(m_split);
+    }
+    std::ostringstream os;
+    for (const auto &leaf : tree.leaves())
+        os << leaf.region << " " << leaf.u0 << " " << leaf.v0 << " " << leaf.u1 << " " << leaf.v1
+           << " " << leaf.visits << "\n";
+    std::string s = os.str();
+    std::strncpy(out, s.c_str(), static_cast<size_t>(cap) - 1);
+    out[cap - 1] = '\0';
+    return splits;
+}
+
+} // extern "C"
