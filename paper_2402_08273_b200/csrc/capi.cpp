@@ -1,0 +1,403 @@
+// capi.cpp -- the C-ABI of libramlt_gpu.so (include/ramlt_gpu.h), the host
+// mirror of the reference's scene parser (core/scene.cpp:104-243) and camera
+// construction (core/camera.cpp:8-30).  Host code only; compiled without FMA
+// contraction so the camera basis rounds exactly like the reference's.
+#include "engine.h"
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+using ramlt_b200::EngineBase;
+using ramlt_b200::HostScene;
+
+struct ramlt_gpu {
+    std::unique_ptr<EngineBase> eng;
+    std::string err;
+};
+
+struct ramlt_scene {
+    HostScene hs;
+    ramlt_scene_desc desc;
+};
+
+namespace ramlt_b200 {
+
+namespace {
+inline void sub3(const double *a, const double *b, double *o) {
+    o[0] = a[0] - b[0];
+    o[1] = a[1] - b[1];
+    o[2] = a[2] - b[2];
+}
+inline double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+inline void cross3(const double *a, const double *b, double *o) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+inline void unit3(const double *a, double *o) {
+    double l = std::sqrt(dot3(a, a));
+    o[0] = a[0] / l;
+    o[1] = a[1] / l;
+    o[2] = a[2] / l;
+}
+}  // namespace
+
+CameraBasis make_camera(const double cam[10], int width, int height) {
+    // Camera::Camera (core/camera.cpp:8-20)
+    double fov = cam[9];
+    if (!(fov > 0.0 && fov < 180.0))
+        throw std::invalid_argument("camera: fov must be in (0, 180) degrees");
+    CameraBasis c;
+    double d[3], r[3];
+    std::memcpy(c.pos, cam, sizeof(c.pos));
+    sub3(cam + 3, cam, d);
+    unit3(d, c.fwd);
+    cross3(c.fwd, cam + 6, r);
+    if (std::sqrt(dot3(r, r)) < 1e-12)
+        throw std::invalid_argument("camera: up vector is parallel to the view direction");
+    unit3(r, c.right);
+    cross3(c.right, c.fwd, c.up);
+    c.tanh = std::tan(0.5 * fov * 3.14159265358979323846 / 180.0);
+    // configure_image (core/camera.cpp:22-30)
+    if (width < 1 || height < 1)
+        throw std::invalid_argument("camera: resolution must be positive");
+    c.aspect = static_cast<double>(width) / static_cast<double>(height);
+    c.area = 4.0 * c.tanh * c.tanh * c.aspect;
+    c.sensor = static_cast<double>(width) * static_cast<double>(height) / c.area;
+    return c;
+}
+
+// parse_scene mirror (core/scene.cpp:104-234): same grammar, same messages.
+static HostScene parse_scene(const std::string &text, const std::string &origin) {
+    HostScene s;
+    std::map<std::string, int> ids;
+    bool have_camera = false;
+    std::vector<std::pair<bool, int>> order;
+    std::istringstream stream(text);
+    std::string line;
+    int ln = 0;
+    auto fail = [&](int l, const std::string &msg) {
+        throw std::runtime_error(origin + ":" + std::to_string(l) + ": " + msg);
+    };
+    while (std::getline(stream, line)) {
+        ++ln;
+        size_t start = line.find_first_not_of(" \t\r");
+        if (start == std::string::npos || line[start] == '#')
+            continue;
+        std::istringstream ls(line);
+        std::string tag;
+        ls >> tag;
+        auto check = [&] {
+            if (ls.fail())
+                fail(ln, "malformed '" + tag + "' record");
+        };
+        auto mat_id = [&](const std::string &name) {
+            auto it = ids.find(name);
+            if (it == ids.end())
+                fail(ln, "unknown material '" + name + "'");
+            return it->second;
+        };
+        if (tag == "camera") {
+            double v[10];
+            for (double &x : v)
+                ls >> x;
+            check();
+            try {
+                make_camera(v, 1, 1);
+            } catch (const std::exception &e) {
+                fail(ln, e.what());
+            }
+            std::memcpy(s.cam, v, sizeof(v));
+            have_camera = true;
+        } else if (tag == "material") {
+            std::string name, kind;
+            ls >> name >> kind;
+            check();
+            ramlt_material m{};
+            m.albedo[0] = m.albedo[1] = m.albedo[2] = 0.5;
+            m.ior = 1.5;
+            m.exponent = 32.0;
+            if (kind == "diffuse") {
+                m.kind = RAMLT_DIFFUSE;
+                ls >> m.albedo[0] >> m.albedo[1] >> m.albedo[2];
+                check();
+            } else if (kind == "mirror") {
+                m.kind = RAMLT_MIRROR;
+                ls >> m.albedo[0] >> m.albedo[1] >> m.albedo[2];
+                check();
+            } else if (kind == "dielectric") {
+                m.kind = RAMLT_DIELECTRIC;
+                ls >> m.ior >> m.albedo[0] >> m.albedo[1] >> m.albedo[2];
+                check();
+                if (m.ior <= 1.0)
+                    fail(ln, "dielectric ior must be > 1");
+            } else if (kind == "glossy") {
+                m.kind = RAMLT_GLOSSY;
+                ls >> m.albedo[0] >> m.albedo[1] >> m.albedo[2] >> m.exponent;
+                check();
+                if (m.exponent <= 0.0)
+                    fail(ln, "glossy exponent must be > 0");
+            } else {
+                fail(ln, "unknown material kind '" + kind + "'");
+            }
+            if (m.kind != RAMLT_DIELECTRIC)
+                for (int c = 0; c < 3; ++c)
+                    if (m.albedo[c] < 0.0 || m.albedo[c] > 1.0)
+                        fail(ln, "albedo components must be in [0,1]");
+            if (ids.count(name))
+                fail(ln, "duplicate material '" + name + "'");
+            ids[name] = static_cast<int>(s.mats.size());
+            s.mats.push_back(m);
+        } else if (tag == "sphere") {
+            ramlt_sphere sp{};
+            std::string mat;
+            ls >> sp.center[0] >> sp.center[1] >> sp.center[2] >> sp.radius >> mat;
+            check();
+            if (sp.radius <= 0.0)
+                fail(ln, "sphere radius must be > 0");
+            sp.material = mat_id(mat);
+            sp.emitter = -1;
+            order.emplace_back(true, static_cast<int>(s.sph.size()));
+            s.sph.push_back(sp);
+        } else if (tag == "tri") {
+            ramlt_triangle t{};
+            std::string mat;
+            ls >> t.a[0] >> t.a[1] >> t.a[2] >> t.b[0] >> t.b[1] >> t.b[2] >> t.c[0] >> t.c[1] >> t.c[2] >> mat;
+            check();
+            t.material = mat_id(mat);
+            t.emitter = -1;
+            order.emplace_back(false, static_cast<int>(s.tri.size()));
+            s.tri.push_back(t);
+        } else if (tag == "emitter") {
+            int index;
+            double r[3];
+            ls >> index >> r[0] >> r[1] >> r[2];
+            check();
+            if (index < 0 || index >= static_cast<int>(order.size()))
+                fail(ln, "emitter geometry index out of range");
+            if (r[0] < 0.0 || r[1] < 0.0 || r[2] < 0.0)
+                fail(ln, "emitted radiance must be non-negative");
+            int e = static_cast<int>(s.emit.size() / 3);
+            s.emit.insert(s.emit.end(), r, r + 3);
+            auto [is_sphere, gi] = order[index];
+            if (is_sphere)
+                s.sph[gi].emitter = e;
+            else
+                s.tri[gi].emitter = e;
+        } else {
+            fail(ln, "unknown record '" + tag + "'");
+        }
+    }
+    if (!have_camera)
+        throw std::runtime_error(origin + ": scene has no camera");
+    if (s.emit.empty())
+        throw std::runtime_error(origin + ": scene has no emitter");
+    return s;
+}
+
+static HostScene from_desc(const ramlt_scene_desc *d) {
+    HostScene s;
+    std::memcpy(s.cam, d->cam_position, 3 * sizeof(double));
+    std::memcpy(s.cam + 3, d->cam_look_at, 3 * sizeof(double));
+    std::memcpy(s.cam + 6, d->cam_up, 3 * sizeof(double));
+    s.cam[9] = d->cam_fov_deg;
+    s.mats.assign(d->materials, d->materials + d->n_materials);
+    s.sph.assign(d->spheres, d->spheres + d->n_spheres);
+    s.tri.assign(d->triangles, d->triangles + d->n_triangles);
+    s.emit.assign(d->emitter_radiance, d->emitter_radiance + 3 * d->n_emitters);
+    if (s.emit.empty())
+        throw std::runtime_error("scene has no emitter");
+    for (auto &t : s.tri)
+        if (t.material < 0 || t.material >= d->n_materials || t.emitter >= d->n_emitters)
+            throw std::invalid_argument("triangle references an unknown material or emitter");
+    for (auto &sp : s.sph)
+        if (sp.material < 0 || sp.material >= d->n_materials || sp.emitter >= d->n_emitters)
+            throw std::invalid_argument("sphere references an unknown material or emitter");
+    return s;
+}
+
+}  // namespace ramlt_b200
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <class F> int guard(std::string &err, F &&f) {
+    try {
+        f();
+        return RAMLT_OK;
+    } catch (const ramlt_b200::CudaError &e) {
+        err = e.what();
+        return RAMLT_E_CUDA;
+    } catch (const std::invalid_argument &e) {
+        err = e.what();
+        return RAMLT_E_INVALID;
+    } catch (const std::logic_error &e) {
+        err = e.what();
+        return RAMLT_E_LOGIC;
+    } catch (const std::runtime_error &e) {
+        err = e.what();
+        return RAMLT_E_RUNTIME;
+    } catch (const std::exception &e) {
+        err = e.what();
+        return RAMLT_E_OTHER;
+    }
+}
+
+ramlt_b200::EngineBase *make(const HostScene &hs, const ramlt_render_desc *d) {
+    if (!d)
+        throw std::logic_error("null render descriptor");
+    if (d->precision == RAMLT_F64)
+        return ramlt_b200::make_engine_f64(hs, *d);
+    if (d->precision == RAMLT_F32)
+        return ramlt_b200::make_engine_f32(hs, *d);
+    throw std::invalid_argument("precision must be RAMLT_F32 or RAMLT_F64");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ramlt_gpu_abi_version(void) { return RAMLT_GPU_ABI_VERSION; }
+
+void ramlt_gpu_default_desc(ramlt_render_desc *d) {
+    std::memset(d, 0, sizeof(*d));
+    // RenderConfig defaults (core/driver.hpp:19-39), AdaptationConfig (adaptation.hpp:14-22)
+    d->strategy = RAMLT_RA_QUADTREE;
+    d->perturbation = RAMLT_LENS;
+    d->mutations = 1000000;
+    d->time_budget_s = 0.0;
+    d->chains = 1;
+    d->batch_size = 10;
+    d->gamma_max = 1.0;
+    d->gamma_scale = 5.0;
+    d->target_acceptance = 0.5;
+    d->lambda_init = 1.0;
+    d->lambda_min = -30.0;
+    d->sigma2_ratio = 1.0;
+    d->n_top = 20;
+    d->n_bottom = 50;
+    d->m_split = 5000;
+    d->m_refine = 10000000;
+    d->b_samples = 1000000;
+    d->seed = 1;
+    d->width = 256;
+    d->height = 256;
+    d->max_vertices = 20;
+    d->metrics_interval = 1000000;
+    d->precision = RAMLT_F32;
+    d->rng = RAMLT_RNG_PHILOX;
+    d->adapt_mode = RAMLT_ADAPT_AUTO;
+    d->lanes_per_chain = 0;
+    d->device = -1;
+}
+
+int ramlt_scene_parse(const char *text, const char *origin, ramlt_scene **out) {
+    return guard(g_create_err, [&] {
+        auto sc = std::make_unique<ramlt_scene>();
+        sc->hs = ramlt_b200::parse_scene(text ? text : "", origin ? origin : "<string>");
+        ramlt_scene_desc &d = sc->desc;
+        std::memset(&d, 0, sizeof(d));
+        std::memcpy(d.cam_position, sc->hs.cam, 3 * sizeof(double));
+        std::memcpy(d.cam_look_at, sc->hs.cam + 3, 3 * sizeof(double));
+        std::memcpy(d.cam_up, sc->hs.cam + 6, 3 * sizeof(double));
+        d.cam_fov_deg = sc->hs.cam[9];
+        d.n_materials = static_cast<int32_t>(sc->hs.mats.size());
+        d.n_spheres = static_cast<int32_t>(sc->hs.sph.size());
+        d.n_triangles = static_cast<int32_t>(sc->hs.tri.size());
+        d.n_emitters = static_cast<int32_t>(sc->hs.emit.size() / 3);
+        d.materials = sc->hs.mats.data();
+        d.spheres = sc->hs.sph.data();
+        d.triangles = sc->hs.tri.data();
+        d.emitter_radiance = sc->hs.emit.data();
+        *out = sc.release();
+    });
+}
+
+const ramlt_scene_desc *ramlt_scene_get_desc(const ramlt_scene *s) { return s ? &s->desc : nullptr; }
+void ramlt_scene_free(ramlt_scene *s) { delete s; }
+
+int ramlt_gpu_create(const ramlt_scene_desc *scene, const ramlt_render_desc *desc, ramlt_gpu **out) {
+    return guard(g_create_err, [&] {
+        if (!scene)
+            throw std::logic_error("null scene descriptor");
+        HostScene hs = ramlt_b200::from_desc(scene);
+        auto h = std::make_unique<ramlt_gpu>();
+        h->eng.reset(make(hs, desc));
+        *out = h.release();
+    });
+}
+
+int ramlt_gpu_create_from_text(const char *text, const char *origin, const ramlt_render_desc *desc,
+                               ramlt_gpu **out) {
+    return guard(g_create_err, [&] {
+        HostScene hs = ramlt_b200::parse_scene(text ? text : "", origin ? origin : "<string>");
+        auto h = std::make_unique<ramlt_gpu>();
+        h->eng.reset(make(hs, desc));
+        *out = h.release();
+    });
+}
+
+const char *ramlt_gpu_last_create_error(void) { return g_create_err.c_str(); }
+
+#define RAMLT_H(body)                                                                              \
+    do {                                                                                           \
+        if (!h)                                                                                    \
+            return RAMLT_E_LOGIC;                                                                  \
+        return guard(h->err, [&] { body; });                                                       \
+    } while (0)
+
+int ramlt_gpu_estimate_b(ramlt_gpu *h, double *b, double *se) { RAMLT_H(h->eng->estimate_b(b, se)); }
+int ramlt_gpu_estimate_b_partials(ramlt_gpu *h, uint64_t begin, uint64_t end, double *out) {
+    RAMLT_H(h->eng->estimate_b_partials(begin, end, out));
+}
+int ramlt_gpu_reduce_b(ramlt_gpu *h, const double *p, uint64_t n, double *b, double *se) {
+    RAMLT_H(h->eng->reduce_b(p, n, b, se));
+}
+int ramlt_gpu_set_b(ramlt_gpu *h, double b) { RAMLT_H(h->eng->set_b(b)); }
+int ramlt_gpu_init_chains(ramlt_gpu *h) { RAMLT_H(h->eng->init_chains()); }
+int ramlt_gpu_run(ramlt_gpu *h, uint64_t m) { RAMLT_H(h->eng->run(m)); }
+int ramlt_gpu_render(ramlt_gpu *h) { RAMLT_H(h->eng->render()); }
+int ramlt_gpu_synchronize(ramlt_gpu *h) { RAMLT_H(h->eng->synchronize()); }
+int ramlt_gpu_read_stats(ramlt_gpu *h, ramlt_stats *o) { RAMLT_H(h->eng->read_stats(o)); }
+int ramlt_gpu_read_film(ramlt_gpu *h, double *rgb, double *lum) { RAMLT_H(h->eng->read_film(rgb, lum)); }
+int ramlt_gpu_read_image(ramlt_gpu *h, float *rgb) { RAMLT_H(h->eng->read_image(rgb)); }
+int ramlt_gpu_read_tallies(ramlt_gpu *h, double *a, uint64_t *v, uint64_t cap, uint64_t *n) {
+    RAMLT_H(uint64_t m = h->eng->read_tallies(a, v, cap); if (n) *n = m);
+}
+int ramlt_gpu_read_regions(ramlt_gpu *h, double *l, uint64_t *nn, uint64_t cap, uint64_t *count) {
+    RAMLT_H(uint64_t m = h->eng->read_regions(l, nn, cap); if (count) *count = m);
+}
+int ramlt_gpu_read_trace(ramlt_gpu *h, ramlt_trace_row *rows, uint64_t cap, uint64_t *n) {
+    RAMLT_H(uint64_t m = h->eng->read_trace(rows, cap); if (n) *n = m);
+}
+int ramlt_gpu_read_metrics(ramlt_gpu *h, double *rows, uint64_t cap, uint64_t *n) {
+    RAMLT_H(uint64_t m = h->eng->read_metrics(rows, cap); if (n) *n = m);
+}
+int ramlt_gpu_read_decisions(ramlt_gpu *h, uint32_t K, double *a, uint8_t *f) {
+    RAMLT_H(h->eng->read_decisions(K, a, f));
+}
+int ramlt_gpu_read_partition(ramlt_gpu *h, char *buf, uint64_t cap) {
+    RAMLT_H(std::string s = h->eng->read_partition(); if (buf && cap) {
+        std::strncpy(buf, s.c_str(), cap - 1);
+        buf[cap - 1] = '\0';
+    });
+}
+int ramlt_gpu_set_stream(ramlt_gpu *h, void *stream) { RAMLT_H(h->eng->set_stream(stream)); }
+int ramlt_gpu_film_device(ramlt_gpu *h, double **film, uint64_t *n) { RAMLT_H(h->eng->film_device(film, n)); }
+int ramlt_gpu_adapt_exchange(ramlt_gpu *h, uint64_t **c, uint64_t **fx, uint64_t **last, uint64_t *n) {
+    RAMLT_H(h->eng->adapt_exchange(c, fx, last, n));
+}
+int ramlt_gpu_adapt_apply(ramlt_gpu *h) { RAMLT_H(h->eng->adapt_apply()); }
+int ramlt_gpu_set_exchange_interval(ramlt_gpu *h, uint32_t s) { RAMLT_H(h->eng->set_exchange_interval(s)); }
+
+const char *ramlt_gpu_last_error(ramlt_gpu *h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+void ramlt_gpu_destroy(ramlt_gpu *h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,1057 @@
+// engine_impl.cuh -- EngineT<R>: device memory, the span loop and the
+// barriers of run_render (core/driver.cpp:177-342) around the sm_100a kernels.
+#pragma once
+
+#include "engine.h"
+#include "ramlt_kernels.cuh"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <sstream>
+#include <vector>
+
+namespace ramlt_b200 {
+
+#define RAMLT_CUDA(x)                                                                              \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess)                                                                     \
+            throw CudaError(std::string("cuda: ") + cudaGetErrorString(e_) + " at " #x);           \
+    } while (0)
+
+template <class T> struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count)
+            RAMLT_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n)
+            RAMLT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void free() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { free(); }
+};
+
+template <class R> class EngineT final : public EngineBase {
+public:
+    EngineT(const HostScene &scene, const ramlt_render_desc &d);
+    ~EngineT() override;
+
+    void estimate_b(double *b, double *se) override;
+    void estimate_b_partials(uint64_t begin, uint64_t end, double *out) override;
+    void reduce_b(const double *partials, uint64_t n, double *b, double *se) override;
+    void set_b(double b) override {
+        b_ = b;
+        b_set_ = true;
+    }
+    void init_chains() override;
+    void run(uint64_t mutations) override;
+    void render() override;
+    void synchronize() override { RAMLT_CUDA(cudaStreamSynchronize(stream_)); }
+    void read_stats(ramlt_stats *out) override;
+    void read_film(double *rgb, double *lum) override;
+    void read_image(float *rgb) override;
+    uint64_t read_tallies(double *acc, uint64_t *vis, uint64_t cap) override;
+    uint64_t read_regions(double *lambda, uint64_t *n, uint64_t cap) override;
+    uint64_t read_trace(ramlt_trace_row *rows, uint64_t cap) override;
+    uint64_t read_metrics(double *rows, uint64_t cap) override;
+    void read_decisions(uint32_t K, double *a, uint8_t *flags) override;
+    std::string read_partition() override;
+    void set_stream(void *stream) override {
+        stream_ = static_cast<cudaStream_t>(stream);
+        own_stream_ = false;
+    }
+    void film_device(double **film, uint64_t *n) override {
+        fold();
+        *film = film64_.p;
+        *n = film64_.n;
+    }
+    void adapt_exchange(uint64_t **cnt, uint64_t **fx, uint64_t **last, uint64_t *n) override {
+        *cnt = reinterpret_cast<uint64_t *>(x_cnt_.p);
+        *fx = reinterpret_cast<uint64_t *>(x_fx_.p);
+        *last = reinterpret_cast<uint64_t *>(x_last_.p);
+        *n = static_cast<uint64_t>(n_regions_host_);
+    }
+    void adapt_apply() override;
+    void set_exchange_interval(uint32_t steps) override { exchange_interval_ = steps; }
+
+private:
+    rd::StepParams<R> params() const;
+    rd::RegionArrays regions() const;
+    rd::TraceBuf tracebuf() const;
+    rd::AdaptCfg adaptcfg() const;
+    void launch_step(int j0, int j1, unsigned long long span_start, unsigned long long per,
+                     unsigned long long rem, bool record);
+    void adapt_after_step(int j, unsigned long long span_start);
+    void refine();
+    void fold();
+    void flush_metrics(uint64_t at);
+    void check_err(const char *what);
+    void alloc_regions(size_t cap);
+    void grow_regions(size_t cap);
+    void reduce_chains(bool reset_interval, double out[6]);
+    void finalize_stats();
+
+    ramlt_render_desc d_;
+    HostScene hs_;
+    CameraBasis cb_;
+    int C_;
+    long long Ctot_, off_;
+    int G_;
+    int ctl_;      // 0 fixed, 1 global, 2 regional
+    int pkind_;    // partition kind (PartView::kind)
+    int adapt_;    // 0 literal, 1 pooled
+    size_t smem_;
+    cudaStream_t stream_ = nullptr;
+    bool own_stream_ = true;
+    uint32_t exchange_interval_ = 0;
+
+    // scene
+    DBuf<rd::TriD<R>> tri_;
+    DBuf<rd::SphD<R>> sph_;
+    DBuf<rd::MatD<R>> mat_;
+    DBuf<rd::V3<R>> emit_;
+    // chains
+    DBuf<rd::GV<R>> verts_;
+    DBuf<int> klen_;
+    DBuf<unsigned> smask_;
+    DBuf<R> cf_, cr_, eyeden_;
+    DBuf<unsigned long long> rng0_, rng1_;
+    DBuf<double> acc_, iacc_, lum_;
+    DBuf<unsigned long long> npert_, nlarge_, ipert_, nsteps_;
+    DBuf<double> log_a_;
+    DBuf<unsigned char> log_f_;
+    DBuf<int> vreg_;
+    DBuf<double> va_;
+    DBuf<int> err_;
+    DBuf<unsigned long long> rays_;
+    // film
+    DBuf<double> film64_;
+    DBuf<float4> film32_;
+    // adaptation / partition
+    size_t reg_cap_ = 0;
+    int n_regions_host_ = 0;
+    int n_nodes_host_ = 0;
+    int n_trees_ = 0;
+    DBuf<rd::KernTab<R>> ktab_;
+    DBuf<double> lambda_, pend_sum_, tot_acc_;
+    DBuf<unsigned long long> n_, pend_fx_, tot_vis_, tot_fx_, x_cnt_, x_fx_, x_last_, visits_;
+    DBuf<unsigned> pend_n_, x_touched_, touched_list_, n_touched_;
+    DBuf<rd::NodeD> nodes_;
+    DBuf<int> roots_, n_nodes_, n_regions_, scratch_cnt_, scratch_list_, splits_;
+    DBuf<unsigned long long> trace_count_, trace_index_, trace_n_;
+    DBuf<long long> trace_region_;
+    DBuf<double> trace_lambda_, trace_alpha_;
+    DBuf<double> red_;
+    // host state
+    double b_ = 0.0, b_se_ = 0.0;
+    uint64_t b_n_ = 0;
+    bool b_set_ = false, chains_ready_ = false;
+    uint64_t done_ = 0, next_refine_, next_metrics_;
+    std::vector<std::array<double, 4>> metrics_;
+    std::chrono::steady_clock::time_point t0_;
+    bool t0_set_ = false;
+    uint64_t launches_ = 0;
+    uint64_t steps_since_fold_ = 0;
+    ramlt_stats final_{};
+    bool finalized_ = false;
+};
+
+// ---------------------------------------------------------------------------------------
+template <class R> static rd::V3<R> v3c(const double *p) {
+    return rd::V3<R>{static_cast<R>(p[0]), static_cast<R>(p[1]), static_cast<R>(p[2])};
+}
+
+template <class R>
+EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d), hs_(scene) {
+    if (d.chains < 1)
+        throw std::logic_error("need at least one chain");
+    if (d.width < 1 || d.height < 1)
+        throw std::logic_error("resolution must be positive");
+    if (d.max_vertices < 2)
+        throw std::logic_error("max_vertices must be at least 2");
+    if (d.max_vertices > rd::kMaxV)
+        throw std::invalid_argument("max_vertices exceeds the engine's path capacity (" +
+                                    std::to_string(rd::kMaxV) + ")");
+    if (d.batch_size < 1)
+        throw std::logic_error("batch_size must be >= 1");
+    if (hs_.emit.size() / 3 >= 4095 || hs_.mats.size() >= 65535)
+        throw std::invalid_argument("too many emitters or materials for the vertex encoding");
+    if (d.device >= 0)
+        RAMLT_CUDA(cudaSetDevice(d.device));
+    RAMLT_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+    C_ = d.chains;
+    Ctot_ = d.chains_total > 0 ? d.chains_total : d.chains;
+    off_ = d.chain_offset;
+    if (off_ < 0 || off_ + C_ > Ctot_)
+        throw std::logic_error("chain shard outside [0, chains_total)");
+    G_ = d.lanes_per_chain;
+    if (G_ <= 0)
+        G_ = C_ <= 8192 ? 32 : 1;
+    if (G_ != 1 && G_ != 2 && G_ != 4 && G_ != 8 && G_ != 16 && G_ != 32)
+        throw std::invalid_argument("lanes_per_chain must be a power of two <= 32");
+    ctl_ = d.strategy == RAMLT_FIXED ? 0 : (d.strategy == RAMLT_GLOBAL ? 1 : 2);
+    pkind_ = 0;
+    if (ctl_ == 2)
+        pkind_ = d.strategy == RAMLT_RA_GRID ? (d.perturbation == RAMLT_LENS ? 1 : 3)
+                                             : (d.perturbation == RAMLT_LENS ? 2 : 4);
+    adapt_ = d.adapt_mode;
+    if (adapt_ < 0)
+        adapt_ = Ctot_ <= 4096 ? 0 : 1;
+    if (Ctot_ != C_ && ctl_ != 0)
+        adapt_ = 1;   // sharded adaptive runs use the pooled rule (G-invariant)
+    next_refine_ = d.m_refine;
+    next_metrics_ = d.metrics_interval;
+
+    // camera (core/driver.cpp:181 -> camera.cpp:22-30)
+    cb_ = make_camera(hs_.cam, d.width, d.height);
+
+    // scene upload
+    std::vector<rd::TriD<R>> tris(hs_.tri.size());
+    for (size_t i = 0; i < hs_.tri.size(); ++i) {
+        const ramlt_triangle &t = hs_.tri[i];
+        double e1[3] = {t.b[0] - t.a[0], t.b[1] - t.a[1], t.b[2] - t.a[2]};
+        double e2[3] = {t.c[0] - t.a[0], t.c[1] - t.a[1], t.c[2] - t.a[2]};
+        double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                        e1[0] * e2[1] - e1[1] * e2[0]};
+        double l = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+        double n[3] = {cr[0] / l, cr[1] / l, cr[2] / l};
+        tris[i].a = v3c<R>(t.a);
+        tris[i].e1 = v3c<R>(e1);
+        tris[i].e2 = v3c<R>(e2);
+        tris[i].n = v3c<R>(n);
+        tris[i].mat = t.material;
+        tris[i].emi = t.emitter;
+    }
+    std::vector<rd::SphD<R>> sphs(hs_.sph.size());
+    for (size_t i = 0; i < hs_.sph.size(); ++i) {
+        sphs[i].c = v3c<R>(hs_.sph[i].center);
+        sphs[i].r = static_cast<R>(hs_.sph[i].radius);
+        sphs[i].mat = hs_.sph[i].material;
+        sphs[i].emi = hs_.sph[i].emitter;
+    }
+    std::vector<rd::MatD<R>> mats(hs_.mats.size());
+    for (size_t i = 0; i < hs_.mats.size(); ++i) {
+        mats[i].kind = hs_.mats[i].kind;
+        mats[i].albedo = v3c<R>(hs_.mats[i].albedo);
+        mats[i].ior = static_cast<R>(hs_.mats[i].ior);
+        mats[i].expo = static_cast<R>(hs_.mats[i].exponent);
+    }
+    std::vector<rd::V3<R>> emit(hs_.emit.size() / 3);
+    for (size_t i = 0; i < emit.size(); ++i)
+        emit[i] = v3c<R>(&hs_.emit[3 * i]);
+    tri_.alloc(std::max<size_t>(tris.size(), 1));
+    sph_.alloc(std::max<size_t>(sphs.size(), 1));
+    mat_.alloc(std::max<size_t>(mats.size(), 1));
+    emit_.alloc(std::max<size_t>(emit.size(), 1));
+    if (!tris.empty())
+        RAMLT_CUDA(cudaMemcpy(tri_.p, tris.data(), tris.size() * sizeof(tris[0]), cudaMemcpyHostToDevice));
+    if (!sphs.empty())
+        RAMLT_CUDA(cudaMemcpy(sph_.p, sphs.data(), sphs.size() * sizeof(sphs[0]), cudaMemcpyHostToDevice));
+    if (!mats.empty())
+        RAMLT_CUDA(cudaMemcpy(mat_.p, mats.data(), mats.size() * sizeof(mats[0]), cudaMemcpyHostToDevice));
+    if (!emit.empty())
+        RAMLT_CUDA(cudaMemcpy(emit_.p, emit.data(), emit.size() * sizeof(emit[0]), cudaMemcpyHostToDevice));
+    smem_ = ((sphs.size() * sizeof(rd::SphD<R>) + 15) & ~size_t(15)) + tris.size() * sizeof(rd::TriD<R>);
+    if (smem_ > 200 * 1024)
+        throw std::invalid_argument("scene too large for the shared-memory primitive path (" +
+                                    std::to_string(hs_.tri.size()) + " triangles)");
+
+    // chain state
+    size_t C = static_cast<size_t>(C_);
+    verts_.alloc(C * static_cast<size_t>(d.max_vertices - 1));
+    klen_.alloc(C);
+    smask_.alloc(C);
+    cf_.alloc(4 * C);
+    cr_.alloc(2 * C);
+    eyeden_.alloc(C);
+    rng0_.alloc(C);
+    rng1_.alloc(C);
+    acc_.alloc(C);
+    iacc_.alloc(C);
+    lum_.alloc(C);
+    npert_.alloc(C);
+    nlarge_.alloc(C);
+    ipert_.alloc(C);
+    nsteps_.alloc(C);
+    if (d.log_steps) {
+        log_a_.alloc(C * d.log_steps);
+        log_f_.alloc(C * d.log_steps);
+        log_a_.zero(stream_);
+        log_f_.zero(stream_);
+    }
+    vreg_.alloc(C);
+    va_.alloc(C);
+    err_.alloc(4);
+    err_.zero(stream_);
+    rays_.alloc(2);
+    rays_.zero(stream_);
+    size_t npix = static_cast<size_t>(d.width) * d.height;
+    film64_.alloc(npix * 3);
+    film64_.zero(stream_);
+    if (sizeof(R) == 4) {
+        film32_.alloc(npix);
+        film32_.zero(stream_);
+    }
+    red_.alloc(6 * ((C + 255) / 256));
+
+    // controller + partition (core/driver.cpp:190-212)
+    size_t initial = 1;
+    if (pkind_ == 1)
+        initial = static_cast<size_t>(d.n_top) * d.n_top;
+    else if (pkind_ == 3)
+        initial = static_cast<size_t>(d.n_top) * d.n_top * d.n_bottom * d.n_bottom;
+    else if (pkind_ == 4)
+        initial = static_cast<size_t>(d.n_top) * d.n_top;
+    size_t cap = initial;
+    if (pkind_ == 2 || pkind_ == 4)
+        cap = std::max<size_t>(d.region_capacity ? d.region_capacity : 4096, initial * 8);
+    alloc_regions(cap);
+    n_regions_host_ = static_cast<int>(initial);
+    {
+        std::vector<double> lam(initial, d.lambda_init);
+        std::vector<unsigned long long> one(initial, 1ull);
+        RAMLT_CUDA(cudaMemcpy(lambda_.p, lam.data(), initial * sizeof(double), cudaMemcpyHostToDevice));
+        RAMLT_CUDA(cudaMemcpy(n_.p, one.data(), initial * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+        rd::k_ktab_init<R><<<static_cast<unsigned>((initial + 255) / 256), 256, 0, stream_>>>(
+            ktab_.p, lambda_.p, static_cast<int>(initial), d.sigma2_ratio);
+        ++launches_;
+        RAMLT_CUDA(cudaGetLastError());
+    }
+    if (pkind_ == 2 || pkind_ == 4) {
+        n_trees_ = pkind_ == 2 ? 1 : d.n_top * d.n_top;
+        std::vector<rd::NodeD> nodes(n_trees_);
+        std::vector<int> roots(n_trees_);
+        for (int t = 0; t < n_trees_; ++t) {
+            nodes[t] = rd::NodeD{0, 0, 0, -1, t, t};
+            roots[t] = t;
+        }
+        RAMLT_CUDA(cudaMemcpy(nodes_.p, nodes.data(), nodes.size() * sizeof(rd::NodeD), cudaMemcpyHostToDevice));
+        roots_.alloc(n_trees_);
+        RAMLT_CUDA(cudaMemcpy(roots_.p, roots.data(), roots.size() * sizeof(int), cudaMemcpyHostToDevice));
+        n_nodes_host_ = n_trees_;
+        n_nodes_.alloc(1);
+        n_regions_.alloc(1);
+        RAMLT_CUDA(cudaMemcpy(n_nodes_.p, &n_nodes_host_, sizeof(int), cudaMemcpyHostToDevice));
+        RAMLT_CUDA(cudaMemcpy(n_regions_.p, &n_regions_host_, sizeof(int), cudaMemcpyHostToDevice));
+        scratch_cnt_.alloc(n_trees_);
+        splits_.alloc(1);
+    }
+    size_t tcap = d.trace_enabled ? (d.trace_capacity ? d.trace_capacity : (1u << 20)) : 0;
+    trace_count_.alloc(1);
+    trace_count_.zero(stream_);
+    if (tcap) {
+        trace_index_.alloc(tcap);
+        trace_n_.alloc(tcap);
+        trace_region_.alloc(tcap);
+        trace_lambda_.alloc(tcap);
+        trace_alpha_.alloc(tcap);
+    }
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+}
+
+template <class R> EngineT<R>::~EngineT() {
+    if (stream_ && own_stream_) {
+        cudaStreamSynchronize(stream_);
+        cudaStreamDestroy(stream_);
+    }
+}
+
+template <class R> void EngineT<R>::alloc_regions(size_t cap) {
+    reg_cap_ = cap;
+    ktab_.alloc(cap);
+    lambda_.alloc(cap);
+    pend_sum_.alloc(cap);
+    tot_acc_.alloc(cap);
+    n_.alloc(cap);
+    pend_fx_.alloc(cap);
+    tot_vis_.alloc(cap);
+    tot_fx_.alloc(cap);
+    x_cnt_.alloc(cap);
+    x_fx_.alloc(cap);
+    x_last_.alloc(cap);
+    visits_.alloc(cap);
+    pend_n_.alloc(cap);
+    x_touched_.alloc(cap);
+    touched_list_.alloc(cap);
+    n_touched_.alloc(1);
+    for (auto *b : {&pend_sum_, &tot_acc_})
+        b->zero(stream_);
+    for (auto *b : {&pend_fx_, &tot_vis_, &tot_fx_, &x_cnt_, &x_fx_, &x_last_, &visits_})
+        b->zero(stream_);
+    pend_n_.zero(stream_);
+    x_touched_.zero(stream_);
+    n_touched_.zero(stream_);
+    if (pkind_ == 2 || pkind_ == 4) {
+        nodes_.alloc(cap + 4);
+        scratch_list_.alloc(cap + 4);
+    }
+}
+
+template <class T> static void grow_buf(DBuf<T> &b, size_t cap, size_t used, cudaStream_t s) {
+    DBuf<T> nb;
+    nb.alloc(cap);
+    nb.zero(s);
+    if (used)
+        RAMLT_CUDA(cudaMemcpyAsync(nb.p, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    RAMLT_CUDA(cudaStreamSynchronize(s));
+    b.free();
+    b.p = nb.p;
+    b.n = nb.n;
+    nb.p = nullptr;
+    nb.n = 0;
+}
+
+template <class R> void EngineT<R>::grow_regions(size_t cap) {
+    size_t used = static_cast<size_t>(n_regions_host_);
+    grow_buf(ktab_, cap, used, stream_);
+    grow_buf(lambda_, cap, used, stream_);
+    grow_buf(pend_sum_, cap, used, stream_);
+    grow_buf(tot_acc_, cap, used, stream_);
+    grow_buf(n_, cap, used, stream_);
+    grow_buf(pend_fx_, cap, used, stream_);
+    grow_buf(tot_vis_, cap, used, stream_);
+    grow_buf(tot_fx_, cap, used, stream_);
+    grow_buf(x_cnt_, cap, used, stream_);
+    grow_buf(x_fx_, cap, used, stream_);
+    grow_buf(x_last_, cap, used, stream_);
+    grow_buf(visits_, cap, used, stream_);
+    grow_buf(pend_n_, cap, used, stream_);
+    grow_buf(x_touched_, cap, used, stream_);
+    grow_buf(touched_list_, cap, 0, stream_);
+    grow_buf(nodes_, cap + 4, static_cast<size_t>(n_nodes_host_), stream_);
+    grow_buf(scratch_list_, cap + 4, 0, stream_);
+    reg_cap_ = cap;
+}
+
+template <class R> rd::StepParams<R> EngineT<R>::params() const {
+    rd::StepParams<R> P{};
+    P.scene.tri = tri_.p;
+    P.scene.sph = sph_.p;
+    P.scene.mat = mat_.p;
+    P.scene.emit = emit_.p;
+    P.scene.ntri = static_cast<int>(hs_.tri.size());
+    P.scene.nsph = static_cast<int>(hs_.sph.size());
+    P.scene.cam.pos = v3c<R>(cb_.pos);
+    P.scene.cam.right = v3c<R>(cb_.right);
+    P.scene.cam.up = v3c<R>(cb_.up);
+    P.scene.cam.fwd = v3c<R>(cb_.fwd);
+    P.scene.cam.tanh = static_cast<R>(cb_.tanh);
+    P.scene.cam.aspect = static_cast<R>(cb_.aspect);
+    P.scene.cam.area = static_cast<R>(cb_.area);
+    P.scene.cam.sensor = static_cast<R>(cb_.sensor);
+    P.C = C_;
+    P.C_total = Ctot_;
+    P.chain_off = off_;
+    P.maxv = d_.max_vertices;
+    P.pk = d_.perturbation;
+    P.ctl = ctl_;
+    P.W = d_.width;
+    P.H = d_.height;
+    P.seed = d_.seed;
+    P.ch.verts = verts_.p;
+    P.ch.klen = klen_.p;
+    P.ch.smask = smask_.p;
+    P.ch.cf = cf_.p;
+    P.ch.cr = cr_.p;
+    P.ch.eyeden = eyeden_.p;
+    P.ch.rng0 = rng0_.p;
+    P.ch.rng1 = rng1_.p;
+    P.ch.acc = acc_.p;
+    P.ch.iacc = iacc_.p;
+    P.ch.lum = lum_.p;
+    P.ch.npert = npert_.p;
+    P.ch.nlarge = nlarge_.p;
+    P.ch.ipert = ipert_.p;
+    P.ch.nsteps = nsteps_.p;
+    P.ch.log_a = log_a_.p;
+    P.ch.log_f = log_f_.p;
+    P.ch.log_K = d_.log_steps;
+    P.ch.vreg = vreg_.p;
+    P.ch.va = va_.p;
+    P.ch.err = err_.p;
+    P.ch.rays = rays_.p;
+    P.part.kind = pkind_;
+    P.part.ntop = d_.n_top;
+    P.part.nbot = d_.n_bottom;
+    P.part.nodes = nodes_.p;
+    P.part.roots = roots_.p;
+    P.part.visits = visits_.p;
+    P.ktab = ktab_.p;
+    P.film64 = film64_.p;
+    P.film32 = film32_.p;
+    P.reg = regions();
+    return P;
+}
+
+template <class R> rd::RegionArrays EngineT<R>::regions() const {
+    rd::RegionArrays ra;
+    ra.lambda = lambda_.p;
+    ra.n = n_.p;
+    ra.pend_n = pend_n_.p;
+    ra.pend_sum = pend_sum_.p;
+    ra.pend_fx = pend_fx_.p;
+    ra.tot_vis = tot_vis_.p;
+    ra.tot_acc = tot_acc_.p;
+    ra.tot_fx = tot_fx_.p;
+    ra.x_cnt = x_cnt_.p;
+    ra.x_fx = x_fx_.p;
+    ra.x_last = x_last_.p;
+    ra.x_touched = x_touched_.p;
+    ra.touched_list = touched_list_.p;
+    ra.n_touched = n_touched_.p;
+    return ra;
+}
+
+template <class R> rd::TraceBuf EngineT<R>::tracebuf() const {
+    rd::TraceBuf t;
+    t.count = trace_count_.p;
+    t.cap = trace_index_.n;
+    t.index = trace_index_.p;
+    t.region = trace_region_.p;
+    t.n = trace_n_.p;
+    t.lambda = trace_lambda_.p;
+    t.alpha = trace_alpha_.p;
+    return t;
+}
+
+template <class R> rd::AdaptCfg EngineT<R>::adaptcfg() const {
+    rd::AdaptCfg a;
+    a.L = d_.batch_size;
+    a.gmax = d_.gamma_max;
+    a.gscale = d_.gamma_scale;
+    a.target = d_.target_acceptance;
+    a.lmin = d_.lambda_min;
+    a.ratio = d_.sigma2_ratio;
+    a.trace = d_.trace_enabled && trace_index_.n > 0;
+    return a;
+}
+
+template <class R> void EngineT<R>::check_err(const char *what) {
+    int e[4];
+    RAMLT_CUDA(cudaMemcpyAsync(e, err_.p, sizeof(e), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    if (e[0] == 1)
+        throw std::runtime_error("black-scene: could not find an initial path");
+    if (e[0] == 2)
+        throw std::runtime_error(std::string("region capacity exceeded in ") + what);
+}
+
+template <class R> void EngineT<R>::estimate_b_partials(uint64_t begin, uint64_t end, double *out) {
+    if (d_.b_samples < 1)
+        throw std::logic_error("estimate_b needs at least one sample");
+    uint64_t S = std::min<uint64_t>(d_.b_samples, d_.b_substreams ? d_.b_substreams : 65536);
+    if (end > S || begin > end)
+        throw std::logic_error("substream range outside [0, b_substreams)");
+    DBuf<double> part;
+    part.alloc(2 * std::max<uint64_t>(end - begin, 1));
+    rd::StepParams<R> P = params();
+    unsigned blocks = static_cast<unsigned>((end - begin + 127) / 128);
+    if (end > begin) {
+        auto kern = d_.rng == RAMLT_RNG_PHILOX ? rd::k_bsub<R, rd::RNG_PHILOX> : rd::k_bsub<R, rd::RNG_PCG>;
+        RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+        kern<<<blocks, 128, smem_, stream_>>>(P, d_.b_samples, S, begin, end, part.p);
+        ++launches_;
+        RAMLT_CUDA(cudaGetLastError());
+        RAMLT_CUDA(cudaMemcpyAsync(out, part.p, 2 * (end - begin) * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    }
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+}
+
+template <class R> void EngineT<R>::reduce_b(const double *partials, uint64_t n, double *b, double *se) {
+    // fixed substream order (oracle/ramlt_oracle.cpp mirrors it)
+    double sum = 0.0, sq = 0.0;
+    for (uint64_t s = 0; s < n; ++s) {
+        sum += partials[2 * s];
+        sq += partials[2 * s + 1];
+    }
+    double nn = static_cast<double>(d_.b_samples);
+    double mean = sum / nn;
+    if (mean <= 0.0)
+        throw std::runtime_error("black-scene: no sample carried any contribution");
+    double var = d_.b_samples > 1 ? std::max(0.0, (sq - nn * mean * mean) / (nn - 1.0)) : 0.0;
+    b_ = mean;
+    b_se_ = std::sqrt(var / nn);
+    b_n_ = d_.b_samples;
+    b_set_ = true;
+    if (b)
+        *b = b_;
+    if (se)
+        *se = b_se_;
+}
+
+template <class R> void EngineT<R>::estimate_b(double *b, double *se) {
+    uint64_t S = std::min<uint64_t>(d_.b_samples, d_.b_substreams ? d_.b_substreams : 65536);
+    std::vector<double> part(2 * S);
+    estimate_b_partials(0, S, part.data());
+    reduce_b(part.data(), S, b, se);
+}
+
+template <class R> void EngineT<R>::init_chains() {
+    rd::StepParams<R> P = params();
+    auto kern = d_.rng == RAMLT_RNG_PHILOX ? rd::k_init<R, rd::RNG_PHILOX> : rd::k_init<R, rd::RNG_PCG>;
+    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+    kern<<<static_cast<unsigned>((C_ + 127) / 128), 128, smem_, stream_>>>(P, 50000000ull);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    check_err("init");
+    chains_ready_ = true;
+}
+
+template <class R>
+void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsigned long long per,
+                             unsigned long long rem, bool record) {
+    rd::StepParams<R> P = params();
+    P.span_start = span_start;
+    P.per = per;
+    P.rem = rem;
+    P.j0 = j0;
+    P.j1 = j1;
+    P.record_visits = record ? 1 : 0;
+    const long long threads = static_cast<long long>(C_) * G_;
+    const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
+    void (*kern)(rd::StepParams<R>) = nullptr;
+#define RAMLT_PICK(RK)                                                                              \
+    switch (G_) {                                                                                   \
+    case 1: kern = rd::k_step<R, RK, 1>; break;                                                     \
+    case 2: kern = rd::k_step<R, RK, 2>; break;                                                     \
+    case 4: kern = rd::k_step<R, RK, 4>; break;                                                     \
+    case 8: kern = rd::k_step<R, RK, 8>; break;                                                     \
+    case 16: kern = rd::k_step<R, RK, 16>; break;                                                   \
+    default: kern = rd::k_step<R, RK, 32>; break;                                                   \
+    }
+    if (d_.rng == RAMLT_RNG_PHILOX) {
+        RAMLT_PICK(rd::RNG_PHILOX)
+    } else {
+        RAMLT_PICK(rd::RNG_PCG)
+    }
+#undef RAMLT_PICK
+    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+    kern<<<blocks, 128, smem_, stream_>>>(P);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+}
+
+template <class R> void EngineT<R>::adapt_after_step(int j, unsigned long long span_start) {
+    if (ctl_ == 0)
+        return;
+    rd::RegionArrays ra = regions();
+    if (adapt_ == 0) {
+        rd::k_adapt_literal<R><<<1, 1024, 0, stream_>>>(vreg_.p, va_.p, C_, off_, Ctot_, span_start, j, ra,
+                                                         ktab_.p, adaptcfg(), tracebuf());
+        ++launches_;
+    } else {
+        rd::k_adapt_pool_accum<<<static_cast<unsigned>((C_ + 255) / 256), 256, 0, stream_>>>(
+            vreg_.p, va_.p, C_, off_, Ctot_, span_start, j, ra);
+        ++launches_;
+        if (!exchange_interval_)
+            adapt_apply();
+    }
+    RAMLT_CUDA(cudaGetLastError());
+}
+
+template <class R> void EngineT<R>::adapt_apply() {
+    if (ctl_ == 0 || adapt_ != 1)
+        return;
+    rd::RegionArrays ra = regions();
+    rd::k_adapt_pool_apply<R><<<148, 256, 0, stream_>>>(ra, ktab_.p, adaptcfg(), tracebuf());
+    rd::k_reset_touched<<<1, 1, 0, stream_>>>(n_touched_.p);
+    launches_ += 2;
+    RAMLT_CUDA(cudaGetLastError());
+}
+
+template <class R> void EngineT<R>::refine() {
+    if (pkind_ != 2 && pkind_ != 4)
+        return;
+    // worst case every current region splits: keep capacity ahead of it
+    size_t need = static_cast<size_t>(n_regions_host_) * 5 + 8;
+    if (need > reg_cap_)
+        grow_regions(std::max(need, reg_cap_ * 2));
+    rd::RegionArrays ra = regions();
+    rd::k_refine<R><<<1, 1, 0, stream_>>>(nodes_.p, n_nodes_.p, static_cast<int>(reg_cap_ + 4), n_trees_,
+                                          scratch_cnt_.p, scratch_list_.p, ra, ktab_.p, visits_.p,
+                                          n_regions_.p, static_cast<int>(reg_cap_), d_.m_split, err_.p,
+                                          splits_.p);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    RAMLT_CUDA(cudaMemcpyAsync(&n_regions_host_, n_regions_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaMemcpyAsync(&n_nodes_host_, n_nodes_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+    check_err("refine");
+}
+
+template <class R> void EngineT<R>::fold() {
+    if (sizeof(R) != 4)
+        return;
+    int npix = d_.width * d_.height;
+    rd::k_fold_film<<<static_cast<unsigned>((npix + 255) / 256), 256, 0, stream_>>>(film32_.p, film64_.p, npix);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    steps_since_fold_ = 0;
+}
+
+template <class R> void EngineT<R>::reduce_chains(bool reset_interval, double out[6]) {
+    unsigned blocks = static_cast<unsigned>((C_ + 255) / 256);
+    rd::k_reduce_chains<<<blocks, 256, 0, stream_>>>(acc_.p, iacc_.p, lum_.p, npert_.p, nlarge_.p, ipert_.p, C_,
+                                                     reset_interval ? 1 : 0, red_.p);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    std::vector<double> h(6 * blocks);
+    RAMLT_CUDA(cudaMemcpyAsync(h.data(), red_.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    for (int q = 0; q < 6; ++q)
+        out[q] = 0.0;
+    for (unsigned b = 0; b < blocks; ++b)
+        for (int q = 0; q < 6; ++q)
+            out[q] += h[6 * b + q];
+}
+
+template <class R> void EngineT<R>::flush_metrics(uint64_t at) {
+    double r[6];
+    reduce_chains(true, r);
+    double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+    metrics_.push_back({t, static_cast<double>(at), std::numeric_limits<double>::quiet_NaN(),
+                        r[5] > 0 ? r[1] / r[5] : 0.0});
+}
+
+template <class R> void EngineT<R>::run(uint64_t mutations) {
+    if (!chains_ready_)
+        throw std::logic_error("run before init_chains");
+    if (!t0_set_) {
+        RAMLT_CUDA(cudaStreamSynchronize(stream_));
+        t0_ = std::chrono::steady_clock::now();
+        t0_set_ = true;
+    }
+    finalized_ = false;
+    const uint64_t target = done_ + mutations;
+    const uint32_t fuse = d_.steps_per_launch ? d_.steps_per_launch : 256;
+    while (done_ < target) {
+        uint64_t boundary = std::min({target, next_refine_, next_metrics_});
+        uint64_t span = boundary - done_;
+        unsigned long long per = span / static_cast<uint64_t>(Ctot_);
+        unsigned long long rem = span % static_cast<uint64_t>(Ctot_);
+        int steps = static_cast<int>(per + (rem ? 1 : 0));
+        if (ctl_ == 0) {
+            for (int j = 0; j < steps; j += static_cast<int>(fuse)) {
+                int j1 = std::min(steps, j + static_cast<int>(fuse));
+                launch_step(j, j1, done_, per, rem, false);
+                steps_since_fold_ += static_cast<uint64_t>(j1 - j);
+                if (sizeof(R) == 4 && steps_since_fold_ >= 4096)
+                    fold();
+            }
+        } else {
+            for (int j = 0; j < steps; ++j) {
+                launch_step(j, j + 1, done_, per, rem, true);
+                adapt_after_step(j, done_);
+                if (sizeof(R) == 4 && ++steps_since_fold_ >= 4096)
+                    fold();
+            }
+        }
+        done_ += span;
+        if (done_ == next_refine_) {
+            refine();
+            next_refine_ += d_.m_refine;
+        }
+        if (done_ == next_metrics_ || done_ == d_.mutations) {
+            flush_metrics(done_);
+            next_metrics_ = done_ + d_.metrics_interval;
+        }
+    }
+    fold();
+}
+
+template <class R> void EngineT<R>::render() {
+    if (!b_set_)
+        estimate_b(nullptr, nullptr);
+    if (!chains_ready_)
+        init_chains();
+    if (d_.time_budget_s > 0.0) {
+        if (!t0_set_) {
+            RAMLT_CUDA(cudaStreamSynchronize(stream_));
+            t0_ = std::chrono::steady_clock::now();
+            t0_set_ = true;
+        }
+        for (;;) {
+            run(std::min<uint64_t>(d_.metrics_interval, next_metrics_ - done_));
+            RAMLT_CUDA(cudaStreamSynchronize(stream_));
+            double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+            if (t >= d_.time_budget_s)
+                break;
+        }
+    } else {
+        run(d_.mutations - std::min(d_.mutations, done_));
+    }
+    finalize_stats();
+}
+
+template <class R> void EngineT<R>::finalize_stats() {
+    if (metrics_.empty() || static_cast<uint64_t>(metrics_.back()[1]) != done_) {
+        if (!t0_set_) {
+            t0_ = std::chrono::steady_clock::now();
+            t0_set_ = true;
+        }
+        flush_metrics(done_);
+    }
+    double r[6];
+    reduce_chains(false, r);
+    ramlt_stats s{};
+    s.b = b_;
+    s.b_stderr = b_se_;
+    s.b_samples = b_n_;
+    s.total_mutations = done_;
+    s.perturbation_proposals = static_cast<uint64_t>(r[3]);
+    s.large_step_proposals = static_cast<uint64_t>(r[4]);
+    s.mean_acceptance = r[3] > 0 ? r[0] / r[3] : 0.0;
+    s.film_luminance = r[2];
+    s.loop_time_s = metrics_.empty() ? 0.0 : metrics_.back()[0];
+    final_ = s;
+    finalized_ = true;
+}
+
+template <class R> void EngineT<R>::read_stats(ramlt_stats *out) {
+    if (!finalized_)
+        finalize_stats();
+    ramlt_stats s = final_;
+    unsigned long long rays[2];
+    RAMLT_CUDA(cudaMemcpyAsync(rays, rays_.p, sizeof(rays), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    s.rays_closest = rays[0];
+    s.rays_visibility = rays[1];
+    std::vector<double> acc(n_regions_host_);
+    std::vector<uint64_t> vis(n_regions_host_);
+    uint64_t nt = read_tallies(acc.data(), vis.data(), acc.size());
+    // global_acceptance_identity (core/adaptation.cpp:103-125)
+    double tot = 0.0, comp = 0.0;
+    uint64_t tv = 0;
+    for (uint64_t i = 0; i < nt; ++i) {
+        double y = acc[i] - comp;
+        double sm = tot + y;
+        comp = (sm - tot) - y;
+        tot = sm;
+        tv += vis[i];
+    }
+    s.identity_residual = 0.0;
+    if (tv > 0) {
+        double pooled = tot / static_cast<double>(tv);
+        double w = 0.0;
+        for (uint64_t i = 0; i < nt; ++i) {
+            if (!vis[i])
+                continue;
+            w += (static_cast<double>(vis[i]) / static_cast<double>(tv)) * (acc[i] / static_cast<double>(vis[i]));
+        }
+        s.identity_residual = std::abs(pooled - w);
+    }
+    s.n_tallies = nt;
+    // region_count: partition leaves (partition.hpp:33) or controller regions
+    if (pkind_ == 2 || pkind_ == 4) {
+        std::vector<rd::NodeD> nodes(n_nodes_host_);
+        RAMLT_CUDA(cudaMemcpy(nodes.data(), nodes_.p, nodes.size() * sizeof(rd::NodeD), cudaMemcpyDeviceToHost));
+        uint64_t leaves = 0;
+        for (auto &nd : nodes)
+            leaves += nd.child < 0;
+        s.region_count = leaves;
+    } else {
+        s.region_count = static_cast<uint64_t>(n_regions_host_);
+    }
+    unsigned long long tc = 0;
+    RAMLT_CUDA(cudaMemcpy(&tc, trace_count_.p, sizeof(tc), cudaMemcpyDeviceToHost));
+    s.n_trace = std::min<uint64_t>(tc, trace_index_.n);
+    s.n_metrics = metrics_.size();
+    s.kernel_launches = launches_;
+    *out = s;
+}
+
+template <class R> void EngineT<R>::read_film(double *rgb, double *lum) {
+    fold();
+    if (rgb)
+        RAMLT_CUDA(cudaMemcpyAsync(rgb, film64_.p, film64_.n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    if (lum) {
+        double r[6];
+        reduce_chains(false, r);
+        *lum = r[2];
+    }
+}
+
+template <class R> void EngineT<R>::read_image(float *rgb) {
+    fold();
+    DBuf<float> img;
+    img.alloc(film64_.n);
+    double scale = done_ > 0 ? b_ / static_cast<double>(done_) : 0.0;
+    rd::k_to_image<<<static_cast<unsigned>((film64_.n + 255) / 256), 256, 0, stream_>>>(
+        film64_.p, img.p, static_cast<int>(film64_.n), scale);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    RAMLT_CUDA(cudaMemcpyAsync(rgb, img.p, film64_.n * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+}
+
+template <class R> uint64_t EngineT<R>::read_tallies(double *acc, uint64_t *vis, uint64_t cap) {
+    // Fixed controllers never record (adaptation.cpp:63-64): one all-zero tally.
+    uint64_t n = static_cast<uint64_t>(n_regions_host_);
+    uint64_t m = std::min(n, cap);
+    std::vector<double> ta(n);
+    std::vector<unsigned long long> tv(n), tf(n);
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    RAMLT_CUDA(cudaMemcpy(ta.data(), tot_acc_.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    RAMLT_CUDA(cudaMemcpy(tv.data(), tot_vis_.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    RAMLT_CUDA(cudaMemcpy(tf.data(), tot_fx_.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < m; ++i) {
+        if (acc)
+            acc[i] = adapt_ == 1 ? static_cast<double>(tf[i]) / 16777216.0 : ta[i];
+        if (vis)
+            vis[i] = tv[i];
+    }
+    return n;
+}
+
+template <class R> uint64_t EngineT<R>::read_regions(double *lambda, uint64_t *n, uint64_t cap) {
+    uint64_t cnt = static_cast<uint64_t>(n_regions_host_);
+    uint64_t m = std::min(cnt, cap);
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    if (lambda && m)
+        RAMLT_CUDA(cudaMemcpy(lambda, lambda_.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (n && m)
+        RAMLT_CUDA(cudaMemcpy(n, n_.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return cnt;
+}
+
+template <class R> uint64_t EngineT<R>::read_trace(ramlt_trace_row *rows, uint64_t cap) {
+    unsigned long long tc = 0;
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    RAMLT_CUDA(cudaMemcpy(&tc, trace_count_.p, sizeof(tc), cudaMemcpyDeviceToHost));
+    uint64_t n = std::min<uint64_t>(tc, trace_index_.n);
+    std::vector<unsigned long long> idx(n), nn(n);
+    std::vector<long long> reg(n);
+    std::vector<double> lam(n), al(n);
+    if (n) {
+        RAMLT_CUDA(cudaMemcpy(idx.data(), trace_index_.p, n * 8, cudaMemcpyDeviceToHost));
+        RAMLT_CUDA(cudaMemcpy(nn.data(), trace_n_.p, n * 8, cudaMemcpyDeviceToHost));
+        RAMLT_CUDA(cudaMemcpy(reg.data(), trace_region_.p, n * 8, cudaMemcpyDeviceToHost));
+        RAMLT_CUDA(cudaMemcpy(lam.data(), trace_lambda_.p, n * 8, cudaMemcpyDeviceToHost));
+        RAMLT_CUDA(cudaMemcpy(al.data(), trace_alpha_.p, n * 8, cudaMemcpyDeviceToHost));
+    }
+    // device appends are unordered across regions: restore (index, region, n) order
+    std::vector<size_t> ord(n);
+    for (size_t i = 0; i < n; ++i)
+        ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+        if (idx[a] != idx[b])
+            return idx[a] < idx[b];
+        if (reg[a] != reg[b])
+            return reg[a] < reg[b];
+        return nn[a] < nn[b];
+    });
+    uint64_t m = std::min(n, cap);
+    for (uint64_t i = 0; i < m && rows; ++i) {
+        size_t o = ord[i];
+        rows[i].mutation_index = idx[o];
+        rows[i].region = reg[o];
+        rows[i].n = nn[o];
+        rows[i].lambda = lam[o];
+        rows[i].alpha_hat = al[o];
+    }
+    return n;
+}
+
+template <class R> uint64_t EngineT<R>::read_metrics(double *rows, uint64_t cap) {
+    uint64_t m = std::min<uint64_t>(metrics_.size(), cap);
+    for (uint64_t i = 0; i < m; ++i)
+        for (int q = 0; q < 4; ++q)
+            rows[4 * i + q] = metrics_[i][q];
+    return metrics_.size();
+}
+
+template <class R> void EngineT<R>::read_decisions(uint32_t K, double *a, uint8_t *flags) {
+    uint32_t Kd = d_.log_steps;
+    size_t C = static_cast<size_t>(C_);
+    std::vector<double> ha(C * Kd);
+    std::vector<unsigned char> hf(C * Kd);
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    if (Kd) {
+        RAMLT_CUDA(cudaMemcpy(ha.data(), log_a_.p, ha.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        RAMLT_CUDA(cudaMemcpy(hf.data(), log_f_.p, hf.size(), cudaMemcpyDeviceToHost));
+    }
+    for (size_t c = 0; c < C; ++c)
+        for (uint32_t k = 0; k < K; ++k) {
+            bool in = k < Kd;
+            if (a)
+                a[c * K + k] = in ? ha[static_cast<size_t>(k) * C + c] : 0.0;
+            if (flags)
+                flags[c * K + k] = in ? hf[static_cast<size_t>(k) * C + c] : 0;
+        }
+}
+
+template <class R> std::string EngineT<R>::read_partition() {
+    // PartitionIndex::dump formats (core/partition.cpp:104-121, 138-147, 175-190, 229-245)
+    uint64_t n = static_cast<uint64_t>(n_regions_host_);
+    std::vector<double> lam(n);
+    std::vector<uint64_t> nn(n);
+    read_regions(lam.data(), nn.data(), n);
+    std::vector<unsigned long long> vis(n);
+    RAMLT_CUDA(cudaMemcpy(vis.data(), visits_.p, n * 8, cudaMemcpyDeviceToHost));
+    std::ostringstream os;
+    auto leaf_line = [&](int region, double u0, double v0, double u1, double v1) {
+        double l = ctl_ == 0 ? d_.lambda_init : lam[region];
+        os << "leaf " << region << " " << u0 << " " << v0 << " " << u1 << " " << v1 << " " << l << " "
+           << nn[region] << " " << vis[region] << "\n";
+    };
+    auto cell_b = [](int g, int cell, double *b) {
+        int iy = cell / g, ix = cell % g;
+        double inv = 1.0 / g;
+        b[0] = ix * inv;
+        b[1] = iy * inv;
+        b[2] = (ix + 1) * inv;
+        b[3] = (iy + 1) * inv;
+    };
+    std::vector<rd::NodeD> nodes(n_nodes_host_);
+    if (n_nodes_host_)
+        RAMLT_CUDA(cudaMemcpy(nodes.data(), nodes_.p, nodes.size() * sizeof(rd::NodeD), cudaMemcpyDeviceToHost));
+    auto tree_leaves = [&](int tree) {
+        for (const rd::NodeD &nd : nodes) {
+            if (nd.tree != tree || nd.child >= 0)
+                continue;
+            double sc = std::ldexp(1.0, -nd.level);
+            leaf_line(nd.region, nd.ix * sc, nd.iy * sc, (nd.ix + 1) * sc, (nd.iy + 1) * sc);
+        }
+    };
+    double b[4];
+    if (pkind_ == 1) {
+        for (int c = 0; c < d_.n_top * d_.n_top; ++c) {
+            cell_b(d_.n_top, c, b);
+            leaf_line(c, b[0], b[1], b[2], b[3]);
+        }
+    } else if (pkind_ == 2) {
+        tree_leaves(0);
+    } else if (pkind_ == 3 || pkind_ == 4) {
+        for (int c = 0; c < d_.n_top * d_.n_top; ++c) {
+            cell_b(d_.n_top, c, b);
+            os << "# cell " << c << " " << b[0] << " " << b[1] << " " << b[2] << " " << b[3] << "\n";
+            if (pkind_ == 4) {
+                tree_leaves(c);
+            } else {
+                int nb2 = d_.n_bottom * d_.n_bottom;
+                for (int sb = 0; sb < nb2; ++sb) {
+                    double bb[4];
+                    cell_b(d_.n_bottom, sb, bb);
+                    leaf_line(c * nb2 + sb, bb[0], bb[1], bb[2], bb[3]);
+                }
+            }
+        }
+    }
+    return os.str();
+}
+
+}  // namespace ramlt_b200

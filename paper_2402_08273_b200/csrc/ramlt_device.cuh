@@ -1,0 +1,744 @@
+// ramlt_device.cuh -- device-side building blocks of the MLT chain step.
+//
+// Everything is templated on the arithmetic type R:
+//   R = double : the parity build.  Compiled with -fmad=false; every expression
+//                keeps the reference's evaluation order, so +,-,*,/,sqrt round
+//                exactly as the reference's x86-64 SSE2 doubles do.  Only the
+//                libm transcendentals (exp, log, erfc, atan2, sin, cos, pow)
+//                differ from glibc by ulps.
+//   R = float  : the production build (FMA contraction allowed).
+// Reference citations: core/X:N = /root/reference/proj/src/core/X line N.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rd {
+
+constexpr int kMaxV = 24;              // compile-time path capacity (max_vertices <= kMaxV)
+constexpr double kPiD = 3.14159265358979323846;
+constexpr double kTwoPiD = 2.0 * 3.14159265358979323846;
+constexpr double kInvPiD = 0.318309886183790671538;
+constexpr double kEpsD = 1e-4;          // core/scene.hpp:13
+constexpr uint64_t kStreamB = 0x4000000000000000ULL;     // core/driver.cpp:20
+constexpr uint64_t kStreamInit = 0x4000000000000001ULL;  // core/driver.cpp:21
+
+// ---- math traits --------------------------------------------------------------
+template <class R> struct M;
+template <> struct M<double> {
+    static __device__ __forceinline__ double exp(double x) { return ::exp(x); }
+    static __device__ __forceinline__ double log(double x) { return ::log(x); }
+    static __device__ __forceinline__ double sqrt(double x) { return ::sqrt(x); }
+    static __device__ __forceinline__ double erfc(double x) { return ::erfc(x); }
+    static __device__ __forceinline__ double atan2(double y, double x) { return ::atan2(y, x); }
+    static __device__ __forceinline__ double sin(double x) { return ::sin(x); }
+    static __device__ __forceinline__ double cos(double x) { return ::cos(x); }
+    static __device__ __forceinline__ double pow(double x, double y) { return ::pow(x, y); }
+    static __device__ __forceinline__ double abs(double x) { return ::fabs(x); }
+    static __device__ __forceinline__ double copysign(double x, double y) { return ::copysign(x, y); }
+    static __device__ __forceinline__ double ldexp(double x, int e) { return ::ldexp(x, e); }
+    static __device__ __forceinline__ bool finite(double x) { return ::isfinite(x); }
+    static __device__ __forceinline__ bool isnan(double x) { return ::isnan(x); }
+    static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+    static __device__ __forceinline__ double inf() { return __longlong_as_double(0x7ff0000000000000LL); }
+};
+template <> struct M<float> {
+    static __device__ __forceinline__ float exp(float x) { return ::expf(x); }
+    static __device__ __forceinline__ float log(float x) { return ::logf(x); }
+    static __device__ __forceinline__ float sqrt(float x) { return ::sqrtf(x); }
+    static __device__ __forceinline__ float erfc(float x) { return ::erfcf(x); }
+    static __device__ __forceinline__ float atan2(float y, float x) { return ::atan2f(y, x); }
+    static __device__ __forceinline__ float sin(float x) { return ::sinf(x); }
+    static __device__ __forceinline__ float cos(float x) { return ::cosf(x); }
+    static __device__ __forceinline__ float pow(float x, float y) { return ::powf(x, y); }
+    static __device__ __forceinline__ float abs(float x) { return ::fabsf(x); }
+    static __device__ __forceinline__ float copysign(float x, float y) { return ::copysignf(x, y); }
+    static __device__ __forceinline__ float ldexp(float x, int e) { return ::ldexpf(x, e); }
+    static __device__ __forceinline__ bool finite(float x) { return ::isfinite(x); }
+    static __device__ __forceinline__ bool isnan(float x) { return ::isnan(x); }
+    static __device__ __forceinline__ float rcp(float x) { return 1.0f / x; }
+    static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
+};
+
+// ---- vectors (core/vec.hpp:9-53, same evaluation order) -----------------------
+template <class R> struct V3 {
+    R x, y, z;
+};
+template <class R> __device__ __forceinline__ V3<R> mk(R x, R y, R z) { return {x, y, z}; }
+template <class R> __device__ __forceinline__ V3<R> add(V3<R> a, V3<R> b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+template <class R> __device__ __forceinline__ V3<R> sub(V3<R> a, V3<R> b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+template <class R> __device__ __forceinline__ V3<R> mul(V3<R> a, V3<R> b) { return {a.x * b.x, a.y * b.y, a.z * b.z}; }
+template <class R> __device__ __forceinline__ V3<R> scl(V3<R> a, R s) { return {a.x * s, a.y * s, a.z * s}; }
+template <class R> __device__ __forceinline__ V3<R> dvs(V3<R> a, R s) { return {a.x / s, a.y / s, a.z / s}; }
+template <class R> __device__ __forceinline__ V3<R> neg(V3<R> a) { return {-a.x, -a.y, -a.z}; }
+template <class R> __device__ __forceinline__ R dot(V3<R> a, V3<R> b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+template <class R> __device__ __forceinline__ V3<R> cross(V3<R> a, V3<R> b) {
+    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+template <class R> __device__ __forceinline__ R len(V3<R> a) { return M<R>::sqrt(dot(a, a)); }
+template <class R> __device__ __forceinline__ V3<R> unit(V3<R> a) { return dvs(a, len(a)); }
+template <class R> __device__ __forceinline__ V3<R> reflect(V3<R> w, V3<R> n) { return sub(scl(n, R(2) * dot(w, n)), w); }
+template <class R> __device__ __forceinline__ R lum(V3<R> c) {
+    return R(0.2126) * c.x + R(0.7152) * c.y + R(0.0722) * c.z;
+}
+template <class R> __device__ __forceinline__ bool zero3(V3<R> a) { return a.x == R(0) && a.y == R(0) && a.z == R(0); }
+
+// ---- random sequences ------------------------------------------------------------
+// RNG_PCG: core/rng.hpp:11-50 bit for bit (same seeds and streams as the
+// reference driver, core/driver.cpp:223-225).
+// RNG_PHILOX: Philox4x32-10, key = seed, counter = (block lo, block hi, stream
+// lo, stream hi); next_u32 consumes one word of each 4-word block in order.
+enum { RNG_PCG = 0, RNG_PHILOX = 1 };
+
+template <int KIND> struct Rng;
+
+template <> struct Rng<RNG_PCG> {
+    uint64_t state, inc;
+    __device__ __forceinline__ uint32_t next_u32() {
+        uint64_t old = state;
+        state = old * 6364136223846793005ULL + inc;
+        uint32_t xs = static_cast<uint32_t>(((old >> 18u) ^ old) >> 27u);
+        uint32_t rot = static_cast<uint32_t>(old >> 59u);
+        return __funnelshift_r(xs, xs, rot);
+    }
+    __device__ __forceinline__ void reseed(uint64_t seed, uint64_t stream) {
+        state = 0u;
+        inc = (stream << 1u) | 1u;
+        next_u32();
+        state += seed;
+        next_u32();
+    }
+};
+
+__device__ __forceinline__ void philox10(uint32_t &c0, uint32_t &c1, uint32_t &c2, uint32_t &c3,
+                                         uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+template <> struct Rng<RNG_PHILOX> {
+    uint64_t key, stream, draw;
+    uint32_t b0, b1, b2, b3;
+    uint64_t bid;
+    __device__ __forceinline__ void reseed(uint64_t seed, uint64_t strm) {
+        key = seed;
+        stream = strm;
+        draw = 0;
+        bid = ~0ULL;
+    }
+    __device__ __forceinline__ uint32_t next_u32() {
+        uint64_t b = draw >> 2;
+        if (b != bid) {
+            b0 = static_cast<uint32_t>(b);
+            b1 = static_cast<uint32_t>(b >> 32);
+            b2 = static_cast<uint32_t>(stream);
+            b3 = static_cast<uint32_t>(stream >> 32);
+            philox10(b0, b1, b2, b3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
+            bid = b;
+        }
+        uint32_t w = draw & 3;
+        ++draw;
+        return w == 0 ? b0 : (w == 1 ? b1 : (w == 2 ? b2 : b3));
+    }
+};
+
+// Uniform in [0,1): next_double (core/rng.hpp:32-40) for R = double; the same
+// two words truncated to 24 bits for R = float (identical consumption).
+template <class R> struct Unit;
+template <> struct Unit<double> {
+    template <class G> static __device__ __forceinline__ double draw(G &g) {
+        uint64_t hi = g.next_u32();
+        uint64_t lo = g.next_u32();
+        return static_cast<double>(((hi << 32) | lo) >> 11) * 0x1.0p-53;
+    }
+};
+template <> struct Unit<float> {
+    template <class G> static __device__ __forceinline__ float draw(G &g) {
+        uint32_t hi = g.next_u32();
+        (void)g.next_u32();
+        return static_cast<float>(hi >> 8) * 0x1.0p-24f;
+    }
+};
+
+// ---- scene --------------------------------------------------------------------------
+enum { MAT_DIFFUSE = 0, MAT_MIRROR = 1, MAT_DIELECTRIC = 2, MAT_GLOSSY = 3 };
+enum { EV_NONE = 0, EV_REFLECT = 1, EV_TRANSMIT = 2 };
+
+template <class R> struct TriD {   // a, e1 = b - a, e2 = c - a, n = normalize(cross(e1, e2))
+    V3<R> a, e1, e2, n;
+    int mat, emi;
+};
+template <class R> struct SphD {
+    V3<R> c;
+    R r;
+    int mat, emi;
+};
+template <class R> struct MatD {
+    int kind;
+    V3<R> albedo;
+    R ior, expo;
+};
+template <class R> struct CamD {   // core/camera.hpp:44-52 (basis computed on the host in fp64)
+    V3<R> pos, right, up, fwd;
+    R tanh, aspect, area, sensor;
+};
+
+template <class R> struct SceneView {
+    const TriD<R> *tri;
+    const SphD<R> *sph;
+    const MatD<R> *mat;
+    const V3<R> *emit;
+    int ntri, nsph;
+    CamD<R> cam;
+};
+
+template <class R> struct Hit {
+    V3<R> p, n;
+    int mat, emi;
+    R t;
+};
+
+// Cooperative lane groups: G lanes share one chain; G = 1 is one chain per thread.
+template <int G> struct Group {
+    unsigned mask;
+    int lane;
+    __device__ __forceinline__ Group() {
+        int wl = threadIdx.x & 31;
+        lane = wl & (G - 1);
+        mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (wl & ~(G - 1)));
+    }
+};
+
+// core/scene.cpp:15-29
+template <class R>
+__device__ __forceinline__ bool hit_sphere(const SphD<R> &s, V3<R> o, V3<R> d, R &t) {
+    V3<R> oc = sub(o, s.c);
+    R b = dot(oc, d);
+    R c = dot(oc, oc) - s.r * s.r;
+    R disc = b * b - c;
+    if (disc < R(0))
+        return false;
+    R sq = M<R>::sqrt(disc);
+    R tt = -b - sq;
+    if (tt > R(kEpsD)) {
+        t = tt;
+        return true;
+    }
+    tt = -b + sq;
+    if (tt > R(kEpsD)) {
+        t = tt;
+        return true;
+    }
+    return false;
+}
+
+// core/scene.cpp:31-52 (Moeller-Trumbore with the stored edges)
+template <class R>
+__device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &t) {
+    V3<R> p = cross(d, tr.e2);
+    R det = dot(tr.e1, p);
+    if (M<R>::abs(det) < R(1e-14))
+        return false;
+    R inv = R(1) / det;
+    V3<R> tv = sub(o, tr.a);
+    R u = dot(tv, p) * inv;
+    if (u < R(0) || u > R(1))
+        return false;
+    V3<R> q = cross(tv, tr.e1);
+    R v = dot(d, q) * inv;
+    if (v < R(0) || u + v > R(1))
+        return false;
+    R tt = dot(tr.e2, q) * inv;
+    if (tt > R(kEpsD)) {
+        t = tt;
+        return true;
+    }
+    return false;
+}
+
+// Closest hit (core/scene.cpp:57-92).  Primitive order = spheres then
+// triangles; each lane scans its stride-G subset in increasing order with
+// strict '<', and the (t, index) lexicographic minimum across lanes is the
+// reference's first-minimum winner.
+template <class R, int G>
+__device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> d, Hit<R> &h,
+                                          const Group<G> &g) {
+    R best = M<R>::inf();
+    int bi = 0x7fffffff;
+    int n = s.nsph + s.ntri;
+    for (int i = g.lane; i < s.nsph; i += G) {
+        R t;
+        if (hit_sphere(s.sph[i], o, d, t) && t < best) {
+            best = t;
+            bi = i;
+        }
+    }
+    for (int i = g.lane + ((s.nsph + G - 1) / G) * G - s.nsph; false;) { (void)i; }
+    for (int j = g.lane; j < s.ntri; j += G) {
+        R t;
+        if (hit_tri(s.tri[j], o, d, t) && t < best) {
+            best = t;
+            bi = s.nsph + j;
+        }
+    }
+    (void)n;
+    if (G > 1) {
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+            R ot = __shfl_xor_sync(g.mask, best, off, G);
+            int oi = __shfl_xor_sync(g.mask, bi, off, G);
+            if (ot < best || (ot == best && oi < bi)) {
+                best = ot;
+                bi = oi;
+            }
+        }
+    }
+    if (bi == 0x7fffffff)
+        return false;
+    h.t = best;
+    h.p = add(o, scl(d, best));
+    if (bi < s.nsph) {
+        const SphD<R> &sp = s.sph[bi];
+        h.n = unit(sub(h.p, sp.c));
+        h.mat = sp.mat;
+        h.emi = sp.emi;
+    } else {
+        const TriD<R> &tr = s.tri[bi - s.nsph];
+        h.n = tr.n;
+        h.mat = tr.mat;
+        h.emi = tr.emi;
+    }
+    return true;
+}
+
+// visible (core/scene.cpp:94-102) as an any-hit query: the reference's
+// "closest t >= dist - eps" is "no primitive's first root lies in (eps, dist - eps)".
+template <class R, int G>
+__device__ __forceinline__ bool visible(const SceneView<R> &s, V3<R> a, V3<R> b, const Group<G> &g) {
+    V3<R> d = sub(b, a);
+    R dist = len(d);
+    if (dist <= R(2) * R(kEpsD))
+        return false;
+    d = dvs(d, dist);
+    R lim = dist - R(kEpsD);
+    bool occ = false;
+    for (int i = g.lane; i < s.nsph && !occ; i += G) {
+        R t;
+        if (hit_sphere(s.sph[i], a, d, t) && t < lim)
+            occ = true;
+    }
+    for (int j = g.lane; j < s.ntri && !occ; j += G) {
+        R t;
+        if (hit_tri(s.tri[j], a, d, t) && t < lim)
+            occ = true;
+    }
+    if (G > 1)
+        occ = __any_sync(g.mask, occ);
+    return !occ;
+}
+
+// ---- camera (core/camera.cpp:32-64) ---------------------------------------------------
+template <class R> __device__ __forceinline__ V3<R> cam_primary(const CamD<R> &c, R u, R v) {
+    R px = (R(2) * u - R(1)) * c.tanh * c.aspect;
+    R py = (R(2) * v - R(1)) * c.tanh;
+    return unit(add(add(scl(c.right, px), scl(c.up, py)), c.fwd));
+}
+template <class R> __device__ __forceinline__ bool cam_raster(const CamD<R> &c, V3<R> w, R &u, R &v) {
+    R ct = dot(w, c.fwd);
+    if (ct <= R(0))
+        return false;
+    R px = dot(w, c.right) / ct;
+    R py = dot(w, c.up) / ct;
+    R uu = R(0.5) * (px / (c.tanh * c.aspect) + R(1));
+    R vv = R(0.5) * (py / c.tanh + R(1));
+    if (uu < R(0) || uu > R(1) || vv < R(0) || vv > R(1))
+        return false;
+    u = uu;
+    v = vv;
+    return true;
+}
+template <class R> __device__ __forceinline__ R cam_importance(const CamD<R> &c, V3<R> w) {
+    R u, v;
+    if (!cam_raster(c, w, u, v))
+        return R(0);
+    R ct = dot(w, c.fwd);
+    R c2 = ct * ct;
+    return c.sensor / (c2 * c2);
+}
+template <class R> __device__ __forceinline__ R cam_dir_pdf(const CamD<R> &c, V3<R> w) {
+    R u, v;
+    if (!cam_raster(c, w, u, v))
+        return R(0);
+    R ct = dot(w, c.fwd);
+    return R(1) / (c.area * ct * ct * ct);
+}
+
+// ---- sampling core (core/sampling.cpp) -------------------------------------------------
+template <class R> __device__ __forceinline__ R npdf(R x) {
+    return M<R>::exp(R(-0.5) * x * x) / M<R>::sqrt(R(kTwoPiD));
+}
+template <class R> __device__ __forceinline__ R ncdf(R x) {
+    return R(0.5) * M<R>::erfc(-x / R(1.41421356237309504880));
+}
+
+// Acklam + one Halley step (core/sampling.cpp:19-60).
+template <class R> __device__ __forceinline__ R nquantile(R p) {
+    const R a0 = R(-3.969683028665376e+01), a1 = R(2.209460984245205e+02),
+            a2 = R(-2.759285104469687e+02), a3 = R(1.383577518672690e+02),
+            a4 = R(-3.066479806614716e+01), a5 = R(2.506628277459239e+00);
+    const R b0 = R(-5.447609879822406e+01), b1 = R(1.615858368580409e+02),
+            b2 = R(-1.556989798598866e+02), b3 = R(6.680131188771972e+01),
+            b4 = R(-1.328068155288572e+01);
+    const R c0 = R(-7.784894002430293e-03), c1 = R(-3.223964580411365e-01),
+            c2 = R(-2.400758277161838e+00), c3 = R(-2.549732539343734e+00),
+            c4 = R(4.374664141464968e+00), c5 = R(2.938163982698783e+00);
+    const R d0 = R(7.784695709041462e-03), d1 = R(3.224671290700398e-01),
+            d2 = R(2.445134137142996e+00), d3 = R(3.754408661907416e+00);
+    R x;
+    if (p < R(0.02425)) {
+        R q = M<R>::sqrt(R(-2) * M<R>::log(p));
+        x = (((((c0 * q + c1) * q + c2) * q + c3) * q + c4) * q + c5) /
+            ((((d0 * q + d1) * q + d2) * q + d3) * q + R(1));
+    } else if (p > R(1) - R(0.02425)) {
+        R q = M<R>::sqrt(R(-2) * M<R>::log(R(1) - p));
+        x = -(((((c0 * q + c1) * q + c2) * q + c3) * q + c4) * q + c5) /
+            ((((d0 * q + d1) * q + d2) * q + d3) * q + R(1));
+    } else {
+        R q = p - R(0.5);
+        R r = q * q;
+        x = (((((a0 * r + a1) * r + a2) * r + a3) * r + a4) * r + a5) * q /
+            (((((b0 * r + b1) * r + b2) * r + b3) * r + b4) * r + R(1));
+    }
+    if (sizeof(R) == 8) {   // the Halley refinement only pays at fp64 precision
+        R e = ncdf(x) - p;
+        R u = e * M<R>::sqrt(R(kTwoPiD)) * M<R>::exp(R(0.5) * x * x);
+        x = x - u / (R(1) + R(0.5) * x * u);
+    }
+    return x;
+}
+
+// Truncated normal on [-pi, pi] (core/sampling.cpp:62-92).  The (sigma,
+// cdf_lo, mass) triple is a pure function of sigma; the engine caches it per
+// region (KernTab) so a proposal never re-evaluates erfc.
+template <class R> struct Kern {
+    R sigma, lo, mass;
+};
+template <class R> __device__ __forceinline__ Kern<R> make_kern(R sigma) {
+    Kern<R> k;
+    k.sigma = sigma;
+    R t = R(kPiD) / sigma;
+    k.lo = ncdf(-t);
+    k.mass = ncdf(t) - k.lo;
+    return k;
+}
+template <class R, class G> __device__ __forceinline__ R kern_sample(const Kern<R> &k, G &rng) {
+    R u = Unit<R>::draw(rng);
+    R p = k.lo + u * k.mass;
+    if (p <= R(0))
+        return R(-kPiD);
+    if (p >= R(1))
+        return R(kPiD);
+    R th = k.sigma * nquantile(p);
+    return th < R(-kPiD) ? R(-kPiD) : (th > R(kPiD) ? R(kPiD) : th);
+}
+template <class R> __device__ __forceinline__ R kern_pdf(const Kern<R> &k, R th) {
+    if (M<R>::abs(th) > R(kPiD))
+        return R(0);
+    return npdf(th / k.sigma) / (k.sigma * k.mass);
+}
+template <class R> __device__ __forceinline__ R kern_pdf_sa(const Kern<R> &k, R alpha) {
+    R s = M<R>::sin(alpha);
+    const R floor_ = sizeof(R) == 8 ? R(1e-300) : R(1e-37);
+    s = s > floor_ ? s : floor_;
+    return kern_pdf(k, alpha) / (R(kPiD) * s);
+}
+
+// Duff et al. frame (core/sampling.cpp:94-101), to_world (sampling.hpp:49-51).
+template <class R> __device__ __forceinline__ V3<R> to_world(V3<R> n, V3<R> l) {
+    R sign = M<R>::copysign(R(1), n.z);
+    R a = R(-1) / (sign + n.z);
+    R b = n.x * n.y * a;
+    V3<R> t = mk(R(1) + sign * n.x * n.x * a, sign * b, -sign * n.x);
+    V3<R> bt = mk(b, sign + n.y * n.y * a, -n.y);
+    return add(add(scl(t, l.x), scl(bt, l.y)), scl(n, l.z));
+}
+
+// core/sampling.cpp:103-110
+template <class R, class G>
+__device__ __forceinline__ V3<R> perturb_dir(V3<R> w, const Kern<R> &k, G &rng) {
+    R th = kern_sample(k, rng);
+    R ph = R(kTwoPiD) * Unit<R>::draw(rng);
+    R st = M<R>::sin(th);
+    V3<R> l = mk(st * M<R>::cos(ph), st * M<R>::sin(ph), M<R>::cos(th));
+    return unit(to_world(w, l));
+}
+
+// core/sampling.cpp:112-121
+template <class R> __device__ __forceinline__ void cylindrical(V3<R> w, R &u, R &v) {
+    R ph = M<R>::atan2(w.y, w.x);
+    if (ph < R(0))
+        ph += R(kTwoPiD);
+    R uu = ph / R(kTwoPiD);
+    if (uu >= R(1))
+        uu = R(0);
+    R vv = R(0.5) * (w.z + R(1));
+    u = uu;
+    v = vv < R(0) ? R(0) : (vv > R(1) ? R(1) : vv);
+}
+
+// ---- BSDFs (core/scene.cpp:245-414) ---------------------------------------------------
+template <class R> __device__ __forceinline__ V3<R> facing(V3<R> n, V3<R> wi) { return dot(n, wi) >= R(0) ? n : neg(n); }
+
+template <class R> __device__ __forceinline__ R fresnel(R cos_i, R ior) {
+    R ei = R(1), et = ior, ci = cos_i;
+    if (ci < R(0)) {
+        R tmp = ei;
+        ei = et;
+        et = tmp;
+        ci = -ci;
+    }
+    R s2 = (ei / et) * (ei / et) * (R(1) - ci * ci);
+    if (s2 >= R(1))
+        return R(1);
+    R ct = M<R>::sqrt(R(1) - s2);
+    R rpa = (et * ci - ei * ct) / (et * ci + ei * ct);
+    R rpe = (ei * ci - et * ct) / (ei * ci + et * ct);
+    return R(0.5) * (rpa * rpa + rpe * rpe);
+}
+
+template <class R> __device__ __forceinline__ V3<R> bsdf_f(const MatD<R> &m, V3<R> wi, V3<R> wo, V3<R> n) {
+    if (m.kind == MAT_DIFFUSE) {
+        V3<R> ns = facing(n, wi);
+        if (dot(ns, wo) <= R(0))
+            return mk(R(0), R(0), R(0));
+        return scl(m.albedo, R(kInvPiD));
+    }
+    if (m.kind == MAT_GLOSSY) {
+        V3<R> ns = facing(n, wi);
+        if (dot(ns, wo) <= R(0))
+            return mk(R(0), R(0), R(0));
+        R ca = dot(reflect(wi, ns), wo);
+        if (ca <= R(0))
+            return mk(R(0), R(0), R(0));
+        R norm = (m.expo + R(1)) / R(kTwoPiD);
+        return scl(m.albedo, norm * M<R>::pow(ca, m.expo));
+    }
+    return mk(R(0), R(0), R(0));
+}
+
+template <class R> __device__ __forceinline__ R bsdf_pdf(const MatD<R> &m, V3<R> wi, V3<R> wo, V3<R> n) {
+    if (m.kind == MAT_DIFFUSE) {
+        V3<R> ns = facing(n, wi);
+        R c = dot(ns, wo);
+        return c > R(0) ? c * R(kInvPiD) : R(0);
+    }
+    if (m.kind == MAT_GLOSSY) {
+        V3<R> ns = facing(n, wi);
+        R ca = dot(reflect(wi, ns), wo);
+        if (ca <= R(0))
+            return R(0);
+        return (m.expo + R(1)) / R(kTwoPiD) * M<R>::pow(ca, m.expo);
+    }
+    return R(0);
+}
+
+template <class R>
+__device__ __forceinline__ bool spec_cont(const MatD<R> &m, V3<R> wi, V3<R> n, int ev, V3<R> &out) {
+    if (m.kind == MAT_MIRROR) {
+        if (ev != EV_REFLECT)
+            return false;
+        out = unit(reflect(wi, facing(n, wi)));
+        return true;
+    }
+    if (m.kind != MAT_DIELECTRIC)
+        return false;
+    R cos_i = dot(n, wi);
+    if (ev == EV_REFLECT) {
+        out = unit(reflect(wi, facing(n, wi)));
+        return true;
+    }
+    R eta = cos_i > R(0) ? R(1) / m.ior : m.ior;
+    V3<R> ns = facing(n, wi);
+    R ci = dot(ns, wi);
+    R s2 = eta * eta * (R(1) - ci * ci);
+    if (s2 >= R(1))
+        return false;
+    R ct = M<R>::sqrt(R(1) - s2);
+    out = unit(add(scl(wi, -eta), scl(ns, eta * ci - ct)));
+    return true;
+}
+
+template <class R> __device__ __forceinline__ V3<R> spec_weight(const MatD<R> &m, V3<R> wi, V3<R> n, int ev) {
+    if (m.kind == MAT_MIRROR)
+        return ev == EV_REFLECT ? m.albedo : mk(R(0), R(0), R(0));
+    if (m.kind == MAT_DIELECTRIC) {
+        R f = fresnel(dot(n, wi), m.ior);
+        if (ev == EV_REFLECT)
+            return scl(m.albedo, f);
+        if (ev == EV_TRANSMIT)
+            return scl(m.albedo, R(1) - f);
+    }
+    return mk(R(0), R(0), R(0));
+}
+
+template <class R> __device__ __forceinline__ R spec_prob(const MatD<R> &m, V3<R> wi, V3<R> n, int ev) {
+    if (m.kind == MAT_MIRROR)
+        return ev == EV_REFLECT ? R(1) : R(0);
+    if (m.kind == MAT_DIELECTRIC) {
+        R f = fresnel(dot(n, wi), m.ior);
+        return ev == EV_REFLECT ? f : R(1) - f;
+    }
+    return R(0);
+}
+
+template <class R> struct BS {
+    V3<R> dir;
+    R pdf;
+    bool zero_thr;
+    bool delta;
+    int ev;
+};
+
+// core/scene.cpp:323-367 (only what the tracer consumes: direction, pdf,
+// whether the throughput is zero, delta flag and event).
+template <class R, class G>
+__device__ __forceinline__ bool bsdf_sample(const MatD<R> &m, V3<R> wi, V3<R> n, G &rng, BS<R> &bs) {
+    if (m.kind == MAT_DIFFUSE) {
+        V3<R> ns = facing(n, wi);
+        R u1 = Unit<R>::draw(rng);
+        R u2 = Unit<R>::draw(rng);
+        R r = M<R>::sqrt(u1);
+        R ph = R(kTwoPiD) * u2;
+        R z = R(1) - u1;
+        V3<R> l = mk(r * M<R>::cos(ph), r * M<R>::sin(ph), M<R>::sqrt(z > R(0) ? z : R(0)));
+        V3<R> wo = to_world(ns, l);
+        R c = dot(ns, wo);
+        R pdf = (c > R(0) ? c : R(0)) * R(kInvPiD);
+        if (pdf <= R(0))
+            return false;
+        bs.dir = wo;
+        bs.pdf = pdf;
+        bs.zero_thr = zero3(m.albedo);
+        bs.delta = false;
+        bs.ev = EV_NONE;
+        return true;
+    }
+    if (m.kind == MAT_GLOSSY) {
+        V3<R> ns = facing(n, wi);
+        V3<R> axis = reflect(wi, ns);
+        R u1 = Unit<R>::draw(rng);
+        R u2 = Unit<R>::draw(rng);
+        R ca = M<R>::pow(u1, R(1) / (m.expo + R(1)));
+        R z = R(1) - ca * ca;
+        R sa = M<R>::sqrt(z > R(0) ? z : R(0));
+        R ph = R(kTwoPiD) * u2;
+        V3<R> l = mk(sa * M<R>::cos(ph), sa * M<R>::sin(ph), ca);
+        V3<R> wo = unit(to_world(axis, l));
+        R pdf = (m.expo + R(1)) / R(kTwoPiD) * M<R>::pow(ca, m.expo);
+        R co = dot(ns, wo);
+        bs.dir = wo;
+        bs.pdf = pdf;
+        bs.zero_thr = !(co > R(0)) || zero3(scl(m.albedo, co));
+        bs.delta = false;
+        bs.ev = EV_NONE;
+        return true;
+    }
+    if (m.kind == MAT_MIRROR) {
+        V3<R> ns = facing(n, wi);
+        bs.dir = unit(reflect(wi, ns));
+        bs.pdf = R(1);
+        bs.zero_thr = zero3(m.albedo);
+        bs.delta = true;
+        bs.ev = EV_REFLECT;
+        return true;
+    }
+    R f = fresnel(dot(n, wi), m.ior);
+    int ev = Unit<R>::draw(rng) < f ? EV_REFLECT : EV_TRANSMIT;
+    V3<R> wo;
+    if (!spec_cont(m, wi, n, ev, wo))
+        return false;
+    R q = ev == EV_REFLECT ? f : R(1) - f;
+    bs.dir = wo;
+    bs.pdf = q;
+    bs.zero_thr = zero3(dvs(spec_weight(m, wi, n, ev), q));
+    bs.delta = true;
+    bs.ev = ev;
+    return true;
+}
+
+// ---- path vertices ----------------------------------------------------------------------
+// Register/local form.  Vertex 0 of every chain path is the camera vertex
+// (core/path.cpp:88-92): position = camera position, normal = forward.
+template <class R> struct Vx {
+    V3<R> p, n;
+    int mat, emi;
+    bool spec;
+    int ev;
+};
+
+// Global SoA record [vertex][chain]; meta packs material+1 (16 bits),
+// emitter+1 (12 bits), specular (1 bit), event (2 bits).
+template <class R> struct alignas(16) GV;
+template <> struct alignas(16) GV<float> {
+    float4 a, b;   // (px py pz nx) (ny nz meta 0)
+};
+template <> struct alignas(16) GV<double> {
+    double2 a, b, c;   // (px py) (pz nx) (ny nz)
+    long long meta, pad;
+};
+
+__device__ __forceinline__ uint32_t pack_meta(int mat, int emi, bool spec, int ev) {
+    return static_cast<uint32_t>(mat + 1) | (static_cast<uint32_t>(emi + 1) << 16) |
+           (spec ? (1u << 28) : 0u) | (static_cast<uint32_t>(ev) << 29);
+}
+template <class R> __device__ __forceinline__ void unpack_meta(uint32_t m, Vx<R> &v) {
+    v.mat = static_cast<int>(m & 0xffffu) - 1;
+    v.emi = static_cast<int>((m >> 16) & 0xfffu) - 1;
+    v.spec = (m >> 28) & 1u;
+    v.ev = static_cast<int>((m >> 29) & 3u);
+}
+
+__device__ __forceinline__ Vx<float> load_gv(const GV<float> *p) {
+    GV<float> g;
+    g.a = __ldcg(&p->a);
+    g.b = __ldcg(&p->b);
+    Vx<float> v;
+    v.p = mk(g.a.x, g.a.y, g.a.z);
+    v.n = mk(g.a.w, g.b.x, g.b.y);
+    unpack_meta(__float_as_uint(g.b.z), v);
+    return v;
+}
+__device__ __forceinline__ void store_gv(GV<float> *p, const Vx<float> &v) {
+    float4 a = make_float4(v.p.x, v.p.y, v.p.z, v.n.x);
+    float4 b = make_float4(v.n.y, v.n.z, __uint_as_float(pack_meta(v.mat, v.emi, v.spec, v.ev)), 0.f);
+    __stcg(&p->a, a);
+    __stcg(&p->b, b);
+}
+__device__ __forceinline__ Vx<double> load_gv(const GV<double> *p) {
+    double2 a = __ldcg(&p->a), b = __ldcg(&p->b), c = __ldcg(&p->c);
+    long long m = __ldcg(&p->meta);
+    Vx<double> v;
+    v.p = mk(a.x, a.y, b.x);
+    v.n = mk(b.y, c.x, c.y);
+    unpack_meta(static_cast<uint32_t>(m), v);
+    return v;
+}
+__device__ __forceinline__ void store_gv(GV<double> *p, const Vx<double> &v) {
+    __stcg(&p->a, make_double2(v.p.x, v.p.y));
+    __stcg(&p->b, make_double2(v.p.z, v.n.x));
+    __stcg(&p->c, make_double2(v.n.y, v.n.z));
+    __stcg(&p->meta, static_cast<long long>(pack_meta(v.mat, v.emi, v.spec, v.ev)));
+}
+
+}  // namespace rd

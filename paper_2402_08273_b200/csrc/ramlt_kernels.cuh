@@ -1,0 +1,1168 @@
+// ramlt_kernels.cuh -- sm_100a kernels of the MLT hot path.
+//
+//   k_step      the persistent chain-step megakernel: one chain per thread (or
+//               per G-lane group), chain state SoA in HBM, proposal path in
+//               per-thread local memory, scene primitives staged in shared
+//               memory, splat fused as vector float4 atomics (fp32) or fp64
+//               atomics (parity build).  Replaces run_chain_span
+//               (core/driver.cpp:109-173) and everything below it.
+//   k_init      chain initialisation (core/driver.cpp:219-242).
+//   k_bsub      estimate_b substream sums (core/driver.cpp:31-57).
+//   k_adapt_*   shared adaptation statistics (KernelController::record_acceptance,
+//               core/adaptation.cpp:60-92) after each lockstep step.
+//   k_refine    quadtree refinement at barriers (core/partition.cpp:68-100,
+//               217-227; core/adaptation.cpp:34-42).
+#pragma once
+
+#include "ramlt_device.cuh"
+
+#include <cub/block/block_radix_sort.cuh>
+
+namespace rd {
+
+// ---- engine-side device structures -------------------------------------------------
+template <class R> struct KernTab {   // per region: kernels for sigma1 and sigma2
+    Kern<R> k1, k2;
+};
+
+struct NodeD {   // quadtree node (core/partition.hpp:92-101)
+    int level, ix, iy, child, region, tree;
+};
+
+struct PartView {
+    int kind;   // 0 none, 1 lens grid, 2 lens quadtree, 3 mc grid, 4 mc quadtree
+    int ntop, nbot;
+    const NodeD *nodes;
+    const int *roots;
+    unsigned long long *visits;   // per region (record_visit)
+};
+
+struct RegionArrays {   // KernelController regions (adaptation.hpp:35-46)
+    double *lambda;
+    unsigned long long *n;        // n_k
+    unsigned int *pend_n;         // i_k
+    double *pend_sum;             // A_k (literal)
+    unsigned long long *pend_fx;  // A_k (pooled, 2^-24 fixed point)
+    unsigned long long *tot_vis;
+    double *tot_acc;              // literal
+    unsigned long long *tot_fx;   // pooled
+    // pooled per-exchange accumulators
+    unsigned long long *x_cnt, *x_fx, *x_last;
+    unsigned int *x_touched;
+    unsigned int *touched_list;
+    unsigned int *n_touched;
+};
+
+struct TraceBuf {
+    unsigned long long *count;
+    unsigned long long cap;
+    unsigned long long *index;
+    long long *region;
+    unsigned long long *n;
+    double *lambda, *alpha;
+};
+
+struct AdaptCfg {
+    int L;
+    double gmax, gscale, target, lmin, ratio;
+    int trace;
+};
+
+template <class R> struct ChainArrays {
+    GV<R> *verts;   // vertex v >= 1 of chain c at verts[(v-1)*C + c]
+    int *klen;
+    unsigned int *smask;
+    R *cf;          // [4][C]: f.x f.y f.z pi
+    R *cr;          // [2][C]: raster u v
+    R *eyeden;      // cached eye_path_density(current), NaN = unknown
+    unsigned long long *rng0, *rng1;
+    double *acc, *iacc, *lum;
+    unsigned long long *npert, *nlarge, *ipert, *nsteps;
+    double *log_a;
+    unsigned char *log_f;
+    unsigned int log_K;
+    int *vreg;
+    double *va;
+    int *err;
+    unsigned long long *rays;   // [2]
+};
+
+template <class R> struct StepParams {
+    SceneView<R> scene;   // tri/sph point to global; staged into smem by the kernel
+    int C;                // chains in this handle
+    long long C_total, chain_off;
+    int maxv, pk, ctl;    // perturbation kind, controller (0 fixed 1 global 2 regional)
+    int W, H;
+    unsigned long long seed;
+    ChainArrays<R> ch;
+    PartView part;
+    const KernTab<R> *ktab;
+    double *film64;   // parity build: RGB fp64
+    float4 *film32;   // production build: RGBA fp32 staging
+    // span
+    unsigned long long span_start, per, rem;
+    int j0, j1;
+    int record_visits;   // write vreg/va (adaptive)
+    int pooled;          // fuse pooled accumulation into the step
+    RegionArrays reg;
+};
+
+// ---- path accessors --------------------------------------------------------------------
+template <class R> struct CurPath {
+    const GV<R> *verts;
+    int C, c;
+    const CamD<R> *cam;
+    __device__ __forceinline__ Vx<R> get(int i) const {
+        if (i == 0) {
+            Vx<R> v;
+            v.p = cam->pos;
+            v.n = cam->fwd;
+            v.mat = -1;
+            v.emi = -1;
+            v.spec = false;
+            v.ev = EV_NONE;
+            return v;
+        }
+        return load_gv(&verts[static_cast<size_t>(i - 1) * C + c]);
+    }
+};
+
+template <class R> struct PropPath {
+    const Vx<R> *pv;
+    int head_end;
+    const CurPath<R> *cur;
+    __device__ __forceinline__ Vx<R> get(int i) const { return i <= head_end ? pv[i] : cur->get(i); }
+};
+
+template <class R, class P> __device__ __forceinline__ V3<R> pdir(const P &path, int i) {
+    return unit(sub(path.get(i + 1).p, path.get(i).p));
+}
+
+struct RayCount {
+    unsigned long long c = 0, v = 0;
+};
+
+// core/path.cpp:7-17
+template <class R, int G>
+__device__ __forceinline__ R geom_term(const SceneView<R> &S, const Vx<R> &a, const Vx<R> &b,
+                                       const Group<G> &g, RayCount &rc) {
+    V3<R> d = sub(b.p, a.p);
+    R d2 = dot(d, d);
+    if (d2 <= R(0))
+        return R(0);
+    V3<R> dir = dvs(d, M<R>::sqrt(d2));
+    R gt = M<R>::abs(dot(a.n, dir)) * M<R>::abs(dot(b.n, dir)) / d2;
+    if (gt <= R(0))
+        return R(0);
+    ++rc.v;
+    return visible(S, a.p, b.p, g) ? gt : R(0);
+}
+
+// core/path.cpp:19-29
+template <class R, int G>
+__device__ __forceinline__ R area_conv(const SceneView<R> &S, V3<R> from, const Vx<R> &b,
+                                       const Group<G> &g, RayCount &rc) {
+    V3<R> d = sub(b.p, from);
+    R d2 = dot(d, d);
+    if (d2 <= R(0))
+        return R(0);
+    V3<R> dir = dvs(d, M<R>::sqrt(d2));
+    R c = M<R>::abs(dot(b.n, dir)) / d2;
+    if (c <= R(0))
+        return R(0);
+    ++rc.v;
+    return visible(S, from, b.p, g) ? c : R(0);
+}
+
+template <class R> struct Contrib {
+    V3<R> f;
+    R pi, u, v;
+};
+
+// eval_contribution (core/path.cpp:40-82)
+template <class R, int G, class P>
+__device__ Contrib<R> evaluate(const SceneView<R> &S, const P &path, int k, const Group<G> &g,
+                               RayCount &rc) {
+    Contrib<R> z;
+    z.f = mk(R(0), R(0), R(0));
+    z.pi = R(0);
+    z.u = R(0);
+    z.v = R(0);
+    if (k < 2)
+        return z;
+    Vx<R> last = path.get(k - 1);
+    if (last.emi < 0)
+        return z;
+    V3<R> w0 = pdir<R>(path, 0);
+    R ru, rv;
+    if (!cam_raster(S.cam, w0, ru, rv))
+        return z;
+    R imp = cam_importance(S.cam, w0);
+    V3<R> f = mk(imp, imp, imp);
+    Vx<R> prev = path.get(0);
+    Vx<R> a = prev;
+    for (int i = 0; i + 1 < k; ++i) {
+        Vx<R> b = path.get(i + 1);
+        if (i > 0 && a.emi >= 0)
+            return z;
+        R seg = a.spec ? area_conv(S, a.p, b, g, rc) : geom_term(S, a, b, g, rc);
+        if (seg <= R(0))
+            return z;
+        f = scl(f, seg);
+        if (i > 0) {
+            const MatD<R> m = S.mat[a.mat];
+            V3<R> wi = unit(sub(prev.p, a.p));
+            V3<R> wo = unit(sub(b.p, a.p));
+            V3<R> bf = a.spec ? spec_weight(m, wi, a.n, a.ev) : bsdf_f(m, wi, wo, a.n);
+            if (zero3(bf))
+                return z;
+            f = mul(f, bf);
+        }
+        prev = a;
+        a = b;
+    }
+    // a == last, prev == path[k-2]
+    V3<R> toward = unit(sub(prev.p, last.p));
+    if (dot(last.n, toward) <= R(0))
+        return z;
+    V3<R> le = S.emit[last.emi];
+    if (zero3(le))
+        return z;
+    f = mul(f, le);
+    R pi = lum(f);
+    if (!(pi > R(0)) || !M<R>::finite(pi))
+        return z;
+    z.f = f;
+    z.pi = pi;
+    z.u = ru;
+    z.v = rv;
+    return z;
+}
+
+// trace_eye_subpath (core/path.cpp:84-142) into pv[0..k-1]; tf = prod of
+// dir_pdf * area_conv (large_step t_forward, mutations.cpp:63-66).
+template <class R, int G, class RNG>
+__device__ bool trace_eye(const SceneView<R> &S, RNG &rng, int maxv, Vx<R> *pv, int &k,
+                          unsigned &sm, R &tf, const Group<G> &g, RayCount &rc) {
+    Vx<R> cv;
+    cv.p = S.cam.pos;
+    cv.n = S.cam.fwd;
+    cv.mat = -1;
+    cv.emi = -1;
+    cv.spec = false;
+    cv.ev = EV_NONE;
+    pv[0] = cv;
+    k = 1;
+    sm = 0;
+    tf = R(1);
+    if (maxv < 2)
+        return false;
+    R u = Unit<R>::draw(rng);
+    R v = Unit<R>::draw(rng);
+    V3<R> dir = cam_primary(S.cam, u, v);
+    R dpdf = cam_dir_pdf(S.cam, dir);
+    V3<R> o = S.cam.pos;
+    while (k < maxv) {
+        Hit<R> h;
+        ++rc.c;
+        if (!intersect(S, o, dir, h, g))
+            return false;
+        Vx<R> x;
+        x.p = h.p;
+        x.n = h.n;
+        x.mat = h.mat;
+        x.emi = h.emi;
+        const MatD<R> m = S.mat[h.mat];
+        x.spec = h.emi < 0 && (m.kind == MAT_MIRROR || m.kind == MAT_DIELECTRIC);
+        x.ev = EV_NONE;
+        tf *= dpdf * (M<R>::abs(dot(h.n, dir)) / (h.t * h.t));
+        pv[k] = x;
+        if (x.spec)
+            sm |= 1u << k;
+        ++k;
+        if (h.emi >= 0)
+            return true;
+        if (k >= maxv)
+            return false;
+        BS<R> bs;
+        if (!bsdf_sample(m, neg(dir), h.n, rng, bs) || bs.zero_thr)
+            return false;
+        pv[k - 1].ev = bs.ev;
+        o = h.p;
+        dir = bs.dir;
+        dpdf = bs.pdf;
+    }
+    return false;
+}
+
+// eye_path_density (core/path.cpp:144-170)
+template <class R, int G, class P>
+__device__ R eye_density(const SceneView<R> &S, const P &path, int k, const Group<G> &g, RayCount &rc) {
+    if (k < 2)
+        return R(0);
+    if (path.get(k - 1).emi < 0)
+        return R(0);
+    R p = cam_dir_pdf(S.cam, pdir<R>(path, 0));
+    if (p <= R(0))
+        return R(0);
+    Vx<R> prev = path.get(0);
+    Vx<R> a = path.get(1);
+    p *= area_conv(S, prev.p, a, g, rc);
+    for (int i = 1; i + 1 < k; ++i) {
+        if (a.emi >= 0)
+            return R(0);
+        Vx<R> b = path.get(i + 1);
+        const MatD<R> m = S.mat[a.mat];
+        V3<R> wi = unit(sub(prev.p, a.p));
+        V3<R> wo = unit(sub(b.p, a.p));
+        R q = a.spec ? spec_prob(m, wi, a.n, a.ev) : bsdf_pdf(m, wi, wo, a.n);
+        if (q <= R(0))
+            return R(0);
+        p *= q * area_conv(S, a.p, b, g, rc);
+        if (p <= R(0))
+            return R(0);
+        prev = a;
+        a = b;
+    }
+    return p;
+}
+
+// ---- mutation structure from (k, specular mask) -------------------------------------------
+// lens_eligibility (core/mutations.cpp:9-21): endpoint or -1
+__device__ __forceinline__ int lens_endpoint(int k, unsigned sm) {
+    if (k < 2)
+        return -1;
+    int s = 1;
+    while (s < k - 1 && ((sm >> s) & 1u))
+        ++s;
+    if (s == k - 1)
+        return s;
+    if (!((sm >> (s + 1)) & 1u))
+        return s;
+    return -1;
+}
+
+// multichain_eligibility (core/mutations.cpp:23-45): returns false when
+// ineligible; first = first non-specular after the camera; pmask = perturbed set.
+__device__ __forceinline__ bool mc_structure(int k, unsigned sm, int &first, int &endpoint,
+                                             unsigned &pmask) {
+    if (k < 3)
+        return false;
+    int f = 1;
+    while (f < k - 1 && ((sm >> f) & 1u))
+        ++f;
+    if (f == k - 1)
+        return false;
+    int e = -1;
+    for (int i = f + 1; i < k; ++i) {
+        if (i == k - 1 || (!((sm >> i) & 1u) && !((sm >> (i + 1)) & 1u))) {
+            e = i;
+            break;
+        }
+    }
+    first = f;
+    endpoint = e;
+    unsigned below = e >= 32 ? 0xffffffffu : ((1u << e) - 1u);
+    pmask = ~sm & below;
+    return true;
+}
+
+__device__ __forceinline__ float suit_of(int pk, int k, unsigned sm) {
+    if (pk == 0)
+        return lens_endpoint(k, sm) >= 0 ? 0.5f : 0.0f;
+    int f, e;
+    unsigned pm;
+    return mc_structure(k, sm, f, e, pm) ? 0.5f : 0.0f;
+}
+
+// retrace_chain (core/mutations.cpp:78-110): pv[start+1..end] re-traced from o along d.
+template <class R, int G>
+__device__ bool retrace(const SceneView<R> &S, const CurPath<R> &ref, int kref, int start, int end,
+                        V3<R> o, V3<R> d, Vx<R> *pv, const Group<G> &g, RayCount &rc) {
+    for (int i = start + 1; i <= end; ++i) {
+        Hit<R> h;
+        ++rc.c;
+        if (!intersect(S, o, d, h, g))
+            return false;
+        Vx<R> r = ref.get(i);
+        const MatD<R> m = S.mat[h.mat];
+        bool he = h.emi >= 0;
+        bool hs = !he && (m.kind == MAT_MIRROR || m.kind == MAT_DIELECTRIC);
+        if (he != (r.emi >= 0) || hs != r.spec)
+            return false;
+        Vx<R> x;
+        x.p = h.p;
+        x.n = h.n;
+        x.mat = h.mat;
+        x.emi = h.emi;
+        x.spec = hs;
+        x.ev = r.ev;
+        pv[i] = x;
+        if (i == end)
+            break;
+        V3<R> c;
+        if (!spec_cont(m, neg(d), h.n, r.ev, c))
+            return false;
+        o = h.p;
+        d = c;
+    }
+    (void)kref;
+    return true;
+}
+
+// perturbation_density (core/mutations.cpp:176-196)
+template <class R, class PF, class PT>
+__device__ R pert_density(const PF &from, const PT &to, unsigned pmask, int endpoint,
+                          const Kern<R> &k1, const Kern<R> &k2) {
+    R q = R(1);
+    unsigned m = pmask;
+    while (m) {
+        int idx = __ffs(m) - 1;
+        m &= m - 1;
+        V3<R> a = pdir<R>(from, idx);
+        V3<R> b = pdir<R>(to, idx);
+        R alpha = M<R>::atan2(len(cross(a, b)), dot(a, b));
+        q *= kern_pdf_sa(idx == 0 ? k1 : k2, alpha);
+    }
+    Vx<R> p0 = to.get(0);
+    for (int i = 0; i < endpoint; ++i) {
+        Vx<R> p1 = to.get(i + 1);
+        V3<R> d = sub(p1.p, p0.p);
+        R d2 = dot(d, d);
+        if (d2 <= R(0))
+            return R(0);
+        q *= M<R>::abs(dot(p1.n, d)) / (d2 * M<R>::sqrt(d2));
+        p0 = p1;
+    }
+    return q;
+}
+
+// mh_accept (core/mutations.cpp:198-208); pi_current > 0 holds for every chain.
+template <class R> __device__ __forceinline__ R mh_accept(R pc, R pp, R tf, R tr, R sf, R sr) {
+    if (!(pp > R(0)) || !(tf > R(0)) || !(sf > R(0)))
+        return R(0);
+    R r = (pp * tr * sr) / (pc * tf * sf);
+    if (M<R>::isnan(r))
+        return R(0);
+    return r < R(1) ? r : R(1);
+}
+
+// ---- partitions (core/partition.cpp) --------------------------------------------------------
+template <class R> __device__ __forceinline__ int grid_cell(int n, R u, R v) {
+    int ix = min(static_cast<int>(u * R(n)), n - 1);
+    int iy = min(static_cast<int>(v * R(n)), n - 1);
+    return iy * n + ix;
+}
+
+template <class R> __device__ __forceinline__ int descend(const NodeD *nodes, int root, R u, R v) {
+    NodeD nd = nodes[root];
+    while (nd.child >= 0) {
+        R sc = M<R>::ldexp(R(1), -nd.level);
+        R mu = (R(nd.ix) + R(0.5)) * sc;
+        R mv = (R(nd.iy) + R(0.5)) * sc;
+        int q = (u >= mu ? 1 : 0) + (v >= mv ? 2 : 0);
+        nd = nodes[nd.child + q];
+    }
+    return nd.region;
+}
+
+template <class R> __device__ __forceinline__ int classify(const PartView &p, R ru, R rv, R cu, R cv) {
+    switch (p.kind) {
+    case 1: return grid_cell(p.ntop, ru, rv);
+    case 2: return descend(p.nodes, 0, ru, rv);
+    case 3: return grid_cell(p.ntop, ru, rv) * (p.nbot * p.nbot) + grid_cell(p.nbot, cu, cv);
+    case 4: return descend(p.nodes, p.roots[grid_cell(p.ntop, ru, rv)], cu, cv);
+    }
+    return 0;
+}
+
+// ---- splat (core/driver.cpp:59-64; core/film.cpp:12-20) ------------------------------------
+template <class R>
+__device__ __forceinline__ void film_add(const StepParams<R> &P, R u, R v, V3<R> val, double &lum_acc);
+
+template <>
+__device__ __forceinline__ void film_add<double>(const StepParams<double> &P, double u, double v,
+                                                 V3<double> val, double &lum_acc) {
+    int x = min(static_cast<int>(u * P.W), P.W - 1);
+    int row = P.H - 1 - min(static_cast<int>(v * P.H), P.H - 1);
+    double *px = &P.film64[(static_cast<size_t>(row) * P.W + x) * 3];
+    atomicAdd(px + 0, val.x);
+    atomicAdd(px + 1, val.y);
+    atomicAdd(px + 2, val.z);
+    lum_acc += lum(val);
+}
+
+template <>
+__device__ __forceinline__ void film_add<float>(const StepParams<float> &P, float u, float v,
+                                                V3<float> val, double &lum_acc) {
+    int x = min(static_cast<int>(u * P.W), P.W - 1);
+    int row = P.H - 1 - min(static_cast<int>(v * P.H), P.H - 1);
+    atomicAdd(&P.film32[static_cast<size_t>(row) * P.W + x], make_float4(val.x, val.y, val.z, 0.f));
+    lum_acc += static_cast<double>(lum(val));
+}
+
+// ---- scene staging ------------------------------------------------------------------------
+template <class R> __device__ __forceinline__ size_t stage_bytes_sph(int nsph) {
+    return (static_cast<size_t>(nsph) * sizeof(SphD<R>) + 15) & ~size_t(15);
+}
+
+template <class R> __device__ SceneView<R> stage_scene(const SceneView<R> &g, char *smem) {
+    SceneView<R> s = g;
+    size_t bs = static_cast<size_t>(g.nsph) * sizeof(SphD<R>);
+    size_t bt = static_cast<size_t>(g.ntri) * sizeof(TriD<R>);
+    size_t off = stage_bytes_sph<R>(g.nsph);
+    const unsigned *src_s = reinterpret_cast<const unsigned *>(g.sph);
+    const unsigned *src_t = reinterpret_cast<const unsigned *>(g.tri);
+    unsigned *dst_s = reinterpret_cast<unsigned *>(smem);
+    unsigned *dst_t = reinterpret_cast<unsigned *>(smem + off);
+    for (size_t i = threadIdx.x; i < bs / 4; i += blockDim.x)
+        dst_s[i] = __ldg(src_s + i);
+    for (size_t i = threadIdx.x; i < bt / 4; i += blockDim.x)
+        dst_t[i] = __ldg(src_t + i);
+    __syncthreads();
+    s.sph = reinterpret_cast<const SphD<R> *>(smem);
+    s.tri = reinterpret_cast<const TriD<R> *>(smem + off);
+    return s;
+}
+
+// ---- the chain-step megakernel --------------------------------------------------------------
+template <class R> struct ChainRegs {
+    int k;
+    unsigned sm;
+    V3<R> f;
+    R pi, ru, rv, eyeden;
+    double acc, iacc, lum;
+    unsigned long long npert, nlarge, ipert, nsteps;
+};
+
+template <int RK> struct RngIO;
+template <> struct RngIO<RNG_PCG> {
+    static __device__ __forceinline__ void load(Rng<RNG_PCG> &r, const unsigned long long *a,
+                                                const unsigned long long *b, int c, unsigned long long,
+                                                unsigned long long) {
+        r.state = a[c];
+        r.inc = b[c];
+    }
+    static __device__ __forceinline__ void store(const Rng<RNG_PCG> &r, unsigned long long *a,
+                                                 unsigned long long *b, int c) {
+        a[c] = r.state;
+        b[c] = r.inc;
+    }
+};
+template <> struct RngIO<RNG_PHILOX> {
+    static __device__ __forceinline__ void load(Rng<RNG_PHILOX> &r, const unsigned long long *a,
+                                                const unsigned long long *, int c, unsigned long long seed,
+                                                unsigned long long stream) {
+        r.reseed(seed, stream);
+        r.draw = a[c];
+    }
+    static __device__ __forceinline__ void store(const Rng<RNG_PHILOX> &r, unsigned long long *a,
+                                                 unsigned long long *, int c) {
+        a[c] = r.draw;
+    }
+};
+
+// One mutation of one chain: core/driver.cpp:113-171.
+template <class R, int RK, int G>
+__device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, long long gc,
+                       unsigned long long index, ChainRegs<R> &cs, Rng<RK> &rng, const Group<G> &g,
+                       RayCount &rc) {
+    CurPath<R> cur{P.ch.verts, P.C, c, &S.cam};
+    Vx<R> pv[kMaxV];
+    int head_end = 0;
+    int kp = cs.k;
+    unsigned smp = cs.sm;
+    R tf = R(0), tr = R(0);
+    const int pk = P.pk;
+
+    // suitability (core/mutations.cpp:47-56)
+    int e_lens = -1, first = 0, endpoint = 0;
+    unsigned pmask = 0;
+    bool elig;
+    if (pk == 0) {
+        e_lens = lens_endpoint(cs.k, cs.sm);
+        elig = e_lens >= 0;
+        endpoint = e_lens;
+        pmask = 1u;
+    } else {
+        elig = mc_structure(cs.k, cs.sm, first, endpoint, pmask);
+    }
+    const R s_pert = elig ? R(0.5) : R(0);
+    const bool choose = elig && Unit<R>::draw(rng) < s_pert;
+
+    R a = R(0);
+    Contrib<R> pc;
+    pc.pi = R(0);
+    int region = -1;
+
+    if (choose) {
+        // classify_path (core/driver.cpp:95-107)
+        R cu = R(0), cv = R(0);
+        if (P.ctl == 2 && pk == 1)
+            cylindrical(pdir<R>(cur, first), cu, cv);
+        region = P.ctl == 2 ? classify(P.part, cs.ru, cs.rv, cu, cv) : 0;
+        const KernTab<R> kt = P.ktab[region];
+        // lens_perturb / multichain_perturb (core/mutations.cpp:122-174)
+        Vx<R> cam0 = cur.get(0);
+        pv[0] = cam0;
+        bool ok = true;
+        unsigned m = pmask;
+        while (m) {
+            int idx = __ffs(m) - 1;
+            m &= m - 1;
+            int next = m ? (__ffs(m) - 1) : endpoint;
+            V3<R> nd = perturb_dir(pdir<R>(cur, idx), idx == 0 ? kt.k1 : kt.k2, rng);
+            if (!retrace(S, cur, cs.k, idx, next, pv[idx].p, nd, pv, g, rc)) {
+                ok = false;
+                break;
+            }
+        }
+        if (ok) {
+            head_end = endpoint;
+            PropPath<R> prop{pv, head_end, &cur};
+            tf = pert_density(cur, prop, pmask, endpoint, kt.k1, kt.k2);
+            tr = pert_density(prop, cur, pmask, endpoint, kt.k1, kt.k2);
+            pc = evaluate(S, prop, cs.k, g, rc);
+            if (pc.pi > R(0)) {
+                if (P.ctl == 2) {
+                    R pu = R(0), pv_ = R(0);
+                    if (pk == 1)
+                        cylindrical(pdir<R>(prop, first), pu, pv_);
+                    int preg = classify(P.part, pc.u, pc.v, pu, pv_);
+                    const KernTab<R> kr = P.ktab[preg];
+                    tr = pert_density(prop, cur, pmask, endpoint, kr.k1, kr.k2);
+                }
+                a = mh_accept(cs.pi, pc.pi, tf, tr, s_pert, s_pert);
+            }
+        }
+        if (g.lane == 0 && P.ctl == 2)
+            atomicAdd(&P.part.visits[region], 1ull);
+        cs.acc += static_cast<double>(a);
+        cs.iacc += static_cast<double>(a);
+        ++cs.npert;
+        ++cs.ipert;
+    } else {
+        ++cs.nlarge;
+        // large_step (core/mutations.cpp:58-71)
+        if (trace_eye(S, rng, P.maxv, pv, kp, smp, tf, g, rc)) {
+            head_end = kp - 1;
+            PropPath<R> prop{pv, head_end, &cur};
+            pc = evaluate(S, prop, kp, g, rc);
+            if (pc.pi > R(0)) {
+                if (!(cs.eyeden == cs.eyeden))   // NaN: not cached yet
+                    cs.eyeden = eye_density(S, cur, cs.k, g, rc);
+                tr = cs.eyeden;
+                R sx = R(1) - s_pert;
+                R sy = R(1) - R(suit_of(pk, kp, smp));
+                a = mh_accept(cs.pi, pc.pi, tf, tr, sx, sy);
+            }
+        }
+    }
+
+    // splat (core/driver.cpp:59-64) -- the group leader writes
+    if (g.lane == 0) {
+        if (a < R(1) && cs.pi > R(0))
+            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - a) / cs.pi), cs.lum);
+        if (pc.pi > R(0) && a > R(0))
+            film_add(P, pc.u, pc.v, scl(pc.f, a / pc.pi), cs.lum);
+    } else {
+        // keep the lum accumulator identical on all lanes (leader's value is stored)
+    }
+
+    // accept / commit (core/driver.cpp:168-171)
+    bool accepted = false;
+    if (a > R(0) && Unit<R>::draw(rng) < a) {
+        accepted = true;
+        if (g.lane == 0)
+            for (int i = 1; i <= head_end; ++i)
+                store_gv(&P.ch.verts[static_cast<size_t>(i - 1) * P.C + c], pv[i]);
+        cs.k = kp;
+        cs.sm = choose ? cs.sm : smp;
+        cs.f = pc.f;
+        cs.pi = pc.pi;
+        cs.ru = pc.u;
+        cs.rv = pc.v;
+        cs.eyeden = M<R>::inf() - M<R>::inf();   // NaN
+    }
+
+    if (g.lane == 0) {
+        if (cs.nsteps < P.ch.log_K) {
+            size_t o = static_cast<size_t>(cs.nsteps) * P.C + c;
+            P.ch.log_a[o] = static_cast<double>(a);
+            P.ch.log_f[o] = static_cast<unsigned char>((accepted ? 1 : 0) | (choose ? 2 : 0) | 4);
+        }
+        if (P.record_visits) {
+            P.ch.vreg[c] = (choose && P.ctl != 0) ? region : -1;
+            P.ch.va[c] = static_cast<double>(a);
+        }
+    }
+    ++cs.nsteps;
+    (void)gc;
+    (void)index;
+}
+
+template <class R, int RK, int G>
+__global__ void __launch_bounds__(128) k_step(StepParams<R> P) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    Group<G> g;
+    const int c = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / G);
+    if (c >= P.C)
+        return;
+    const long long gc = P.chain_off + c;
+    const unsigned long long my_steps = P.per + (static_cast<unsigned long long>(gc) < P.rem ? 1ull : 0ull);
+
+    ChainRegs<R> cs;
+    cs.k = P.ch.klen[c];
+    cs.sm = P.ch.smask[c];
+    cs.f = mk(P.ch.cf[c], P.ch.cf[P.C + c], P.ch.cf[2 * P.C + c]);
+    cs.pi = P.ch.cf[3 * P.C + c];
+    cs.ru = P.ch.cr[c];
+    cs.rv = P.ch.cr[P.C + c];
+    cs.eyeden = P.ch.eyeden[c];
+    cs.acc = P.ch.acc[c];
+    cs.iacc = P.ch.iacc[c];
+    cs.lum = P.ch.lum[c];
+    cs.npert = P.ch.npert[c];
+    cs.nlarge = P.ch.nlarge[c];
+    cs.ipert = P.ch.ipert[c];
+    cs.nsteps = P.ch.nsteps[c];
+    Rng<RK> rng;
+    RngIO<RK>::load(rng, P.ch.rng0, P.ch.rng1, c, P.seed, static_cast<unsigned long long>(gc));
+    RayCount rc;
+
+    for (int j = P.j0; j < P.j1; ++j) {
+        if (static_cast<unsigned long long>(j) >= my_steps) {
+            if (P.record_visits && g.lane == 0)
+                P.ch.vreg[c] = -1;
+            break;
+        }
+        unsigned long long index = P.span_start + static_cast<unsigned long long>(j) * P.C_total + gc;
+        mutate<R, RK, G>(P, S, c, gc, index, cs, rng, g, rc);
+    }
+
+    if (g.lane == 0) {
+        P.ch.klen[c] = cs.k;
+        P.ch.smask[c] = cs.sm;
+        P.ch.cf[c] = cs.f.x;
+        P.ch.cf[P.C + c] = cs.f.y;
+        P.ch.cf[2 * P.C + c] = cs.f.z;
+        P.ch.cf[3 * P.C + c] = cs.pi;
+        P.ch.cr[c] = cs.ru;
+        P.ch.cr[P.C + c] = cs.rv;
+        P.ch.eyeden[c] = cs.eyeden;
+        P.ch.acc[c] = cs.acc;
+        P.ch.iacc[c] = cs.iacc;
+        P.ch.lum[c] = cs.lum;
+        P.ch.npert[c] = cs.npert;
+        P.ch.nlarge[c] = cs.nlarge;
+        P.ch.ipert[c] = cs.ipert;
+        P.ch.nsteps[c] = cs.nsteps;
+        RngIO<RK>::store(rng, P.ch.rng0, P.ch.rng1, c);
+        // warp-aggregated ray counters
+    }
+    unsigned long long rcc = g.lane == 0 ? rc.c : 0ull, rcv = g.lane == 0 ? rc.v : 0ull;
+    unsigned act = __activemask();
+    for (int off = 16; off > 0; off >>= 1) {
+        rcc += __shfl_down_sync(act, rcc, off);
+        rcv += __shfl_down_sync(act, rcv, off);
+    }
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+        atomicAdd(&P.ch.rays[0], rcc);
+        atomicAdd(&P.ch.rays[1], rcv);
+    }
+}
+
+// ---- chain initialisation (core/driver.cpp:219-242) -----------------------------------------
+template <class R, int RK>
+__global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long long max_attempts) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    Group<1> g;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P.C)
+        return;
+    const long long gc = P.chain_off + c;
+    Rng<RK> init;
+    init.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(gc) * 2ull);
+    Vx<R> pv[kMaxV];
+    RayCount rc;
+    bool ok = false;
+    for (unsigned long long t = 0; t < max_attempts; ++t) {
+        int k;
+        unsigned sm;
+        R tf;
+        if (!trace_eye(S, init, P.maxv, pv, k, sm, tf, g, rc))
+            continue;
+        CurPath<R> dummy{P.ch.verts, P.C, c, &S.cam};
+        PropPath<R> path{pv, k - 1, &dummy};
+        Contrib<R> con = evaluate(S, path, k, g, rc);
+        if (con.pi > R(0)) {
+            for (int i = 1; i < k; ++i)
+                store_gv(&P.ch.verts[static_cast<size_t>(i - 1) * P.C + c], pv[i]);
+            P.ch.klen[c] = k;
+            P.ch.smask[c] = sm;
+            P.ch.cf[c] = con.f.x;
+            P.ch.cf[P.C + c] = con.f.y;
+            P.ch.cf[2 * P.C + c] = con.f.z;
+            P.ch.cf[3 * P.C + c] = con.pi;
+            P.ch.cr[c] = con.u;
+            P.ch.cr[P.C + c] = con.v;
+            ok = true;
+            break;
+        }
+    }
+    if (!ok)
+        atomicExch(P.ch.err, 1);
+    P.ch.eyeden[c] = M<R>::inf() - M<R>::inf();
+    P.ch.acc[c] = 0.0;
+    P.ch.iacc[c] = 0.0;
+    P.ch.lum[c] = 0.0;
+    P.ch.npert[c] = 0;
+    P.ch.nlarge[c] = 0;
+    P.ch.ipert[c] = 0;
+    P.ch.nsteps[c] = 0;
+    Rng<RK> rng;
+    rng.reseed(P.seed, static_cast<unsigned long long>(gc));
+    RngIO<RK>::store(rng, P.ch.rng0, P.ch.rng1, c);
+}
+
+// ---- estimate_b substreams (core/driver.cpp:31-57) --------------------------------------------
+template <class R, int RK>
+__global__ void __launch_bounds__(128) k_bsub(StepParams<R> P, unsigned long long n_samples,
+                                              unsigned long long S_total, unsigned long long s_begin,
+                                              unsigned long long s_end, double *partials) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    Group<1> g;
+    unsigned long long s = s_begin + blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+    if (s >= s_end)
+        return;
+    Rng<RK> rng;
+    rng.reseed(P.seed, kStreamB + 2ull * s);
+    Vx<R> pv[kMaxV];
+    RayCount rc;
+    double sum = 0.0, sq = 0.0;
+    for (unsigned long long j = s; j < n_samples; j += S_total) {
+        int k;
+        unsigned sm;
+        R tf;
+        double v = 0.0;
+        if (trace_eye(S, rng, P.maxv, pv, k, sm, tf, g, rc)) {
+            CurPath<R> dummy{P.ch.verts, P.C, 0, &S.cam};
+            PropPath<R> path{pv, k - 1, &dummy};
+            Contrib<R> con = evaluate(S, path, k, g, rc);
+            if (con.pi > R(0)) {
+                if (tf > R(0))
+                    v = static_cast<double>(con.pi / tf);
+            }
+        }
+        sum += v;
+        sq += v * v;
+    }
+    partials[2 * (s - s_begin)] = sum;
+    partials[2 * (s - s_begin) + 1] = sq;
+}
+
+// ---- adaptation ------------------------------------------------------------------------------
+// step_size / update_lambda (core/adaptation.cpp:10-20)
+__device__ __forceinline__ double lambda_next(double lam, double ah, unsigned long long n, const AdaptCfg &c) {
+    double gs = c.gscale / ::sqrt(static_cast<double>(n));
+    double gm = c.gmax < gs ? c.gmax : gs;
+    double diff = ah - c.target;
+    double sg = diff > 0.0 ? 1.0 : (diff < 0.0 ? -1.0 : 0.0);
+    double nl = lam + gm * sg;
+    return c.lmin > nl ? c.lmin : nl;
+}
+
+template <class R> __device__ __forceinline__ void set_ktab(KernTab<R> *kt, double lambda, double ratio) {
+    // sigma_for (core/adaptation.cpp:44-50) + AngularKernel ctor in fp64, stored as R
+    double s = ::exp(0.5 * lambda);
+    Kern<double> a = make_kern<double>(s);
+    Kern<double> b = make_kern<double>(ratio * s);
+    KernTab<R> t;
+    t.k1.sigma = static_cast<R>(a.sigma);
+    t.k1.lo = static_cast<R>(a.lo);
+    t.k1.mass = static_cast<R>(a.mass);
+    t.k2.sigma = static_cast<R>(b.sigma);
+    t.k2.lo = static_cast<R>(b.lo);
+    t.k2.mass = static_cast<R>(b.mass);
+    *kt = t;
+}
+
+template <class R>
+__global__ void k_ktab_init(KernTab<R> *kt, const double *lambda, int n, double ratio) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        set_ktab(&kt[i], lambda[i], ratio);
+}
+
+__device__ __forceinline__ void trace_push(const TraceBuf &tb, unsigned long long index, int region,
+                                           unsigned long long n, double lam, double ah) {
+    unsigned long long slot = atomicAdd(tb.count, 1ull);
+    if (slot < tb.cap) {
+        tb.index[slot] = index;
+        tb.region[slot] = region;
+        tb.n[slot] = n;
+        tb.lambda[slot] = lam;
+        tb.alpha[slot] = ah;
+    }
+}
+
+// Literal rule: record_acceptance in canonical (lockstep step, chain) order.
+// One block; tiles of 1024 chains in order; each tile stable-sorted by region
+// so every region's visits form a run processed sequentially by one thread.
+template <class R>
+__global__ void __launch_bounds__(1024) k_adapt_literal(const int *vreg, const double *va, int C,
+                                                        long long chain_off, long long C_total,
+                                                        unsigned long long span_start, int j,
+                                                        RegionArrays ra, KernTab<R> *ktab, AdaptCfg cfg,
+                                                        TraceBuf tb) {
+    typedef cub::BlockRadixSort<int, 1024, 1, int> Sort;
+    __shared__ typename Sort::TempStorage tmp;
+    __shared__ int keys_s[1024];
+    __shared__ int vals_s[1024];
+    for (int base = 0; base < C; base += 1024) {
+        int t = threadIdx.x;
+        int cidx = base + t;
+        int key[1], val[1];
+        key[0] = (cidx < C && vreg[cidx] >= 0) ? vreg[cidx] : 0x7fffffff;
+        val[0] = cidx;
+        Sort(tmp).Sort(key, val);
+        // BlockRadixSort with 1 item/thread leaves thread t holding rank t
+        keys_s[t] = key[0];
+        vals_s[t] = val[0];
+        __syncthreads();
+        int r = keys_s[t];
+        bool head = r != 0x7fffffff && (t == 0 || keys_s[t - 1] != r);
+        if (head) {
+            double lam = ra.lambda[r];
+            unsigned long long n = ra.n[r];
+            unsigned int pn = ra.pend_n[r];
+            double ps = ra.pend_sum[r];
+            unsigned long long tv = ra.tot_vis[r];
+            double ta = ra.tot_acc[r];
+            bool changed = false;
+            for (int q = t; q < 1024 && keys_s[q] == r; ++q) {
+                int ci = vals_s[q];
+                double a = va[ci];
+                ta += a;
+                tv += 1;
+                ps += a;
+                pn += 1;
+                if (pn < static_cast<unsigned int>(cfg.L))
+                    continue;
+                double ah = ps / pn;
+                ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
+                unsigned long long n0 = n;
+                lam = lambda_next(lam, ah, n0, cfg);
+                n = n0 + 1;
+                pn = 0;
+                ps = 0.0;
+                changed = true;
+                if (cfg.trace)
+                    trace_push(tb, span_start + static_cast<unsigned long long>(j) * C_total + chain_off + ci,
+                               r, n0, lam, ah);
+            }
+            ra.lambda[r] = lam;
+            ra.n[r] = n;
+            ra.pend_n[r] = pn;
+            ra.pend_sum[r] = ps;
+            ra.tot_vis[r] = tv;
+            ra.tot_acc[r] = ta;
+            if (changed)
+                set_ktab(&ktab[r], lam, cfg.ratio);
+        }
+        __syncthreads();
+    }
+}
+
+// Pooled rule, phase 1: per-region visit counts / fixed-point sums / last
+// index, warp-aggregated over lanes that share a region.
+__device__ __forceinline__ unsigned long long to_fx(double a) {
+    return static_cast<unsigned long long>(a * 16777216.0 + 0.5);   // 2^-24 resolution
+}
+
+__global__ void k_adapt_pool_accum(const int *vreg, const double *va, int C, long long chain_off,
+                                   long long C_total, unsigned long long span_start, int j, RegionArrays ra) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    int r = (c < C) ? vreg[c] : -1;
+    unsigned act = __ballot_sync(0xffffffffu, r >= 0);
+    if (r < 0)
+        return;
+    unsigned peers = __match_any_sync(act, r);
+    unsigned long long fx = to_fx(va[c]);
+    unsigned long long idx = span_start + static_cast<unsigned long long>(j) * C_total + chain_off + c;
+    // reduce over peers
+    unsigned fx32 = static_cast<unsigned>(fx);   // <= 2^24, 32 lanes <= 2^29
+    unsigned s = __reduce_add_sync(peers, fx32);
+    unsigned cnt = __popc(peers);
+    int leader = __ffs(peers) - 1;
+    int hi = 31 - __clz(peers);
+    unsigned long long last = __shfl_sync(peers, idx, hi);
+    if ((threadIdx.x & 31) == leader) {
+        atomicAdd(&ra.x_cnt[r], static_cast<unsigned long long>(cnt));
+        atomicAdd(&ra.x_fx[r], static_cast<unsigned long long>(s));
+        atomicMax(&ra.x_last[r], last);
+        if (atomicExch(&ra.x_touched[r], 1u) == 0u) {
+            unsigned slot = atomicAdd(ra.n_touched, 1u);
+            ra.touched_list[slot] = static_cast<unsigned>(r);
+        }
+    }
+}
+
+// Pooled rule, phase 2: one update per touched region.
+template <class R>
+__global__ void k_adapt_pool_apply(RegionArrays ra, KernTab<R> *ktab, AdaptCfg cfg, TraceBuf tb) {
+    unsigned nt = *ra.n_touched;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += gridDim.x * blockDim.x) {
+        int r = static_cast<int>(ra.touched_list[i]);
+        unsigned long long cnt = ra.x_cnt[r], fx = ra.x_fx[r], last = ra.x_last[r];
+        ra.x_cnt[r] = 0;
+        ra.x_fx[r] = 0;
+        ra.x_last[r] = 0;
+        ra.x_touched[r] = 0;
+        ra.tot_vis[r] += cnt;
+        ra.tot_fx[r] += fx;
+        unsigned long long pn = ra.pend_n[r] + cnt;
+        unsigned long long pf = ra.pend_fx[r] + fx;
+        if (pn < static_cast<unsigned long long>(cfg.L)) {
+            ra.pend_n[r] = static_cast<unsigned>(pn);
+            ra.pend_fx[r] = pf;
+            continue;
+        }
+        double ah = static_cast<double>(pf) / 16777216.0 / static_cast<double>(pn);
+        ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
+        unsigned long long n0 = ra.n[r];
+        double lam = lambda_next(ra.lambda[r], ah, n0, cfg);
+        ra.lambda[r] = lam;
+        ra.n[r] = n0 + 1;
+        ra.pend_n[r] = 0;
+        ra.pend_fx[r] = 0;
+        set_ktab(&ktab[r], lam, cfg.ratio);
+        if (cfg.trace)
+            trace_push(tb, last, r, n0, lam, ah);
+    }
+}
+
+__global__ void k_reset_touched(unsigned *n_touched) { *n_touched = 0; }
+
+// ---- quadtree refinement (single thread; core/partition.cpp:68-100, 217-227) ---------------------
+template <class R>
+__global__ void k_refine(NodeD *nodes, int *n_nodes, int cap_nodes, int n_trees, int *scratch_cnt,
+                         int *scratch_list, RegionArrays ra, KernTab<R> *ktab,
+                         unsigned long long *visits, int *n_regions, int cap_regions,
+                         unsigned long long m_split, int *err, int *splits_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0)
+        return;
+    const int n0 = *n_nodes;
+    for (int t = 0; t < n_trees; ++t)
+        scratch_cnt[t] = 0;
+    // snapshot of candidate leaves, grouped tree-major, node order inside a tree
+    for (int i = 0; i < n0; ++i) {
+        NodeD nd = nodes[i];
+        if (nd.child < 0 && nd.level < 16 && visits[nd.region] >= m_split)
+            scratch_cnt[nd.tree]++;
+    }
+    int acc = 0;
+    for (int t = 0; t < n_trees; ++t) {
+        int c = scratch_cnt[t];
+        scratch_cnt[t] = acc;
+        acc += c;
+    }
+    for (int i = 0; i < n0; ++i) {
+        NodeD nd = nodes[i];
+        if (nd.child < 0 && nd.level < 16 && visits[nd.region] >= m_split)
+            scratch_list[scratch_cnt[nd.tree]++] = i;
+    }
+    int nn = n0, nr = *n_regions, splits = 0;
+    for (int s = 0; s < acc; ++s) {
+        int idx = scratch_list[s];
+        NodeD nd = nodes[idx];
+        if (nn + 4 > cap_nodes || nr + 4 > cap_regions) {
+            *err = 2;
+            break;
+        }
+        unsigned long long np = ra.n[nd.region];
+        double lam = ra.lambda[nd.region];
+        unsigned long long nc = np / 4 > 1 ? np / 4 : 1;
+        for (int q = 0; q < 4; ++q) {
+            NodeD ch;
+            ch.level = nd.level + 1;
+            ch.ix = nd.ix * 2 + (q & 1);
+            ch.iy = nd.iy * 2 + (q >> 1);
+            ch.child = -1;
+            ch.tree = nd.tree;
+            ch.region = nr;
+            ra.lambda[nr] = lam;
+            ra.n[nr] = nc;
+            ra.pend_n[nr] = 0;
+            ra.pend_sum[nr] = 0.0;
+            ra.pend_fx[nr] = 0;
+            ra.tot_vis[nr] = 0;
+            ra.tot_acc[nr] = 0.0;
+            ra.tot_fx[nr] = 0;
+            visits[nr] = 0;
+            ktab[nr] = ktab[nd.region];
+            nodes[nn + q] = ch;
+            ++nr;
+        }
+        nodes[idx].child = nn;
+        visits[nd.region] = 0;
+        nn += 4;
+        ++splits;
+    }
+    *n_nodes = nn;
+    *n_regions = nr;
+    *splits_out = splits;
+}
+
+// ---- reductions & film ---------------------------------------------------------------------
+// Fixed-order two-level reduction of per-chain tallies: block b sums chains
+// [b*256, (b+1)*256) by a shared-memory tree; the host-side caller finishes
+// in block order.  out[b*6 + 0..5] = acc, iacc, lum, npert, nlarge, ipert.
+__global__ void k_reduce_chains(const double *acc, double *iacc, const double *lum,
+                                const unsigned long long *npert, const unsigned long long *nlarge,
+                                unsigned long long *ipert, int C, int reset_interval, double *out) {
+    __shared__ double s[6][256];
+    int c = blockIdx.x * 256 + threadIdx.x;
+    bool in = c < C;
+    s[0][threadIdx.x] = in ? acc[c] : 0.0;
+    s[1][threadIdx.x] = in ? iacc[c] : 0.0;
+    s[2][threadIdx.x] = in ? lum[c] : 0.0;
+    s[3][threadIdx.x] = in ? static_cast<double>(npert[c]) : 0.0;
+    s[4][threadIdx.x] = in ? static_cast<double>(nlarge[c]) : 0.0;
+    s[5][threadIdx.x] = in ? static_cast<double>(ipert[c]) : 0.0;
+    if (in && reset_interval) {
+        iacc[c] = 0.0;
+        ipert[c] = 0;
+    }
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w)
+            for (int q = 0; q < 6; ++q)
+                s[q][threadIdx.x] += s[q][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 6)
+        out[blockIdx.x * 6 + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_fold_film(float4 *stage, double *master, int npix) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npix)
+        return;
+    float4 v = stage[i];
+    master[3 * i + 0] += static_cast<double>(v.x);
+    master[3 * i + 1] += static_cast<double>(v.y);
+    master[3 * i + 2] += static_cast<double>(v.z);
+    stage[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void k_to_image(const double *film, float *img, int n, double scale) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n)
+        img[i] = static_cast<float>(film[i] * scale);
+}
+
+}  // namespace rd
