@@ -273,6 +273,30 @@ class OracleLib(_Lib):
 
     def __init__(self):
         super().__init__(ORACLE_SO)
+        L = self.lib
+        L.orc_normal_quantile.restype = C.c_double
+        L.orc_normal_quantile.argtypes = [C.c_double]
+        L.orc_angular_pdf.argtypes = [C.c_double, C.c_double, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]
+        L.orc_angular_sample.argtypes = [C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
+                                         C.POINTER(C.c_double), C.c_int]
+        L.orc_rng_u32.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint32), C.c_int]
+        L.orc_philox_block.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_uint32)]
+        L.orc_perturb_direction.argtypes = [C.POINTER(C.c_double), C.c_double, C.c_uint64,
+                                            C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]
+        L.orc_cylindrical.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.orc_update_lambda.restype = C.c_double
+        L.orc_update_lambda.argtypes = [C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
+        L.orc_grid_cell.restype = C.c_int
+        L.orc_grid_cell.argtypes = [C.c_int, C.c_double, C.c_double]
+        L.orc_mh_accept.restype = C.c_double
+        L.orc_mh_accept.argtypes = [C.c_double] * 6 + [C.POINTER(C.c_int)]
+        L.orc_fresnel.restype = C.c_double
+        L.orc_fresnel.argtypes = [C.c_double, C.c_double]
+        L.orc_camera.argtypes = [C.POINTER(C.c_double), C.c_int, C.c_int, C.c_double, C.c_double,
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]
 
 
 def dp(arr: np.ndarray):
