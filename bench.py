@@ -1,0 +1,338 @@
+"""Benchmark of the B200 MLT hot path (contract: see DESIGN.md §6).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1] [--impl ours|reference]
+
+One "step" = one lockstep mutation of every chain (C mutations).  Rank 0 prints
+ONE JSON line.  Under torchrun (N > 1) chains shard across ranks
+(paper_2402_08273_b200.distributed); timing is CUDA events on the engine's
+stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs; "strategy/perturbation" follow the
+# reference defaults (RA-quadtree) and the survey's per-config perturbation.
+WORKLOADS = {
+    "c3": dict(scene="caustic", chains=262144, steps_per_chain=1 << 16, width=512, height=512,
+               max_vertices=17, strategy="ra-quadtree", perturbation="multi-chain",
+               desc="C3 caustic box: 36 tri + glass sphere, 1% light, 512^2, path length 16, "
+                    "262,144 chains"),
+    "c1": dict(scene="cornell", chains=1024, steps_per_chain=1 << 20, width=256, height=256,
+               max_vertices=9, strategy="ra-quadtree", perturbation="lens",
+               desc="C1 Cornell box: 36 tri, 256^2, path length 8, 1,024 chains"),
+}
+METRIC = "MLT mutations/sec"
+UNIT = "mutations/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.strip() == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def oracle_rays_per_mutation(wl: dict, scene_text: str) -> float:
+    """R_m: reference-equivalent ray casts (closest-hit + visibility) per mutation,
+    counted by the CPU oracle on a small sample of the same variant and scene
+    (SURVEY.md §8(d))."""
+    from oracle.abi import OracleConfig, OracleLib
+    cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=64,
+                       mutations=64 * 300, width=wl["width"], height=wl["height"],
+                       max_vertices=wl["max_vertices"], b_samples=20000, seed=3, rng="philox",
+                       adapt_mode="pooled", m_refine=64 * 100, m_split=500)
+    o = OracleLib().render(scene_text, cfg)
+    return (o.stats.rays_closest + o.stats.rays_visibility) / max(o.stats.total_mutations, 1)
+
+
+def cpu_reference_run(wl: dict, scene_text: str, mutations: int, threads: int):
+    """The reference's own run_render (oracle/_ref, unmodified sources) on host
+    cores: chains = threads (one std::thread per chain, core/driver.cpp:282-297).
+    Falls back to the restatement oracle (single thread) when the reference
+    library was not built."""
+    from oracle.abi import OracleConfig, RefLib, OracleLib, REF_SO
+    cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=threads,
+                       mutations=mutations, width=wl["width"], height=wl["height"],
+                       max_vertices=wl["max_vertices"], b_samples=4096, seed=1,
+                       metrics_interval=mutations, m_refine=10_000_000)
+    if os.path.exists(REF_SO):
+        out = RefLib(log=False).render(scene_text, cfg)
+        kind, cores = "reference", threads
+    else:
+        cfg.chains = 1
+        out = OracleLib().render(scene_text, cfg)
+        kind, cores = "port", 1
+    t = out.stats.loop_time_s
+    return out.stats.total_mutations / t, kind, cores, t, cfg.chains
+
+
+def run_ours(args, wl, scene_text):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2402_08273_b200 import Engine, RenderConfig
+    from paper_2402_08273_b200.distributed import ShardPlan, exchange_adaptation, all_gather_b
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    C = wl["chains"]
+    plan = ShardPlan(C, world, rank)
+    total_steps = args.warmup + args.steps
+    stream = torch.cuda.current_stream()
+    cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=plan.count,
+                       chains_total=C, chain_offset=plan.offset,
+                       mutations=C * wl["steps_per_chain"], width=wl["width"], height=wl["height"],
+                       max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=1,
+                       precision="f32", rng="philox", device=local, profile_kernels=True,
+                       metrics_interval=C * wl["steps_per_chain"])
+    eng = Engine(wl["scene_text"], cfg)
+    eng.set_stream(stream.cuda_stream)
+    # prologue: b over substreams (sharded, gathered in substream order), chain init
+    if world > 1:
+        all_gather_b(eng, cfg, plan)
+        eng.set_exchange_interval(1)
+    else:
+        eng.estimate_b()
+    eng.init_chains()
+
+    def step():
+        eng.run(C)
+        if world > 1:
+            exchange_adaptation(eng)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    s0 = eng.stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+    s1 = eng.stats()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    muts = args.steps * C
+    value = muts / (ms_max / 1e3)
+    launches = s1.kernel_launches - s0.kernel_launches
+    step_ms = (s1.step_kernel_ms - s0.step_kernel_ms)
+    step_launches = s1.step_kernel_launches - s0.step_kernel_launches
+    rays_dev = (s1.rays_closest + s1.rays_visibility) - (s0.rays_closest + s0.rays_visibility)
+    eng.close()
+    return dict(value=value, ms=ms_max, launches=launches, step_ms=step_ms,
+                step_launches=step_launches, rays_dev=rays_dev, muts=muts, clocks=clk.summary(),
+                world=world, rank=rank, local=local, mutations_per_rank=args.steps * plan.count)
+
+
+def run_e2e(args, wl):
+    """End to end through the reference-facing C-ABI with host buffers: scene
+    text from host memory -> ramlt_gpu_create_from_text -> ramlt_gpu_render
+    (estimate_b, chain init, K steps) -> ramlt_gpu_read_image into a host array."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2402_08273_b200 import _capi
+    from paper_2402_08273_b200.render import RenderConfig
+    lib = _capi.load()
+    Cn = wl["chains"]
+    cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=Cn,
+                       mutations=Cn * args.steps, width=wl["width"], height=wl["height"],
+                       max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=2,
+                       precision="f32", rng="philox", device=0,
+                       metrics_interval=Cn * args.steps)
+    text = wl["scene_text"].encode()
+    img = np.zeros((wl["height"], wl["width"], 3), np.float32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h = C.c_void_p()
+    d = cfg.to_c()
+    rc = lib.ramlt_gpu_create_from_text(text, b"<bench>", C.byref(d), C.byref(h))
+    assert rc == 0, lib.ramlt_gpu_last_create_error()
+    rc = lib.ramlt_gpu_render(h)
+    assert rc == 0, lib.ramlt_gpu_last_error(h)
+    rc = lib.ramlt_gpu_read_image(h, img.ctypes.data_as(C.POINTER(C.c_float)))
+    assert rc == 0
+    t1 = time.perf_counter()
+    lib.ramlt_gpu_destroy(h)
+    return Cn * args.steps / (t1 - t0), len(text), img.nbytes, float(img.mean())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=0, help="mutations in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2402_08273_b200 import scenes
+    wl = dict(WORKLOADS[args.workload])
+    wl["scene_text"] = scenes.SCENES[wl["scene"]]()
+    world, rank, local = dist_env()
+    threads = os.cpu_count() or 1
+    config = {"workload": args.workload, "desc": wl["desc"], "chains": wl["chains"],
+              "strategy": wl["strategy"], "perturbation": wl["perturbation"],
+              "image": [wl["width"], wl["height"]], "max_vertices": wl["max_vertices"],
+              "step": "one lockstep mutation of every chain",
+              "l2": "chain state exceeds the 126 MB L2 (c3: ~150 MB of path SoA); no flush",
+              "rng": "philox4x32-10", "adaptation": "pooled" if wl["chains"] > 4096 else "literal"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        sample = args.cpu_sample or (1 << 21)
+        vals, times = [], []
+        for _ in range(args.warmup if args.warmup < 3 else 1):
+            cpu_reference_run(wl, wl["scene_text"], sample // 8, threads)
+        for _ in range(args.steps if args.steps <= 8 else 8):
+            v, kind, cores, t, chains = cpu_reference_run(wl, wl["scene_text"], sample, threads)
+            vals.append(v)
+            times.append(t)
+        v = sum(vals) / len(vals)
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": len(vals),
+                "warmup": 1, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "impl": "reference", "config": dict(config, chains_cpu=chains),
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                 "sample": f"{sample} mutations of the {args.workload} scene/variant "
+                                           f"with chains = {chains} host threads"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    res = run_ours(args, wl, wl["scene_text"])
+    if res["rank"] != 0:
+        return
+    peaks = load_peaks()
+    r_m = oracle_rays_per_mutation(wl, wl["scene_text"])
+    from paper_2402_08273_b200 import parse_scene
+    n_mat, n_sph, n_tri, n_emi = parse_scene(wl["scene_text"]).counts
+    flop_per_mut = r_m * (45.0 * n_tri + 20.0 * n_sph)
+    # dominant kernel: the chain-step megakernel; algorithmic FLOPs per launch
+    # = mutations per launch (all chains of this rank) x W, / its mean event time
+    per_launch_muts = res["mutations_per_rank"] / max(res["step_launches"], 1)
+    mean_launch_s = (res["step_ms"] / max(res["step_launches"], 1)) / 1e3
+    achieved = per_launch_muts * flop_per_mut / mean_launch_s / 1e12
+    sm_max = res["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * float(sm_max) * 1e6 / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": traffic,
+                "peak_source": "nominal FP32 issue: 148 SM x 128 lanes x 2 x sm_max_mhz "
+                               "(MEASURED_PEAKS.json has no FP32 figure)",
+                "work_per_unit": f"R_m x (45 N_tri + 20 N_sph) = {r_m:.3f} x (45x{n_tri} + 20x{n_sph}) "
+                                 f"= {flop_per_mut:.0f} FLOP/mutation (R_m oracle-counted)",
+                "kernel": "k_step (chain-step megakernel)",
+                "kernel_share": res["step_ms"] / res["ms"] if res["ms"] else None}
+    cpu = None
+    if not args.no_cpu_baseline and res["world"] == 1:
+        sample = args.cpu_sample or (1 << 21)
+        v, kind, cores, t, chains = cpu_reference_run(wl, wl["scene_text"], sample, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{sample} mutations, chains = {chains} host threads, loop-only time "
+                         f"{t:.2f} s (core/driver.cpp:246,262)"}
+    e2e_v, h2d, d2h, _ = run_e2e(args, wl) if res["world"] == 1 else (None, 0, 0, 0)
+    steps = args.steps
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": res["world"],
+        "steps": steps, "warmup": args.warmup, "ms_per_step": res["ms"] / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded stand-in scene, BASELINE.json config)", "config": config,
+        "rays_per_s": {"device": res["rays_dev"] / (res["ms"] / 1e3) * res["world"],
+                       "reference_equivalent": res["value"] * r_m, "r_m": r_m},
+        "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d / steps,
+                "d2h_bytes_per_step": d2h / steps,
+                "path": "ramlt_gpu_create_from_text + ramlt_gpu_render (b, init, K steps) + "
+                        "ramlt_gpu_read_image, host buffers, wall clock"},
+        "gpu_launches": res["launches"], "clocks": res["clocks"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

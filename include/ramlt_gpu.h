@@ -138,6 +138,8 @@ typedef struct ramlt_render_desc {
     uint64_t trace_capacity;  /* adaptation trace rows kept on the device */
     uint64_t region_capacity; /* initial region/node capacity (0 = auto; grows at barriers) */
     uint64_t b_substreams;    /* parallel b-estimate substreams (0 = 65536) */
+    int32_t profile_kernels;  /* record CUDA events around every chain-step launch */
+    int32_t pad2_;
 } ramlt_render_desc;
 
 /* RenderResult scalars (driver.hpp:64-78) + device counters. */
@@ -159,6 +161,8 @@ typedef struct ramlt_stats {
     uint64_t n_trace;
     uint64_t n_metrics;
     uint64_t kernel_launches;    /* engine kernels launched so far */
+    double step_kernel_ms;       /* summed event time of chain-step launches (profile_kernels) */
+    uint64_t step_kernel_launches;
 } ramlt_stats;
 
 /* UpdateEvent trace row (driver.hpp:59-62, adaptation.hpp:51-56). */

@@ -40,6 +40,7 @@ class _CConfig(C.Structure):
         ("width", C.c_int32), ("height", C.c_int32), ("max_vertices", C.c_int32),
         ("trace_enabled", C.c_int32), ("metrics_interval", C.c_uint64),
         ("rng", C.c_int32), ("adapt_mode", C.c_int32), ("b_override", C.c_double),
+        ("chain_offset", C.c_int64), ("chains_total", C.c_int64),
     ]
 
 
@@ -72,6 +73,7 @@ class _COutputs(C.Structure):
         ("trace", C.POINTER(_CTrace)), ("cap_trace", C.c_uint64),
         ("dump", C.c_char_p), ("cap_dump", C.c_uint64),
         ("metrics", C.POINTER(C.c_double)), ("cap_metrics", C.c_uint64),
+        ("film", C.POINTER(C.c_double)),
     ]
 
 
@@ -103,6 +105,8 @@ class OracleConfig:
     rng: str = "pcg32"
     adapt_mode: str = "literal"
     b_override: float = 0.0
+    chain_offset: int = 0
+    chains_total: int = 0
 
     def to_c(self) -> _CConfig:
         c = _CConfig()
@@ -201,6 +205,8 @@ class _Lib:
         out.dump = C.cast(dbuf, C.c_char_p) if dump else None
         out.cap_dump = (1 << 22) if dump else 0
         mt = np.zeros((max(cap_metrics, 1), 4), np.float64)
+        film = np.zeros((cfg.height, cfg.width, 3), np.float64)
+        out.film = film.ctypes.data_as(C.POINTER(C.c_double))
         out.metrics = mt.ctypes.data_as(C.POINTER(C.c_double))
         out.cap_metrics = cap_metrics
         lg = None
@@ -224,7 +230,7 @@ class _Lib:
         return RenderOutput(
             stats=stats, image=img, log_a=la, log_flags=lf, tallies=tallies, trace=trace,
             dump=dbuf.value.decode() if dump else "", metrics=mt[: min(st.n_metrics, cap_metrics)],
-            extra={"n_tallies": st.n_tallies, "n_trace": st.n_trace})
+            extra={"n_tallies": st.n_tallies, "n_trace": st.n_trace, "film": film})
 
 
 class RefLib(_Lib):
@@ -294,9 +300,22 @@ class OracleLib(_Lib):
         L.orc_mh_accept.argtypes = [C.c_double] * 6 + [C.POINTER(C.c_int)]
         L.orc_fresnel.restype = C.c_double
         L.orc_fresnel.argtypes = [C.c_double, C.c_double]
+        L.orc_b_partials.restype = C.c_int
+        L.orc_b_partials.argtypes = [C.c_char_p, C.POINTER(_CConfig), C.c_uint64, C.c_uint64,
+                                     C.POINTER(C.c_double)]
         L.orc_camera.argtypes = [C.POINTER(C.c_double), C.c_int, C.c_int, C.c_double, C.c_double,
                                  C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
+
+
+def oracle_b_partials(lib: "OracleLib", scene: str, cfg: OracleConfig, begin: int, end: int):
+    out = np.zeros((max(end - begin, 0), 2), np.float64)
+    c = cfg.to_c()
+    rc = lib.lib.orc_b_partials(scene.encode(), C.byref(c), begin, end,
+                                out.ctypes.data_as(C.POINTER(C.c_double)))
+    if rc:
+        raise RenderError(rc, "orc_b_partials failed")
+    return out
 
 
 def dp(arr: np.ndarray):

@@ -50,6 +50,8 @@ typedef struct oracle_config {
     int32_t rng;           /* 0 pcg32 (reference), 1 philox4x32-10 */
     int32_t adapt_mode;    /* 0 literal (canonical lockstep order), 1 pooled */
     double b_override;     /* > 0: skip estimate_b and use this b */
+    int64_t chain_offset;  /* sharding: this run simulates global chains */
+    int64_t chains_total;  /* [chain_offset, chain_offset + chains) of chains_total (0 = chains) */
 } oracle_config;
 
 typedef struct oracle_stats {
@@ -99,6 +101,7 @@ typedef struct oracle_outputs {
     uint64_t cap_dump;
     double *metrics;            /* cap_metrics * 4: time_s, mutations, rrmse, mean_acc */
     uint64_t cap_metrics;
+    double *film;               /* optional raw fp64 film W*H*3 (restatement only) */
 } oracle_outputs;
 
 #ifdef __cplusplus

@@ -1464,16 +1464,20 @@ struct Render {
             }
         }
 
-        // chain init (core/driver.cpp:219-242)
+        // chain init (core/driver.cpp:219-242); chain i has global id off + i
+        const uint64_t off = static_cast<uint64_t>(c.chain_offset);
+        const uint64_t ctot = c.chains_total > 0 ? static_cast<uint64_t>(c.chains_total)
+                                                 : static_cast<uint64_t>(c.chains);
         ch.resize(c.chains);
         logs.resize(c.chains);
         for (int i = 0; i < c.chains; ++i) {
             Chain &cc = ch[i];
+            const uint64_t gid = off + static_cast<uint64_t>(i);
             cc.rng.kind = c.rng;
-            cc.rng.reseed(c.seed, static_cast<uint64_t>(i));
+            cc.rng.reseed(c.seed, gid);
             Rng init;
             init.kind = c.rng;
-            init.reseed(c.seed, STREAM_INIT + static_cast<uint64_t>(i) * 2);
+            init.reseed(c.seed, STREAM_INIT + gid * 2);
             bool ok = false;
             Path P;
             std::vector<Rec> R;
@@ -1517,15 +1521,15 @@ struct Render {
         while (done < budget) {
             uint64_t boundary = std::min({budget, next_refine, next_metrics});
             uint64_t span = boundary - done;
-            uint64_t per = span / c.chains, rem = span % c.chains;
+            uint64_t per = span / ctot, rem = span % ctot;
             uint64_t steps = per + (rem ? 1 : 0);
-            uint64_t index = done;
             for (uint64_t j = 0; j < steps; ++j) {
                 visits.clear();
                 for (int i = 0; i < c.chains; ++i) {
-                    if (j >= per + (static_cast<uint64_t>(i) < rem ? 1 : 0))
+                    const uint64_t gid = off + static_cast<uint64_t>(i);
+                    if (j >= per + (gid < rem ? 1 : 0))
                         continue;
-                    step(i, index++, visits);
+                    step(i, done + j * ctot + gid, visits);
                 }
                 adapt(visits);
             }
@@ -1634,6 +1638,8 @@ int oracle_render(const char *scene_text, const oracle_config *c, oracle_stats *
             if (out->image)
                 for (size_t i = 0; i < o.film.size(); ++i)
                     out->image[i] = static_cast<float>(o.film[i] * scale);
+            if (out->film)
+                std::memcpy(out->film, o.film.data(), o.film.size() * sizeof(double));
             for (size_t i = 0; i < o.tallies.size() && i < out->cap_tallies; ++i) {
                 if (out->tally_accept)
                     out->tally_accept[i] = o.tallies[i].first;
@@ -1673,6 +1679,33 @@ int oracle_render(const char *scene_text, const oracle_config *c, oracle_stats *
         return 1;
     } catch (const std::exception &e) {
         copy_err(err, errlen, e.what());
+        return 4;
+    }
+}
+
+// Per-substream b partial sums (sum, sum of squares) for substreams
+// [begin, end): the sharded form of estimate_b used by multi-GPU runs.
+int orc_b_partials(const char *scene_text, const oracle_config *c, uint64_t begin, uint64_t end,
+                   double *out) {
+    try {
+        orc::Scene s = orc::parse(scene_text);
+        s.cam.configure(c->width, c->height);
+        uint64_t S = std::min<uint64_t>(c->b_samples, orc::B_SUBSTREAMS);
+        for (uint64_t sub = begin; sub < end && sub < S; ++sub) {
+            orc::Rng rng;
+            rng.kind = c->rng;
+            rng.reseed(c->seed, orc::STREAM_B + 2 * sub);
+            double sum = 0.0, sq = 0.0;
+            for (uint64_t j = sub; j < c->b_samples; j += S) {
+                double v = orc::b_sample(s, rng, c->max_vertices);
+                sum += v;
+                sq += v * v;
+            }
+            out[2 * (sub - begin)] = sum;
+            out[2 * (sub - begin) + 1] = sq;
+        }
+        return 0;
+    } catch (...) {
         return 4;
     }
 }

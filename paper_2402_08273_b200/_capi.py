@@ -53,6 +53,7 @@ class ramlt_render_desc(C.Structure):
         ("chains_total", C.c_int64), ("chain_offset", C.c_int64), ("log_steps", C.c_uint32),
         ("steps_per_launch", C.c_uint32), ("trace_capacity", C.c_uint64),
         ("region_capacity", C.c_uint64), ("b_substreams", C.c_uint64),
+        ("profile_kernels", C.c_int32), ("pad2_", C.c_int32),
     ]
 
 
@@ -65,7 +66,8 @@ class ramlt_stats(C.Structure):
         ("region_count", C.c_uint64), ("loop_time_s", C.c_double),
         ("rays_closest", C.c_uint64), ("rays_visibility", C.c_uint64),
         ("n_tallies", C.c_uint64), ("n_trace", C.c_uint64), ("n_metrics", C.c_uint64),
-        ("kernel_launches", C.c_uint64),
+        ("kernel_launches", C.c_uint64), ("step_kernel_ms", C.c_double),
+        ("step_kernel_launches", C.c_uint64),
     ]
 
 

@@ -167,6 +167,11 @@ private:
     uint64_t steps_since_fold_ = 0;
     ramlt_stats final_{};
     bool finalized_ = false;
+    // live kernel timing (profile_kernels): event pairs around chain-step launches
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_;
+    double step_ms_ = 0.0;
+    uint64_t step_launches_ = 0;
+    void drain_events();
 };
 
 // ---------------------------------------------------------------------------------------
@@ -363,7 +368,24 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     RAMLT_CUDA(cudaStreamSynchronize(stream_));
 }
 
+template <class R> void EngineT<R>::drain_events() {
+    for (auto &e : ev_) {
+        RAMLT_CUDA(cudaEventSynchronize(e.second));
+        float ms = 0.f;
+        RAMLT_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+        step_ms_ += ms;
+        ++step_launches_;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    ev_.clear();
+}
+
 template <class R> EngineT<R>::~EngineT() {
+    for (auto &e : ev_) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     if (stream_ && own_stream_) {
         cudaStreamSynchronize(stream_);
         cudaStreamDestroy(stream_);
@@ -640,9 +662,21 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     }
 #undef RAMLT_PICK
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (d_.profile_kernels) {
+        if (ev_.size() >= 4096)
+            drain_events();
+        RAMLT_CUDA(cudaEventCreate(&e0));
+        RAMLT_CUDA(cudaEventCreate(&e1));
+        RAMLT_CUDA(cudaEventRecord(e0, stream_));
+    }
     kern<<<blocks, 128, smem_, stream_>>>(P);
     ++launches_;
     RAMLT_CUDA(cudaGetLastError());
+    if (d_.profile_kernels) {
+        RAMLT_CUDA(cudaEventRecord(e1, stream_));
+        ev_.emplace_back(e0, e1);
+    }
 }
 
 template <class R> void EngineT<R>::adapt_after_step(int j, unsigned long long span_start) {
@@ -870,6 +904,9 @@ template <class R> void EngineT<R>::read_stats(ramlt_stats *out) {
     s.n_trace = std::min<uint64_t>(tc, trace_index_.n);
     s.n_metrics = metrics_.size();
     s.kernel_launches = launches_;
+    drain_events();
+    s.step_kernel_ms = step_ms_;
+    s.step_kernel_launches = step_launches_;
     *out = s;
 }
 

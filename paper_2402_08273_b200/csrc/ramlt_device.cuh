@@ -276,7 +276,6 @@ __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> 
                                           const Group<G> &g) {
     R best = M<R>::inf();
     int bi = 0x7fffffff;
-    int n = s.nsph + s.ntri;
     for (int i = g.lane; i < s.nsph; i += G) {
         R t;
         if (hit_sphere(s.sph[i], o, d, t) && t < best) {
@@ -284,7 +283,6 @@ __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> 
             bi = i;
         }
     }
-    for (int i = g.lane + ((s.nsph + G - 1) / G) * G - s.nsph; false;) { (void)i; }
     for (int j = g.lane; j < s.ntri; j += G) {
         R t;
         if (hit_tri(s.tri[j], o, d, t) && t < best) {
@@ -292,7 +290,6 @@ __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> 
             bi = s.nsph + j;
         }
     }
-    (void)n;
     if (G > 1) {
 #pragma unroll
         for (int off = G / 2; off > 0; off >>= 1) {
@@ -711,8 +708,8 @@ template <class R> __device__ __forceinline__ void unpack_meta(uint32_t m, Vx<R>
 
 __device__ __forceinline__ Vx<float> load_gv(const GV<float> *p) {
     GV<float> g;
-    g.a = __ldcg(&p->a);
-    g.b = __ldcg(&p->b);
+    g.a = p->a;
+    g.b = p->b;
     Vx<float> v;
     v.p = mk(g.a.x, g.a.y, g.a.z);
     v.n = mk(g.a.w, g.b.x, g.b.y);
@@ -722,12 +719,12 @@ __device__ __forceinline__ Vx<float> load_gv(const GV<float> *p) {
 __device__ __forceinline__ void store_gv(GV<float> *p, const Vx<float> &v) {
     float4 a = make_float4(v.p.x, v.p.y, v.p.z, v.n.x);
     float4 b = make_float4(v.n.y, v.n.z, __uint_as_float(pack_meta(v.mat, v.emi, v.spec, v.ev)), 0.f);
-    __stcg(&p->a, a);
-    __stcg(&p->b, b);
+    p->a = a;
+    p->b = b;
 }
 __device__ __forceinline__ Vx<double> load_gv(const GV<double> *p) {
-    double2 a = __ldcg(&p->a), b = __ldcg(&p->b), c = __ldcg(&p->c);
-    long long m = __ldcg(&p->meta);
+    double2 a = p->a, b = p->b, c = p->c;
+    long long m = p->meta;
     Vx<double> v;
     v.p = mk(a.x, a.y, b.x);
     v.n = mk(b.y, c.x, c.y);
@@ -735,10 +732,10 @@ __device__ __forceinline__ Vx<double> load_gv(const GV<double> *p) {
     return v;
 }
 __device__ __forceinline__ void store_gv(GV<double> *p, const Vx<double> &v) {
-    __stcg(&p->a, make_double2(v.p.x, v.p.y));
-    __stcg(&p->b, make_double2(v.p.z, v.n.x));
-    __stcg(&p->c, make_double2(v.n.y, v.n.z));
-    __stcg(&p->meta, static_cast<long long>(pack_meta(v.mat, v.emi, v.spec, v.ev)));
+    p->a = make_double2(v.p.x, v.p.y);
+    p->b = make_double2(v.p.z, v.n.x);
+    p->c = make_double2(v.n.y, v.n.z);
+    p->meta = static_cast<long long>(pack_meta(v.mat, v.emi, v.spec, v.ev));
 }
 
 }  // namespace rd

@@ -761,15 +761,16 @@ __global__ void __launch_bounds__(128) k_step(StepParams<R> P) {
         RngIO<RK>::store(rng, P.ch.rng0, P.ch.rng1, c);
         // warp-aggregated ray counters
     }
-    unsigned long long rcc = g.lane == 0 ? rc.c : 0ull, rcv = g.lane == 0 ? rc.v : 0ull;
+    // ray counters: one atomic per converged lane set (any subset mask is safe
+    // for __reduce_add_sync; per-launch per-thread counts fit 32 bits)
+    unsigned rcc = g.lane == 0 ? static_cast<unsigned>(rc.c) : 0u;
+    unsigned rcv = g.lane == 0 ? static_cast<unsigned>(rc.v) : 0u;
     unsigned act = __activemask();
-    for (int off = 16; off > 0; off >>= 1) {
-        rcc += __shfl_down_sync(act, rcc, off);
-        rcv += __shfl_down_sync(act, rcv, off);
-    }
+    unsigned sc = __reduce_add_sync(act, rcc);
+    unsigned sv = __reduce_add_sync(act, rcv);
     if ((threadIdx.x & 31) == __ffs(act) - 1) {
-        atomicAdd(&P.ch.rays[0], rcc);
-        atomicAdd(&P.ch.rays[1], rcv);
+        atomicAdd(&P.ch.rays[0], static_cast<unsigned long long>(sc));
+        atomicAdd(&P.ch.rays[1], static_cast<unsigned long long>(sv));
     }
 }
 
@@ -922,6 +923,7 @@ __global__ void __launch_bounds__(1024) k_adapt_literal(const int *vreg, const d
     __shared__ typename Sort::TempStorage tmp;
     __shared__ int keys_s[1024];
     __shared__ int vals_s[1024];
+    __shared__ double a_s[1024];
     for (int base = 0; base < C; base += 1024) {
         int t = threadIdx.x;
         int cidx = base + t;
@@ -932,6 +934,7 @@ __global__ void __launch_bounds__(1024) k_adapt_literal(const int *vreg, const d
         // BlockRadixSort with 1 item/thread leaves thread t holding rank t
         keys_s[t] = key[0];
         vals_s[t] = val[0];
+        a_s[t] = key[0] != 0x7fffffff ? va[val[0]] : 0.0;
         __syncthreads();
         int r = keys_s[t];
         bool head = r != 0x7fffffff && (t == 0 || keys_s[t - 1] != r);
@@ -945,7 +948,7 @@ __global__ void __launch_bounds__(1024) k_adapt_literal(const int *vreg, const d
             bool changed = false;
             for (int q = t; q < 1024 && keys_s[q] == r; ++q) {
                 int ci = vals_s[q];
-                double a = va[ci];
+                double a = a_s[q];
                 ta += a;
                 tv += 1;
                 ps += a;

@@ -86,6 +86,7 @@ class RenderConfig:
     trace_capacity: int = 0
     region_capacity: int = 0
     b_substreams: int = 0
+    profile_kernels: bool = False
 
     def to_c(self) -> _capi.ramlt_render_desc:
         d = _capi.ramlt_render_desc()
