@@ -920,17 +920,25 @@ __global__ void __launch_bounds__(1024) k_adapt_literal(const int *vreg, const d
                                                         RegionArrays ra, KernTab<R> *ktab, AdaptCfg cfg,
                                                         TraceBuf tb) {
     typedef cub::BlockRadixSort<int, 1024, 1, int> Sort;
-    __shared__ typename Sort::TempStorage tmp;
-    __shared__ int keys_s[1024];
-    __shared__ int vals_s[1024];
-    __shared__ double a_s[1024];
+    __shared__ union {
+        typename Sort::TempStorage tmp;
+        struct {
+            int k[1024];
+            int v[1024];
+            double a[1024];
+        } d;
+    } sm;
+    int *keys_s = sm.d.k;
+    int *vals_s = sm.d.v;
+    double *a_s = sm.d.a;
     for (int base = 0; base < C; base += 1024) {
         int t = threadIdx.x;
         int cidx = base + t;
         int key[1], val[1];
         key[0] = (cidx < C && vreg[cidx] >= 0) ? vreg[cidx] : 0x7fffffff;
         val[0] = cidx;
-        Sort(tmp).Sort(key, val);
+        Sort(sm.tmp).Sort(key, val);
+        __syncthreads();   // temp storage is aliased by the run arrays below
         // BlockRadixSort with 1 item/thread leaves thread t holding rank t
         keys_s[t] = key[0];
         vals_s[t] = val[0];

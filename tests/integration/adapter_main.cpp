@@ -1,0 +1,32 @@
+// Compile/link check of include/ramlt_b200_adapter.hpp inside the reference's
+// include tree: the reference's own types flow through the C-ABI.
+#include "driver.hpp"
+#include "scene.hpp"
+#include "ramlt_b200_adapter.hpp"
+
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+
+int main(int argc, char **argv) {
+    if (argc < 2)
+        return 2;
+    std::ifstream f(argv[1]);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    ramlt::RenderConfig cfg;
+    cfg.strategy = ramlt::StrategyVariant::Fixed;
+    cfg.chains = 16;
+    cfg.mutations = 16 * 64;
+    cfg.width = cfg.height = 32;
+    cfg.max_vertices = 9;
+    cfg.b_samples = 4096;
+    ramlt_b200::Options opt;
+    opt.precision = RAMLT_F64;
+    opt.rng = RAMLT_RNG_PCG32;
+    ramlt::RenderResult gpu = ramlt_b200::run_render<ramlt::RenderResult>(ss.str(), cfg, opt);
+    ramlt::RenderResult cpu = ramlt::run_render(ramlt::parse_scene(ss.str()), cfg);
+    std::printf("gpu acc=%.6f lum=%.3f  cpu acc=%.6f lum=%.3f  b gpu=%.4f cpu=%.4f\n", gpu.mean_acceptance,
+                gpu.film_luminance, cpu.mean_acceptance, cpu.film_luminance, gpu.b.b, cpu.b.b);
+    return gpu.mean_acceptance == cpu.mean_acceptance ? 0 : 1;
+}
