@@ -4,10 +4,12 @@
 
 #include "engine.h"
 #include "ramlt_kernels.cuh"
+#include "ramlt_step_co.cuh"
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -95,6 +97,10 @@ private:
     void launch_step(int j0, int j1, unsigned long long span_start, unsigned long long per,
                      unsigned long long rem, bool record);
     void adapt_after_step(int j, unsigned long long span_start);
+    void launch_step_co(const rd::StepParams<R> &P);
+    bool launch_coop(int j0, int j1, unsigned long long span_start, unsigned long long per,
+                     unsigned long long rem);
+    int coop_state_ = -1;   // -1 unknown, 0 unavailable, 1 usable
     void refine();
     void fold();
     void flush_metrics(uint64_t at);
@@ -137,6 +143,9 @@ private:
     DBuf<double> va_;
     DBuf<int> err_;
     DBuf<unsigned long long> rays_;
+    DBuf<unsigned> work_;     // work-stealing counter of k_step_co
+    bool use_co_ = false;     // G == 1: RAMLT_STEP_KERNEL=co selects the coroutine kernel
+    int steal_ = 1;           // RAMLT_STEP_KERNEL=co_static: one chain per lane, no stealing
     // film
     DBuf<double> film64_;
     DBuf<float4> film32_;
@@ -304,6 +313,11 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     err_.zero(stream_);
     rays_.alloc(2);
     rays_.zero(stream_);
+    work_.alloc(1);
+    if (const char *v = std::getenv("RAMLT_STEP_KERNEL")) {
+        use_co_ = std::string(v) == "co" || std::string(v) == "co_static";
+        steal_ = std::string(v) == "co_static" ? 0 : 1;
+    }
     size_t npix = static_cast<size_t>(d.width) * d.height;
     film64_.alloc(npix * 3);
     film64_.zero(stream_);
@@ -643,6 +657,11 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     P.j0 = j0;
     P.j1 = j1;
     P.record_visits = record ? 1 : 0;
+    if (G_ == 1 && use_co_) {
+        P.steal = steal_;
+        launch_step_co(P);
+        return;
+    }
     const long long threads = static_cast<long long>(C_) * G_;
     const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
     void (*kern)(rd::StepParams<R>) = nullptr;
@@ -677,6 +696,112 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
         RAMLT_CUDA(cudaEventRecord(e1, stream_));
         ev_.emplace_back(e0, e1);
     }
+}
+
+template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P) {
+    auto kern = d_.rng == RAMLT_RNG_PHILOX ? rd::k_step_co<R, rd::RNG_PHILOX> : rd::k_step_co<R, rd::RNG_PCG>;
+    size_t scene = (smem_ + 15) & ~size_t(15);
+    size_t smem = scene + static_cast<size_t>(128) * d_.max_vertices * sizeof(rd::GV<R>);
+    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    int dev = 0, sms = 148;
+    RAMLT_CUDA(cudaGetDevice(&dev));
+    RAMLT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    unsigned want = static_cast<unsigned>((C_ + 127) / 128);
+    unsigned blocks = P.steal ? std::min<unsigned>(want, static_cast<unsigned>(std::max(per_sm, 1) * sms)) : want;
+    RAMLT_CUDA(cudaMemsetAsync(work_.p, 0, sizeof(unsigned), stream_));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (d_.profile_kernels) {
+        if (ev_.size() >= 4096)
+            drain_events();
+        RAMLT_CUDA(cudaEventCreate(&e0));
+        RAMLT_CUDA(cudaEventCreate(&e1));
+        RAMLT_CUDA(cudaEventRecord(e0, stream_));
+    }
+    kern<<<blocks, 128, smem, stream_>>>(P, work_.p);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    if (d_.profile_kernels) {
+        RAMLT_CUDA(cudaEventRecord(e1, stream_));
+        ev_.emplace_back(e0, e1);
+    }
+}
+
+// All steps of a span in one cooperative launch when every chain group fits
+// on the GPU at once (small chain counts, where per-step launches dominate).
+template <class R>
+bool EngineT<R>::launch_coop(int j0, int j1, unsigned long long span_start, unsigned long long per,
+                             unsigned long long rem) {
+    if (coop_state_ == 0 || j1 <= j0)
+        return coop_state_ != 0 && j1 <= j0;
+    if (const char *v = std::getenv("RAMLT_COOP"))
+        if (std::string(v) == "0")
+            coop_state_ = 0;
+    void (*kern)(rd::StepParams<R>, rd::CoopArgs<R>) = nullptr;
+#define RAMLT_PICK(RK)                                                                              \
+    switch (G_) {                                                                                   \
+    case 1: kern = rd::k_step_coop<R, RK, 1>; break;                                                \
+    case 2: kern = rd::k_step_coop<R, RK, 2>; break;                                                \
+    case 4: kern = rd::k_step_coop<R, RK, 4>; break;                                                \
+    case 8: kern = rd::k_step_coop<R, RK, 8>; break;                                                \
+    case 16: kern = rd::k_step_coop<R, RK, 16>; break;                                              \
+    default: kern = rd::k_step_coop<R, RK, 32>; break;                                              \
+    }
+    if (d_.rng == RAMLT_RNG_PHILOX) {
+        RAMLT_PICK(rd::RNG_PHILOX)
+    } else {
+        RAMLT_PICK(rd::RNG_PCG)
+    }
+#undef RAMLT_PICK
+    const long long threads = static_cast<long long>(C_) * G_;
+    const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
+    if (coop_state_ < 0) {
+        int dev = 0, sms = 0, coop = 0, per_sm = 0;
+        RAMLT_CUDA(cudaGetDevice(&dev));
+        RAMLT_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        RAMLT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+        RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem_));
+        coop_state_ = (coop && static_cast<long long>(per_sm) * sms >= blocks) ? 1 : 0;
+        if (!coop_state_)
+            return false;
+    }
+    rd::StepParams<R> P = params();
+    P.span_start = span_start;
+    P.per = per;
+    P.rem = rem;
+    P.j0 = j0;
+    P.j1 = j1;
+    P.record_visits = 1;
+    P.ktab_l2 = 1;
+    rd::CoopArgs<R> A;
+    A.ktab = ktab_.p;
+    A.cfg = adaptcfg();
+    A.tb = tracebuf();
+    A.pooled = adapt_ == 1 ? 1 : 0;
+    A.key_bits = 1;
+    while ((1ll << A.key_bits) - 1 < static_cast<long long>(n_regions_host_) + 0)
+        ++A.key_bits;
+    if ((1ll << A.key_bits) - 1 <= n_regions_host_ - 1)
+        ++A.key_bits;
+    void *args[] = {&P, &A};
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (d_.profile_kernels) {
+        if (ev_.size() >= 4096)
+            drain_events();
+        RAMLT_CUDA(cudaEventCreate(&e0));
+        RAMLT_CUDA(cudaEventCreate(&e1));
+        RAMLT_CUDA(cudaEventRecord(e0, stream_));
+    }
+    RAMLT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(blocks), dim3(128), args, smem_,
+                                           stream_));
+    ++launches_;
+    if (d_.profile_kernels) {
+        RAMLT_CUDA(cudaEventRecord(e1, stream_));
+        ev_.emplace_back(e0, e1);
+    }
+    return true;
 }
 
 template <class R> void EngineT<R>::adapt_after_step(int j, unsigned long long span_start) {
@@ -785,6 +910,8 @@ template <class R> void EngineT<R>::run(uint64_t mutations) {
                 if (sizeof(R) == 4 && steps_since_fold_ >= 4096)
                     fold();
             }
+        } else if (!exchange_interval_ && launch_coop(0, steps, done_, per, rem)) {
+            steps_since_fold_ += static_cast<uint64_t>(steps);
         } else {
             for (int j = 0; j < steps; ++j) {
                 launch_step(j, j + 1, done_, per, rem, true);

@@ -137,16 +137,20 @@ template <> struct Rng<RNG_PHILOX> {
         draw = 0;
         bid = ~0ULL;
     }
+    // The 10-round block computation is out of line: next_u32 is inlined at
+    // every draw site, the refill runs once per four words.
+    __device__ __noinline__ void refill(uint64_t b) {
+        b0 = static_cast<uint32_t>(b);
+        b1 = static_cast<uint32_t>(b >> 32);
+        b2 = static_cast<uint32_t>(stream);
+        b3 = static_cast<uint32_t>(stream >> 32);
+        philox10(b0, b1, b2, b3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
+        bid = b;
+    }
     __device__ __forceinline__ uint32_t next_u32() {
         uint64_t b = draw >> 2;
-        if (b != bid) {
-            b0 = static_cast<uint32_t>(b);
-            b1 = static_cast<uint32_t>(b >> 32);
-            b2 = static_cast<uint32_t>(stream);
-            b3 = static_cast<uint32_t>(stream >> 32);
-            philox10(b0, b1, b2, b3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
-            bid = b;
-        }
+        if (b != bid)
+            refill(b);
         uint32_t w = draw & 3;
         ++draw;
         return w == 0 ? b0 : (w == 1 ? b1 : (w == 2 ? b2 : b3));

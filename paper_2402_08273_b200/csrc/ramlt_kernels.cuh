@@ -17,6 +17,8 @@
 #include "ramlt_device.cuh"
 
 #include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
 
 namespace rd {
 
@@ -103,9 +105,27 @@ template <class R> struct StepParams {
     unsigned long long span_start, per, rem;
     int j0, j1;
     int record_visits;   // write vreg/va (adaptive)
+    int steal;           // k_step_co: 1 = warp-aggregated work stealing, 0 = one chain per lane
+    int ktab_l2;         // region kernel tables change inside this launch (cooperative): read via L2
     int pooled;          // fuse pooled accumulation into the step
     RegionArrays reg;
 };
+
+// Region kernel tables are rewritten between lockstep steps of one cooperative
+// launch: read them through L2 (never a stale L1 line).
+template <class R> __device__ __forceinline__ KernTab<R> ld_ktab(const KernTab<R> *p, int via_l2) {
+    if (!via_l2)
+        return *p;
+    const R *q = reinterpret_cast<const R *>(p);
+    KernTab<R> t;
+    t.k1.sigma = __ldcg(q + 0);
+    t.k1.lo = __ldcg(q + 1);
+    t.k1.mass = __ldcg(q + 2);
+    t.k2.sigma = __ldcg(q + 3);
+    t.k2.lo = __ldcg(q + 4);
+    t.k2.mass = __ldcg(q + 5);
+    return t;
+}
 
 // ---- path accessors --------------------------------------------------------------------
 template <class R> struct CurPath {
@@ -412,7 +432,7 @@ __device__ bool retrace(const SceneView<R> &S, const CurPath<R> &ref, int kref, 
 
 // perturbation_density (core/mutations.cpp:176-196)
 template <class R, class PF, class PT>
-__device__ R pert_density(const PF &from, const PT &to, unsigned pmask, int endpoint,
+__device__ __noinline__ R pert_density(const PF &from, const PT &to, unsigned pmask, int endpoint,
                           const Kern<R> &k1, const Kern<R> &k2) {
     R q = R(1);
     unsigned m = pmask;
@@ -601,7 +621,7 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
         if (P.ctl == 2 && pk == 1)
             cylindrical(pdir<R>(cur, first), cu, cv);
         region = P.ctl == 2 ? classify(P.part, cs.ru, cs.rv, cu, cv) : 0;
-        const KernTab<R> kt = P.ktab[region];
+        const KernTab<R> kt = ld_ktab(P.ktab + region, P.ktab_l2);
         // lens_perturb / multichain_perturb (core/mutations.cpp:122-174)
         Vx<R> cam0 = cur.get(0);
         pv[0] = cam0;
@@ -629,7 +649,7 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
                     if (pk == 1)
                         cylindrical(pdir<R>(prop, first), pu, pv_);
                     int preg = classify(P.part, pc.u, pc.v, pu, pv_);
-                    const KernTab<R> kr = P.ktab[preg];
+                    const KernTab<R> kr = ld_ktab(P.ktab + preg, P.ktab_l2);
                     tr = pert_density(prop, cur, pmask, endpoint, kr.k1, kr.k2);
                 }
                 a = mh_accept(cs.pi, pc.pi, tf, tr, s_pert, s_pert);
@@ -1174,6 +1194,355 @@ __global__ void k_to_image(const double *film, float *img, int n, double scale) 
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n)
         img[i] = static_cast<float>(film[i] * scale);
+}
+
+}  // namespace rd
+
+// ---- cooperative persistent step kernel (adaptive strategies, small chain counts) ----------
+#include <cooperative_groups.h>
+
+namespace rd {
+
+// Literal adaptation for one lockstep step by one 128-thread block: tiles of
+// 1024 chains in order (core/adaptation.cpp:60-92 applied in canonical order).
+//  * single-region tiles (Global, or a quadtree before its first split): the
+//    visits are compacted in chain order by a block scan; complete batches of L
+//    are summed in parallel (each sequentially, the first continuing from the
+//    pending sum); one thread runs the lambda recurrence over the batches while
+//    another accumulates the lifetime tally sequentially;
+//  * multi-region tiles: stable radix sort by region over just the key bits in
+//    use, then each region's run is processed sequentially by its head thread.
+struct LiteralSmem {
+    typedef cub::BlockRadixSort<int, 128, 8, int> Sort;
+    typedef cub::BlockScan<int, 128> Scan;
+    typedef cub::BlockReduce<int, 128> Reduce;
+    union {
+        typename Sort::TempStorage tmp;
+        typename Scan::TempStorage scan;
+        typename Reduce::TempStorage red;
+        struct {
+            int k[1024];
+            int v[1024];
+            double a[1024];
+        } d;
+    };
+    double bsum[1024 / 1 + 1];
+    double bstep[1024 / 1 + 1];   // gamma(n + b) * sgn(alpha_hat_b - target) per complete batch
+    double bah[1024 / 1 + 1];
+    int rmin, rmax, cnt;
+};
+
+template <class R>
+__device__ void adapt_literal_block(LiteralSmem &sm, const int *vreg, const double *va, int C, long long chain_off,
+                                    long long C_total, unsigned long long span_start, int j, RegionArrays ra,
+                                    KernTab<R> *ktab, const AdaptCfg &cfg, const TraceBuf &tb, int key_bits) {
+    const int t = threadIdx.x;
+    for (int base = 0; base < C; base += 1024) {
+        int key[8], val[8], flag[8];
+        int lo = 0x7fffffff, hi = -1, nv = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            int ci = base + t * 8 + q;
+            int r = (ci < C) ? __ldcg(&vreg[ci]) : -1;
+            key[q] = r;
+            val[q] = ci;
+            flag[q] = r >= 0;
+            if (r >= 0) {
+                lo = min(lo, r);
+                hi = max(hi, r);
+                ++nv;
+            }
+        }
+        int blo = LiteralSmem::Reduce(sm.red).Reduce(lo, cub::Min());
+        __syncthreads();
+        int bhi = LiteralSmem::Reduce(sm.red).Reduce(hi, cub::Max());
+        __syncthreads();
+        if (t == 0) {
+            sm.rmin = blo;
+            sm.rmax = bhi;
+        }
+        __syncthreads();
+        if (sm.rmax < 0) {   // no visits in this tile
+            __syncthreads();
+            continue;
+        }
+        if (sm.rmin == sm.rmax) {
+            // ---- single region: compact in chain order ----
+            const int r = sm.rmin;
+            int pos[8];
+            int total;
+            LiteralSmem::Scan(sm.scan).ExclusiveSum(flag, pos, total);
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (flag[q]) {
+                    sm.d.a[pos[q]] = __ldcg(&va[val[q]]);
+                    sm.d.v[pos[q]] = val[q];
+                }
+            if (t == 0)
+                sm.cnt = total;
+            __syncthreads();
+            const int m = sm.cnt;
+            const int L = cfg.L;
+            const unsigned pn0 = ra.pend_n[r];
+            const double ps0 = ra.pend_sum[r];
+            const int first_len = L - static_cast<int>(pn0);   // visits that complete batch 0
+            const int nb = m >= first_len ? 1 + (m - first_len) / L : 0;   // complete batches
+            // batch b covers [s_b, e_b): s_0 = 0, e_0 = first_len, then L each
+            for (int b = t; b <= nb; b += 128) {
+                int sb = b == 0 ? 0 : first_len + (b - 1) * L;
+                int eb = b == 0 ? min(m, first_len) : min(m, sb + L);
+                double acc = b == 0 ? ps0 : 0.0;
+                for (int q = sb; q < eb; ++q)
+                    acc += sm.d.a[q];
+                sm.bsum[b] = acc;
+                if (b < nb) {
+                    // the lambda-independent half of update_lambda (adaptation.cpp:15-20)
+                    double ah = acc / static_cast<unsigned>(L);
+                    ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
+                    double gs = cfg.gscale / ::sqrt(static_cast<double>(ra.n[r] + static_cast<unsigned long long>(b)));
+                    double gm = cfg.gmax < gs ? cfg.gmax : gs;
+                    double diff = ah - cfg.target;
+                    double sg = diff > 0.0 ? 1.0 : (diff < 0.0 ? -1.0 : 0.0);
+                    sm.bstep[b] = gm * sg;   // exact: sg is -1, 0 or 1
+                    sm.bah[b] = ah;
+                }
+            }
+            __syncthreads();
+            if (t == 0) {
+                double lam = ra.lambda[r];
+                unsigned long long n = ra.n[r];
+                for (int b = 0; b < nb; ++b) {
+                    double ah = sm.bah[b];
+                    unsigned long long n0 = n;
+                    double nl = lam + sm.bstep[b];
+                    lam = cfg.lmin > nl ? cfg.lmin : nl;
+                    n = n0 + 1;
+                    if (cfg.trace) {
+                        int last = first_len + b * L - 1;
+                        trace_push(tb, span_start + static_cast<unsigned long long>(j) * C_total + chain_off +
+                                           sm.d.v[last], r, n0, lam, ah);
+                    }
+                }
+                // leftover partial batch (sequential partial sum of batch nb)
+                int lead = nb == 0 ? m : m - (first_len + (nb - 1) * L);
+                ra.pend_n[r] = nb == 0 ? pn0 + static_cast<unsigned>(m) : static_cast<unsigned>(lead);
+                ra.pend_sum[r] = sm.bsum[nb];
+                if (nb > 0) {
+                    ra.lambda[r] = lam;
+                    ra.n[r] = n;
+                    set_ktab(&ktab[r], lam, cfg.ratio);
+                }
+            } else if (t == 32) {
+                double ta = ra.tot_acc[r];
+                for (int q = 0; q < m; ++q)
+                    ta += sm.d.a[q];
+                ra.tot_acc[r] = ta;
+                ra.tot_vis[r] += static_cast<unsigned long long>(m);
+            }
+            __syncthreads();
+            continue;
+        }
+        // ---- several regions: stable sort over the bits in use ----
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            key[q] = key[q] >= 0 ? key[q] : ((1 << key_bits) - 1);
+        LiteralSmem::Sort(sm.tmp).Sort(key, val, 0, key_bits);
+        __syncthreads();
+        const int none = (1 << key_bits) - 1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            sm.d.k[t * 8 + q] = key[q];
+            sm.d.v[t * 8 + q] = val[q];
+            sm.d.a[t * 8 + q] = key[q] != none ? __ldcg(&va[val[q]]) : 0.0;
+        }
+        __syncthreads();
+        for (int p = t; p < 1024; p += 128) {
+            int r = sm.d.k[p];
+            if (r == none || (p > 0 && sm.d.k[p - 1] == r))
+                continue;
+            double lam = ra.lambda[r];
+            unsigned long long n = ra.n[r];
+            unsigned int pn = ra.pend_n[r];
+            double ps = ra.pend_sum[r];
+            unsigned long long tv = ra.tot_vis[r];
+            double ta = ra.tot_acc[r];
+            bool changed = false;
+            for (int q = p; q < 1024 && sm.d.k[q] == r; ++q) {
+                double a = sm.d.a[q];
+                ta += a;
+                tv += 1;
+                ps += a;
+                pn += 1;
+                if (pn < static_cast<unsigned int>(cfg.L))
+                    continue;
+                double ah = ps / pn;
+                ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
+                unsigned long long n0 = n;
+                lam = lambda_next(lam, ah, n0, cfg);
+                n = n0 + 1;
+                pn = 0;
+                ps = 0.0;
+                changed = true;
+                if (cfg.trace)
+                    trace_push(tb, span_start + static_cast<unsigned long long>(j) * C_total + chain_off + sm.d.v[q], r,
+                               n0, lam, ah);
+            }
+            ra.lambda[r] = lam;
+            ra.n[r] = n;
+            ra.pend_n[r] = pn;
+            ra.pend_sum[r] = ps;
+            ra.tot_vis[r] = tv;
+            ra.tot_acc[r] = ta;
+            if (changed)
+                set_ktab(&ktab[r], lam, cfg.ratio);
+        }
+        __syncthreads();
+        (void)nv;
+    }
+}
+
+template <class R> struct CoopArgs {
+    KernTab<R> *ktab;   // writable view of P.ktab
+    AdaptCfg cfg;
+    TraceBuf tb;
+    int pooled;
+    int key_bits;       // radix-sort bits covering region ids + one sentinel
+};
+
+// All lockstep steps [j0, j1) of a span in one cooperative launch: every group
+// keeps its chain in registers; after each step a grid-wide barrier, the
+// adaptation update (block 0 for the literal rule, the whole grid for the
+// pooled rule), another barrier.  Same semantics as k_step + k_adapt_* per step.
+template <class R, int RK, int G>
+__global__ void __launch_bounds__(128) k_step_coop(StepParams<R> P, CoopArgs<R> A) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) char smem[];
+    __shared__ LiteralSmem lit;
+    cg::grid_group grid = cg::this_grid();
+    SceneView<R> S = stage_scene(P.scene, smem);
+    Group<G> g;
+    const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c = static_cast<int>(tid / G);
+    const bool active = c < P.C;
+    const long long gc = P.chain_off + c;
+    const unsigned long long my_steps = P.per + (static_cast<unsigned long long>(gc) < P.rem ? 1ull : 0ull);
+
+    ChainRegs<R> cs;
+    Rng<RK> rng;
+    RayCount rc;
+    if (active) {
+        cs.k = P.ch.klen[c];
+        cs.sm = P.ch.smask[c];
+        cs.f = mk(P.ch.cf[c], P.ch.cf[P.C + c], P.ch.cf[2 * P.C + c]);
+        cs.pi = P.ch.cf[3 * P.C + c];
+        cs.ru = P.ch.cr[c];
+        cs.rv = P.ch.cr[P.C + c];
+        cs.eyeden = P.ch.eyeden[c];
+        cs.acc = P.ch.acc[c];
+        cs.iacc = P.ch.iacc[c];
+        cs.lum = P.ch.lum[c];
+        cs.npert = P.ch.npert[c];
+        cs.nlarge = P.ch.nlarge[c];
+        cs.ipert = P.ch.ipert[c];
+        cs.nsteps = P.ch.nsteps[c];
+        RngIO<RK>::load(rng, P.ch.rng0, P.ch.rng1, c, P.seed, static_cast<unsigned long long>(gc));
+    }
+    for (int j = P.j0; j < P.j1; ++j) {
+        if (active) {
+            if (static_cast<unsigned long long>(j) < my_steps) {
+                unsigned long long index = P.span_start + static_cast<unsigned long long>(j) * P.C_total + gc;
+                mutate<R, RK, G>(P, S, c, gc, index, cs, rng, g, rc);
+            } else if (g.lane == 0) {
+                P.ch.vreg[c] = -1;
+            }
+        }
+        grid.sync();
+        if (!A.pooled) {
+            if (blockIdx.x == 0)
+                adapt_literal_block<R>(lit, P.ch.vreg, P.ch.va, P.C, P.chain_off, P.C_total, P.span_start, j, P.reg,
+                                       A.ktab, A.cfg, A.tb, A.key_bits);
+            grid.sync();
+        } else {
+            // pooled: accumulate (one thread per chain) ...
+            if (tid < P.C) {
+                int r = __ldcg(&P.ch.vreg[tid]);
+                if (r >= 0) {
+                    unsigned long long fx = to_fx(__ldcg(&P.ch.va[tid]));
+                    unsigned long long idx =
+                        P.span_start + static_cast<unsigned long long>(j) * P.C_total + P.chain_off + tid;
+                    atomicAdd(&P.reg.x_cnt[r], 1ull);
+                    atomicAdd(&P.reg.x_fx[r], fx);
+                    atomicMax(&P.reg.x_last[r], idx);
+                    if (atomicExch(&P.reg.x_touched[r], 1u) == 0u) {
+                        unsigned slot = atomicAdd(P.reg.n_touched, 1u);
+                        P.reg.touched_list[slot] = static_cast<unsigned>(r);
+                    }
+                }
+            }
+            grid.sync();
+            // ... then one update per touched region
+            unsigned nt = __ldcg(P.reg.n_touched);
+            for (unsigned i = static_cast<unsigned>(tid); i < nt; i += gridDim.x * blockDim.x) {
+                RegionArrays ra = P.reg;
+                int r = static_cast<int>(ra.touched_list[i]);
+                unsigned long long cnt = ra.x_cnt[r], fx = ra.x_fx[r], last = ra.x_last[r];
+                ra.x_cnt[r] = 0;
+                ra.x_fx[r] = 0;
+                ra.x_last[r] = 0;
+                ra.x_touched[r] = 0;
+                ra.tot_vis[r] += cnt;
+                ra.tot_fx[r] += fx;
+                unsigned long long pn = ra.pend_n[r] + cnt;
+                unsigned long long pf = ra.pend_fx[r] + fx;
+                if (pn < static_cast<unsigned long long>(A.cfg.L)) {
+                    ra.pend_n[r] = static_cast<unsigned>(pn);
+                    ra.pend_fx[r] = pf;
+                    continue;
+                }
+                double ah = static_cast<double>(pf) / 16777216.0 / static_cast<double>(pn);
+                ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
+                unsigned long long n0 = ra.n[r];
+                double lam = lambda_next(ra.lambda[r], ah, n0, A.cfg);
+                ra.lambda[r] = lam;
+                ra.n[r] = n0 + 1;
+                ra.pend_n[r] = 0;
+                ra.pend_fx[r] = 0;
+                set_ktab(&A.ktab[r], lam, A.cfg.ratio);
+                if (A.cfg.trace)
+                    trace_push(A.tb, last, r, n0, lam, ah);
+            }
+            grid.sync();
+            if (tid == 0)
+                *P.reg.n_touched = 0;
+        }
+    }
+    if (active && g.lane == 0) {
+        P.ch.klen[c] = cs.k;
+        P.ch.smask[c] = cs.sm;
+        P.ch.cf[c] = cs.f.x;
+        P.ch.cf[P.C + c] = cs.f.y;
+        P.ch.cf[2 * P.C + c] = cs.f.z;
+        P.ch.cf[3 * P.C + c] = cs.pi;
+        P.ch.cr[c] = cs.ru;
+        P.ch.cr[P.C + c] = cs.rv;
+        P.ch.eyeden[c] = cs.eyeden;
+        P.ch.acc[c] = cs.acc;
+        P.ch.iacc[c] = cs.iacc;
+        P.ch.lum[c] = cs.lum;
+        P.ch.npert[c] = cs.npert;
+        P.ch.nlarge[c] = cs.nlarge;
+        P.ch.ipert[c] = cs.ipert;
+        P.ch.nsteps[c] = cs.nsteps;
+        RngIO<RK>::store(rng, P.ch.rng0, P.ch.rng1, c);
+    }
+    unsigned act = __activemask();
+    unsigned sc = __reduce_add_sync(act, g.lane == 0 ? static_cast<unsigned>(rc.c) : 0u);
+    unsigned sv = __reduce_add_sync(act, g.lane == 0 ? static_cast<unsigned>(rc.v) : 0u);
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+        atomicAdd(&P.ch.rays[0], static_cast<unsigned long long>(sc));
+        atomicAdd(&P.ch.rays[1], static_cast<unsigned long long>(sv));
+    }
 }
 
 }  // namespace rd

@@ -1,0 +1,691 @@
+// ramlt_step_co.cuh -- the divergence-free chain-step kernel (one chain per lane).
+//
+// The reference's mutation (core/driver.cpp:113-171) is written as a
+// resumable coroutine (protothread style: every variable that lives across a
+// ray cast is a member, and `CO_RAY` returns to the caller with a pending ray
+// and resumes at the same point).  The kernel loop then alternates
+//   (1) converged:  warp-aggregated work stealing -- idle lanes take the next
+//                   chain from a global counter (one atomic per warp),
+//   (2) divergent:  every lane advances its coroutine until its next ray cast
+//                   (or the end of its chain's steps),
+//   (3) converged:  every lane with a pending ray traces it with the uniform
+//                   smem-broadcast primitive loop -- the expensive part, now
+//                   executed by (nearly) full warps whatever phase each chain is
+//                   in (perturbation replay, large-step bounce, visibility).
+// Arithmetic and RNG consumption are identical to `mutate` (ramlt_kernels.cuh),
+// so the fp64/PCG build stays bit-exact with the reference.
+#pragma once
+
+#include "ramlt_kernels.cuh"
+
+namespace rd {
+
+template <class R> struct RayReq {
+    V3<R> o, d;
+    R lim;   // +inf: closest hit; dist - eps: visibility (occluded iff some t < lim)
+};
+
+// Closest hit below `lim` over spheres then triangles (core/scene.cpp:57-92);
+// ties resolved to the lowest primitive index exactly as the reference loop.
+template <class R>
+__device__ __forceinline__ int trace_ray(const SceneView<R> &s, const RayReq<R> &r, R &t_out) {
+    R best = r.lim;
+    int bi = -1;
+    for (int i = 0; i < s.nsph; ++i) {
+        R t;
+        if (hit_sphere(s.sph[i], r.o, r.d, t) && t < best) {
+            best = t;
+            bi = i;
+        }
+    }
+#pragma unroll 2
+    for (int j = 0; j < s.ntri; ++j) {
+        R t;
+        if (hit_tri(s.tri[j], r.o, r.d, t) && t < best) {
+            best = t;
+            bi = s.nsph + j;
+        }
+    }
+    t_out = best;
+    return bi;
+}
+
+template <class R> __device__ __forceinline__ void hit_record(const SceneView<R> &s, const RayReq<R> &r, int prim,
+                                                             R t, Hit<R> &h) {
+    h.t = t;
+    h.p = add(r.o, scl(r.d, t));
+    if (prim < s.nsph) {
+        const SphD<R> &sp = s.sph[prim];
+        h.n = unit(sub(h.p, sp.c));
+        h.mat = sp.mat;
+        h.emi = sp.emi;
+    } else {
+        const TriD<R> &tr = s.tri[prim - s.nsph];
+        h.n = tr.n;
+        h.mat = tr.mat;
+        h.emi = tr.emi;
+    }
+}
+
+// Proposal path storage in shared memory: vertex i of lane t at pv[i*B + t].
+template <class R> struct PvSmem {
+    GV<R> *base;
+    int stride;
+    __device__ __forceinline__ Vx<R> get(int i) const;
+    __device__ __forceinline__ void set(int i, const Vx<R> &v) const;
+};
+template <> __device__ __forceinline__ Vx<float> PvSmem<float>::get(int i) const {
+    GV<float> g = base[i * stride];
+    Vx<float> v;
+    v.p = mk(g.a.x, g.a.y, g.a.z);
+    v.n = mk(g.a.w, g.b.x, g.b.y);
+    unpack_meta(__float_as_uint(g.b.z), v);
+    return v;
+}
+template <> __device__ __forceinline__ void PvSmem<float>::set(int i, const Vx<float> &v) const {
+    GV<float> g;
+    g.a = make_float4(v.p.x, v.p.y, v.p.z, v.n.x);
+    g.b = make_float4(v.n.y, v.n.z, __uint_as_float(pack_meta(v.mat, v.emi, v.spec, v.ev)), 0.f);
+    base[i * stride] = g;
+}
+template <> __device__ __forceinline__ Vx<double> PvSmem<double>::get(int i) const {
+    const GV<double> &g = base[i * stride];
+    Vx<double> v;
+    v.p = mk(g.a.x, g.a.y, g.b.x);
+    v.n = mk(g.b.y, g.c.x, g.c.y);
+    unpack_meta(static_cast<uint32_t>(g.meta), v);
+    return v;
+}
+template <> __device__ __forceinline__ void PvSmem<double>::set(int i, const Vx<double> &v) const {
+    GV<double> &g = base[i * stride];
+    g.a = make_double2(v.p.x, v.p.y);
+    g.b = make_double2(v.p.z, v.n.x);
+    g.c = make_double2(v.n.y, v.n.z);
+    g.meta = static_cast<long long>(pack_meta(v.mat, v.emi, v.spec, v.ev));
+}
+
+// Proposal = smem head [0..head_end] + current-path tail.
+template <class R> struct PropS {
+    PvSmem<R> pv;
+    int head_end;
+    const CurPath<R> *cur;
+    __device__ __forceinline__ Vx<R> get(int i) const { return i <= head_end ? pv.get(i) : cur->get(i); }
+};
+
+enum { CO_RAY_PENDING = 1, CO_STEP_DONE = 2 };
+
+#define CO_RAY(O, D, LIM, N)                                                                       \
+    do {                                                                                           \
+        ray.o = (O);                                                                               \
+        ray.d = (D);                                                                               \
+        ray.lim = (LIM);                                                                           \
+        pc = (N);                                                                                  \
+        return CO_RAY_PENDING;                                                                     \
+    case (N):;                                                                                     \
+    } while (0)
+
+template <class R, int RK> struct StepCo {
+    // ---- chain (persists over the chain's steps) ----
+    int c;
+    long long gc;
+    ChainRegs<R> cs;
+    Rng<RK> rng;
+    // ---- coroutine ----
+    int pc;
+    RayReq<R> ray;
+    int res_prim;   // -1 miss / visible
+    R res_t;
+    // ---- per-step state ----
+    bool choose, ok, accepted;
+    R s_pert, tf, tr, a, dpdf;
+    int endpoint, first, idx, next, i, region, kp, head_end;
+    unsigned pmask, m, smp;
+    V3<R> o, d;
+    Contrib<R> pcb;
+    // evaluate / eye density sub-state
+    V3<R> ef;
+    R ep, eseg;
+    int ek, ei;
+
+    __device__ __forceinline__ int advance(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
+                                           RayCount &rc, unsigned long long index);
+};
+
+template <class R, int RK>
+__device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, const SceneView<R> &S,
+                                                      const PvSmem<R> &pv, RayCount &rc,
+                                                      unsigned long long index) {
+    CurPath<R> cur{P.ch.verts, P.C, c, &S.cam};
+    switch (pc) {
+    case 0: {
+        {
+            // suitability (core/mutations.cpp:47-56) and strategy selection (driver.cpp:115-116)
+            bool elig;
+            if (P.pk == 0) {
+                endpoint = lens_endpoint(cs.k, cs.sm);
+                elig = endpoint >= 0;
+                pmask = 1u;
+                first = 0;
+            } else {
+                elig = mc_structure(cs.k, cs.sm, first, endpoint, pmask);
+            }
+            s_pert = elig ? R(0.5) : R(0);
+            choose = elig && Unit<R>::draw(rng) < s_pert;
+        }
+        a = R(0);
+        pcb.pi = R(0);
+        region = -1;
+        ok = false;
+        kp = cs.k;
+        smp = cs.sm;
+        head_end = 0;
+        if (!choose)
+            goto large_step;
+        {
+            // classify_path (driver.cpp:95-107)
+            R cu = R(0), cv = R(0);
+            if (P.ctl == 2 && P.pk == 1)
+                cylindrical(pdir<R>(cur, first), cu, cv);
+            region = P.ctl == 2 ? classify(P.part, cs.ru, cs.rv, cu, cv) : 0;
+            pv.set(0, cur.get(0));
+        }
+        // lens_perturb / multichain_perturb (mutations.cpp:122-174)
+        m = pmask;
+        ok = true;
+        while (m) {
+            idx = __ffs(m) - 1;
+            m &= m - 1;
+            next = m ? (__ffs(m) - 1) : endpoint;
+            {
+                const KernTab<R> kt = P.ktab[region];
+                d = perturb_dir(pdir<R>(cur, idx), idx == 0 ? kt.k1 : kt.k2, rng);
+                o = pv.get(idx).p;
+            }
+            // retrace_chain (mutations.cpp:78-110)
+            for (i = idx + 1; i <= next; ++i) {
+                ++rc.c;
+                CO_RAY(o, d, M<R>::inf(), 1);
+                {
+                    if (res_prim < 0) {
+                        ok = false;
+                        break;
+                    }
+                    Hit<R> h;
+                    hit_record(S, ray, res_prim, res_t, h);
+                    Vx<R> r = cur.get(i);
+                    const MatD<R> mt = S.mat[h.mat];
+                    bool he = h.emi >= 0;
+                    bool hs = !he && (mt.kind == MAT_MIRROR || mt.kind == MAT_DIELECTRIC);
+                    if (he != (r.emi >= 0) || hs != r.spec) {
+                        ok = false;
+                        break;
+                    }
+                    Vx<R> x;
+                    x.p = h.p;
+                    x.n = h.n;
+                    x.mat = h.mat;
+                    x.emi = h.emi;
+                    x.spec = hs;
+                    x.ev = r.ev;
+                    pv.set(i, x);
+                    if (i == next)
+                        break;
+                    V3<R> cn;
+                    if (!spec_cont(mt, neg(d), h.n, r.ev, cn)) {
+                        ok = false;
+                        break;
+                    }
+                    o = h.p;
+                    d = cn;
+                }
+            }
+            if (!ok)
+                break;
+        }
+        if (!ok)
+            goto pert_record;
+        head_end = endpoint;
+        {
+            const KernTab<R> kt = P.ktab[region];
+            PropS<R> prop{pv, head_end, &cur};
+            tf = pert_density(cur, prop, pmask, endpoint, kt.k1, kt.k2);
+            tr = pert_density(prop, cur, pmask, endpoint, kt.k1, kt.k2);
+        }
+        ek = cs.k;
+        goto eval_start;
+
+    large_step:
+        ++cs.nlarge;
+        // trace_eye_subpath (path.cpp:84-142) -- large_step (mutations.cpp:58-71)
+        {
+            Vx<R> cv;
+            cv.p = S.cam.pos;
+            cv.n = S.cam.fwd;
+            cv.mat = -1;
+            cv.emi = -1;
+            cv.spec = false;
+            cv.ev = EV_NONE;
+            pv.set(0, cv);
+            kp = 1;
+            smp = 0;
+            tf = R(1);
+            ok = false;
+            if (P.maxv < 2)
+                goto finish;
+            R u = Unit<R>::draw(rng);
+            R v = Unit<R>::draw(rng);
+            d = cam_primary(S.cam, u, v);
+            dpdf = cam_dir_pdf(S.cam, d);
+            o = S.cam.pos;
+        }
+        while (kp < P.maxv) {
+            ++rc.c;
+            CO_RAY(o, d, M<R>::inf(), 2);
+            {
+                if (res_prim < 0)
+                    break;
+                Hit<R> h;
+                hit_record(S, ray, res_prim, res_t, h);
+                const MatD<R> mt = S.mat[h.mat];
+                Vx<R> x;
+                x.p = h.p;
+                x.n = h.n;
+                x.mat = h.mat;
+                x.emi = h.emi;
+                x.spec = h.emi < 0 && (mt.kind == MAT_MIRROR || mt.kind == MAT_DIELECTRIC);
+                x.ev = EV_NONE;
+                tf *= dpdf * (M<R>::abs(dot(h.n, d)) / (h.t * h.t));
+                if (x.spec)
+                    smp |= 1u << kp;
+                if (h.emi >= 0) {
+                    pv.set(kp, x);
+                    ++kp;
+                    ok = true;
+                    break;
+                }
+                if (kp + 1 >= P.maxv) {
+                    pv.set(kp, x);
+                    ++kp;
+                    break;
+                }
+                BS<R> bs;
+                if (!bsdf_sample(mt, neg(d), h.n, rng, bs) || bs.zero_thr) {
+                    pv.set(kp, x);
+                    ++kp;
+                    break;
+                }
+                x.ev = bs.ev;
+                pv.set(kp, x);
+                ++kp;
+                o = h.p;
+                d = bs.dir;
+                dpdf = bs.pdf;
+            }
+        }
+        if (!ok)
+            goto finish;
+        head_end = kp - 1;
+        ek = kp;
+
+    eval_start:
+        // eval_contribution (path.cpp:40-82) over the proposal
+        {
+            PropS<R> prop{pv, head_end, &cur};
+            pcb.pi = R(0);
+            Vx<R> last = prop.get(ek - 1);
+            if (ek < 2 || last.emi < 0)
+                goto eval_done;
+            V3<R> w0 = pdir<R>(prop, 0);
+            R ru, rv;
+            if (!cam_raster(S.cam, w0, ru, rv))
+                goto eval_done;
+            pcb.u = ru;
+            pcb.v = rv;
+            R imp = cam_importance(S.cam, w0);
+            ef = mk(imp, imp, imp);
+        }
+        for (ei = 0; ei + 1 < ek; ++ei) {
+            {
+                PropS<R> prop{pv, head_end, &cur};
+                Vx<R> av = prop.get(ei);
+                Vx<R> bv = prop.get(ei + 1);
+                if (ei > 0 && av.emi >= 0)
+                    goto eval_fail;
+                // geometry_term / area_conversion (path.cpp:7-29) up to the visibility test
+                V3<R> dd = sub(bv.p, av.p);
+                R d2 = dot(dd, dd);
+                if (d2 <= R(0))
+                    goto eval_fail;
+                V3<R> dir = dvs(dd, M<R>::sqrt(d2));
+                eseg = av.spec ? M<R>::abs(dot(bv.n, dir)) / d2
+                               : M<R>::abs(dot(av.n, dir)) * M<R>::abs(dot(bv.n, dir)) / d2;
+                if (eseg <= R(0))
+                    goto eval_fail;
+                ++rc.v;
+                // visible(a, b) (scene.cpp:94-102)
+                R dist = len(dd);
+                if (dist <= R(2) * R(kEpsD))
+                    goto eval_fail;
+                o = av.p;
+                d = dvs(dd, dist);
+                ep = dist - R(kEpsD);
+            }
+            CO_RAY(o, d, ep, 3);
+            {
+                if (res_prim >= 0)
+                    goto eval_fail;
+                ef = scl(ef, eseg);
+                if (ei > 0) {
+                    PropS<R> prop{pv, head_end, &cur};
+                    Vx<R> pr = prop.get(ei - 1);
+                    Vx<R> av = prop.get(ei);
+                    Vx<R> bv = prop.get(ei + 1);
+                    const MatD<R> mt = S.mat[av.mat];
+                    V3<R> wi = unit(sub(pr.p, av.p));
+                    V3<R> wo = unit(sub(bv.p, av.p));
+                    V3<R> bf = av.spec ? spec_weight(mt, wi, av.n, av.ev) : bsdf_f(mt, wi, wo, av.n);
+                    if (zero3(bf))
+                        goto eval_fail;
+                    ef = mul(ef, bf);
+                }
+            }
+        }
+        {
+            PropS<R> prop{pv, head_end, &cur};
+            Vx<R> last = prop.get(ek - 1);
+            Vx<R> pr = prop.get(ek - 2);
+            V3<R> toward = unit(sub(pr.p, last.p));
+            if (dot(last.n, toward) <= R(0))
+                goto eval_fail;
+            V3<R> le = S.emit[last.emi];
+            if (zero3(le))
+                goto eval_fail;
+            V3<R> f = mul(ef, le);
+            R pi = lum(f);
+            if (!(pi > R(0)) || !M<R>::finite(pi))
+                goto eval_fail;
+            pcb.f = f;
+            pcb.pi = pi;
+        }
+        goto eval_done;
+    eval_fail:
+        pcb.pi = R(0);
+    eval_done:
+        if (choose) {
+            if (pcb.pi > R(0)) {
+                if (P.ctl == 2) {
+                    PropS<R> prop{pv, head_end, &cur};
+                    R pu = R(0), pvv = R(0);
+                    if (P.pk == 1)
+                        cylindrical(pdir<R>(prop, first), pu, pvv);
+                    int preg = classify(P.part, pcb.u, pcb.v, pu, pvv);
+                    const KernTab<R> kr = P.ktab[preg];
+                    tr = pert_density(prop, cur, pmask, endpoint, kr.k1, kr.k2);
+                }
+                a = mh_accept(cs.pi, pcb.pi, tf, tr, s_pert, s_pert);
+            }
+            goto pert_record;
+        }
+        if (!(pcb.pi > R(0)))
+            goto finish;
+        if (cs.eyeden == cs.eyeden)   // cached eye_path_density(current)
+            goto large_accept;
+        // eye_path_density (path.cpp:144-170) of the current path
+        ep = R(0);
+        {
+            if (cs.k < 2 || cur.get(cs.k - 1).emi < 0)
+                goto ed_done;
+            R p0 = cam_dir_pdf(S.cam, pdir<R>(cur, 0));
+            if (p0 <= R(0))
+                goto ed_done;
+            ep = p0;
+        }
+        for (ei = 0; ei + 1 < cs.k; ++ei) {
+            {
+                Vx<R> av = cur.get(ei);
+                Vx<R> bv = cur.get(ei + 1);
+                if (ei > 0) {
+                    if (av.emi >= 0) {
+                        ep = R(0);
+                        goto ed_done;
+                    }
+                    Vx<R> pr = cur.get(ei - 1);
+                    const MatD<R> mt = S.mat[av.mat];
+                    V3<R> wi = unit(sub(pr.p, av.p));
+                    V3<R> wo = unit(sub(bv.p, av.p));
+                    eseg = av.spec ? spec_prob(mt, wi, av.n, av.ev) : bsdf_pdf(mt, wi, wo, av.n);
+                    if (eseg <= R(0)) {
+                        ep = R(0);
+                        goto ed_done;
+                    }
+                }
+                // area_conversion(a.p, b) (path.cpp:19-29)
+                V3<R> dd = sub(bv.p, av.p);
+                R d2 = dot(dd, dd);
+                R cval = R(0);
+                if (d2 > R(0)) {
+                    V3<R> dir = dvs(dd, M<R>::sqrt(d2));
+                    cval = M<R>::abs(dot(bv.n, dir)) / d2;
+                }
+                if (cval <= R(0)) {
+                    ef.x = R(0);
+                } else {
+                    ef.x = cval;
+                    ++rc.v;
+                    R dist = len(dd);
+                    if (dist <= R(2) * R(kEpsD)) {
+                        ef.x = R(0);
+                    } else {
+                        o = av.p;
+                        d = dvs(dd, dist);
+                        ef.y = dist - R(kEpsD);
+                        goto ed_ray;
+                    }
+                }
+                goto ed_apply;
+            }
+        ed_ray:
+            CO_RAY(o, d, ef.y, 4);
+            if (res_prim >= 0)
+                ef.x = R(0);
+        ed_apply:
+            if (ei == 0)
+                ep *= ef.x;                 // p *= area_conversion(path[0], path[1])
+            else
+                ep *= eseg * ef.x;          // p *= q * area_conversion(...)
+            if (ep <= R(0)) {
+                ep = R(0);
+                goto ed_done;
+            }
+        }
+    ed_done:
+        cs.eyeden = ep;
+    large_accept:
+        tr = cs.eyeden;
+        {
+            R sx = R(1) - s_pert;
+            R sy = R(1) - R(suit_of(P.pk, kp, smp));
+            a = mh_accept(cs.pi, pcb.pi, tf, tr, sx, sy);
+        }
+        goto finish;
+
+    pert_record:
+        if (P.ctl == 2)
+            atomicAdd(&P.part.visits[region], 1ull);
+        cs.acc += static_cast<double>(a);
+        cs.iacc += static_cast<double>(a);
+        ++cs.npert;
+        ++cs.ipert;
+
+    finish:
+        // splat (driver.cpp:59-64)
+        if (a < R(1) && cs.pi > R(0))
+            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - a) / cs.pi), cs.lum);
+        if (pcb.pi > R(0) && a > R(0))
+            film_add(P, pcb.u, pcb.v, scl(pcb.f, a / pcb.pi), cs.lum);
+        // accept / commit (driver.cpp:168-171)
+        accepted = false;
+        if (a > R(0) && Unit<R>::draw(rng) < a) {
+            accepted = true;
+            for (int q = 1; q <= head_end; ++q)
+                store_gv(&P.ch.verts[static_cast<size_t>(q - 1) * P.C + c], pv.get(q));
+            cs.k = kp;
+            cs.sm = choose ? cs.sm : smp;
+            cs.f = pcb.f;
+            cs.pi = pcb.pi;
+            cs.ru = pcb.u;
+            cs.rv = pcb.v;
+            cs.eyeden = M<R>::inf() - M<R>::inf();
+        }
+        if (cs.nsteps < P.ch.log_K) {
+            size_t ofs = static_cast<size_t>(cs.nsteps) * P.C + c;
+            P.ch.log_a[ofs] = static_cast<double>(a);
+            P.ch.log_f[ofs] = static_cast<unsigned char>((accepted ? 1 : 0) | (choose ? 2 : 0) | 4);
+        }
+        if (P.record_visits) {
+            P.ch.vreg[c] = (choose && P.ctl != 0) ? region : -1;
+            P.ch.va[c] = static_cast<double>(a);
+        }
+        ++cs.nsteps;
+        (void)index;
+        pc = 0;
+        return CO_STEP_DONE;
+    }
+    default:
+        break;
+    }
+    pc = 0;
+    return CO_STEP_DONE;
+}
+
+#undef CO_RAY
+
+template <class R, int RK>
+__device__ __forceinline__ void co_load(StepCo<R, RK> &co, const StepParams<R> &P, int c) {
+    co.c = c;
+    co.gc = P.chain_off + c;
+    ChainRegs<R> &cs = co.cs;
+    cs.k = P.ch.klen[c];
+    cs.sm = P.ch.smask[c];
+    cs.f = mk(P.ch.cf[c], P.ch.cf[P.C + c], P.ch.cf[2 * P.C + c]);
+    cs.pi = P.ch.cf[3 * P.C + c];
+    cs.ru = P.ch.cr[c];
+    cs.rv = P.ch.cr[P.C + c];
+    cs.eyeden = P.ch.eyeden[c];
+    cs.acc = P.ch.acc[c];
+    cs.iacc = P.ch.iacc[c];
+    cs.lum = P.ch.lum[c];
+    cs.npert = P.ch.npert[c];
+    cs.nlarge = P.ch.nlarge[c];
+    cs.ipert = P.ch.ipert[c];
+    cs.nsteps = P.ch.nsteps[c];
+    RngIO<RK>::load(co.rng, P.ch.rng0, P.ch.rng1, c, P.seed, static_cast<unsigned long long>(co.gc));
+    co.pc = 0;
+}
+
+template <class R, int RK>
+__device__ __forceinline__ void co_store(const StepCo<R, RK> &co, const StepParams<R> &P) {
+    const int c = co.c;
+    const ChainRegs<R> &cs = co.cs;
+    P.ch.klen[c] = cs.k;
+    P.ch.smask[c] = cs.sm;
+    P.ch.cf[c] = cs.f.x;
+    P.ch.cf[P.C + c] = cs.f.y;
+    P.ch.cf[2 * P.C + c] = cs.f.z;
+    P.ch.cf[3 * P.C + c] = cs.pi;
+    P.ch.cr[c] = cs.ru;
+    P.ch.cr[P.C + c] = cs.rv;
+    P.ch.eyeden[c] = cs.eyeden;
+    P.ch.acc[c] = cs.acc;
+    P.ch.iacc[c] = cs.iacc;
+    P.ch.lum[c] = cs.lum;
+    P.ch.npert[c] = cs.npert;
+    P.ch.nlarge[c] = cs.nlarge;
+    P.ch.ipert[c] = cs.ipert;
+    P.ch.nsteps[c] = cs.nsteps;
+    RngIO<RK>::store(co.rng, P.ch.rng0, P.ch.rng1, c);
+}
+
+// Persistent, work-stealing chain-step kernel.  `work` is a zeroed counter.
+template <class R, int RK>
+__global__ void __launch_bounds__(128) k_step_co(StepParams<R> P, unsigned int *work) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    size_t scene_bytes = stage_bytes_sph<R>(P.scene.nsph) + static_cast<size_t>(P.scene.ntri) * sizeof(TriD<R>);
+    scene_bytes = (scene_bytes + 15) & ~size_t(15);
+    PvSmem<R> pv{reinterpret_cast<GV<R> *>(smem + scene_bytes) + threadIdx.x, static_cast<int>(blockDim.x)};
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+
+    StepCo<R, RK> co;
+    RayCount rc;
+    bool have = false, exhausted = false, want = false;
+    int j = 0, jend = 0;
+    bool first_grab = true;
+    for (;;) {
+        // (1) converged: idle lanes take chains (one atomic per warp), or --
+        // without stealing -- each lane takes its own chain once
+        unsigned need = __ballot_sync(0xffffffffu, !have && !exhausted);
+        if (need) {
+            unsigned base = 0;
+            int leader = __ffs(need) - 1;
+            if (P.steal) {
+                if (static_cast<int>(lane) == leader)
+                    base = atomicAdd(work, static_cast<unsigned>(__popc(need)));
+                base = __shfl_sync(0xffffffffu, base, leader);
+            }
+            if (!have && !exhausted) {
+                unsigned mine = base + __popc(need & lt);
+                if (!P.steal) {
+                    mine = first_grab ? blockIdx.x * blockDim.x + threadIdx.x : 0xffffffffu;
+                    first_grab = false;
+                }
+                if (mine < static_cast<unsigned>(P.C)) {
+                    co_load(co, P, static_cast<int>(mine));
+                    const unsigned long long my_steps =
+                        P.per + (static_cast<unsigned long long>(co.gc) < P.rem ? 1ull : 0ull);
+                    j = P.j0;
+                    jend = static_cast<int>(min(static_cast<unsigned long long>(P.j1), my_steps));
+                    have = true;
+                    if (j >= jend) {   // inactive for this launch
+                        if (P.record_visits)
+                            P.ch.vreg[co.c] = -1;
+                        have = false;
+                    }
+                } else {
+                    exhausted = true;
+                }
+            }
+        }
+        // (2) divergent: advance to the next ray cast
+        while (have && !want) {
+            unsigned long long index = P.span_start + static_cast<unsigned long long>(j) * P.C_total + co.gc;
+            int st = co.advance(P, S, pv, rc, index);
+            if (st == CO_RAY_PENDING) {
+                want = true;
+            } else if (++j >= jend) {
+                co_store(co, P);
+                have = false;
+            }
+        }
+        // (3) converged: trace every pending ray
+        __syncwarp();
+        if (!__any_sync(0xffffffffu, want || !exhausted))
+            break;
+        if (want) {
+            R t;
+            co.res_prim = trace_ray(S, co.ray, t);
+            co.res_t = t;
+            want = false;
+        }
+    }
+    unsigned act = __activemask();
+    unsigned sc = __reduce_add_sync(act, static_cast<unsigned>(rc.c));
+    unsigned sv = __reduce_add_sync(act, static_cast<unsigned>(rc.v));
+    if (lane == static_cast<unsigned>(__ffs(act) - 1)) {
+        atomicAdd(&P.ch.rays[0], static_cast<unsigned long long>(sc));
+        atomicAdd(&P.ch.rays[1], static_cast<unsigned long long>(sv));
+    }
+}
+
+}  // namespace rd

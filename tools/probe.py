@@ -37,12 +37,14 @@ def probe(scene_name, strategy, perturbation, chains, steps, lanes, precision="f
 
 
 if __name__ == "__main__":
-    probe("cornell", "fixed", "lens", 1024, 512, 32)
-    probe("cornell", "fixed", "lens", 1024, 512, 8)
-    probe("cornell", "fixed", "lens", 1024, 512, 1)
-    probe("cornell", "ra-quadtree", "lens", 1024, 512, 32)
-    probe("cornell", "global", "lens", 1024, 512, 32)
-    probe("cornell", "fixed", "lens", 262144, 16, 1)
-    probe("caustic", "fixed", "multi-chain", 262144, 16, 1, maxv=17, res=512)
-    probe("caustic", "ra-quadtree", "multi-chain", 262144, 16, 1, maxv=17, res=512)
-    probe("cornell", "fixed", "lens", 1024, 128, 32, precision="f64", rng="pcg32")
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if which in ("all", "lanes"):
+        for g in (1, 2, 4):
+            probe("caustic", "ra-quadtree", "multi-chain", 262144, 16, g, maxv=17, res=512)
+            probe("cornell", "fixed", "lens", 262144, 16, g)
+    if which in ("all",):
+        probe("cornell", "fixed", "lens", 1024, 512, 32)
+        probe("cornell", "fixed", "lens", 1024, 512, 16)
+        probe("cornell", "ra-quadtree", "lens", 1024, 512, 32)
+        probe("caustic", "fixed", "multi-chain", 262144, 16, 1, maxv=17, res=512)
+        probe("cornell", "fixed", "lens", 1024, 128, 32, precision="f64", rng="pcg32")
