@@ -56,6 +56,8 @@ enum { RAMLT_DIFFUSE = 0, RAMLT_MIRROR = 1, RAMLT_DIELECTRIC = 2, RAMLT_GLOSSY =
 enum { RAMLT_F32 = 0, RAMLT_F64 = 1 };
 enum { RAMLT_RNG_PCG32 = 0, RAMLT_RNG_PHILOX = 1 };
 enum { RAMLT_ADAPT_AUTO = -1, RAMLT_ADAPT_LITERAL = 0, RAMLT_ADAPT_POOLED = 1 };
+/* auto: BVH above 128 triangles; brute: smem-staged linear scan; bvh: SAH BVH2 */
+enum { RAMLT_ACCEL_AUTO = 0, RAMLT_ACCEL_BRUTE = 1, RAMLT_ACCEL_BVH = 2 };
 
 /* Material (scene.hpp:20-31) */
 typedef struct ramlt_material {
@@ -139,7 +141,7 @@ typedef struct ramlt_render_desc {
     uint64_t region_capacity; /* initial region/node capacity (0 = auto; grows at barriers) */
     uint64_t b_substreams;    /* parallel b-estimate substreams (0 = 65536) */
     int32_t profile_kernels;  /* record CUDA events around every chain-step launch */
-    int32_t pad2_;
+    int32_t accel;            /* RAMLT_ACCEL_*: triangle intersection structure */
 } ramlt_render_desc;
 
 /* RenderResult scalars (driver.hpp:64-78) + device counters. */

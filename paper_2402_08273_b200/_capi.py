@@ -53,7 +53,7 @@ class ramlt_render_desc(C.Structure):
         ("chains_total", C.c_int64), ("chain_offset", C.c_int64), ("log_steps", C.c_uint32),
         ("steps_per_launch", C.c_uint32), ("trace_capacity", C.c_uint64),
         ("region_capacity", C.c_uint64), ("b_substreams", C.c_uint64),
-        ("profile_kernels", C.c_int32), ("pad2_", C.c_int32),
+        ("profile_kernels", C.c_int32), ("accel", C.c_int32),
     ]
 
 

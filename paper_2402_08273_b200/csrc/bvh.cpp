@@ -1,0 +1,238 @@
+// bvh.cpp -- binned SAH BVH2 build (host, O(n log n)).
+#include "bvh.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+
+namespace ramlt_b200 {
+
+namespace {
+
+struct Box {
+    double lo[3], hi[3];
+    void reset() {
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::numeric_limits<double>::infinity();
+            hi[k] = -std::numeric_limits<double>::infinity();
+        }
+    }
+    void grow(const Box &b) {
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], b.lo[k]);
+            hi[k] = std::max(hi[k], b.hi[k]);
+        }
+    }
+    void grow(const double *p) {
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], p[k]);
+            hi[k] = std::max(hi[k], p[k]);
+        }
+    }
+    double area() const {
+        double d[3];
+        for (int k = 0; k < 3; ++k)
+            d[k] = std::max(0.0, hi[k] - lo[k]);
+        return 2.0 * (d[0] * d[1] + d[1] * d[2] + d[2] * d[0]);
+    }
+};
+
+struct Builder {
+    const double *tris;
+    std::vector<Box> tb;          // per-triangle bounds
+    std::vector<double> cen;      // centroids, 3 per triangle
+    std::vector<int32_t> idx;     // working order
+    std::vector<BvhBuildNode> nodes;
+    int leaf_max;
+    int depth = 0;
+
+    // Outward padding: a few ulps of the coordinate magnitude plus an absolute
+    // floor, so fp32/fp64 slab tests (with their own slack) never cull a hit.
+    static void pad(Box &b) {
+        for (int k = 0; k < 3; ++k) {
+            double m = std::max(std::fabs(b.lo[k]), std::fabs(b.hi[k]));
+            double e = m * 4e-7 + 1e-9;
+            b.lo[k] -= e;
+            b.hi[k] += e;
+        }
+    }
+
+    Box range_box(int s, int e) const {
+        Box b;
+        b.reset();
+        for (int i = s; i < e; ++i)
+            b.grow(tb[idx[i]]);
+        return b;
+    }
+
+    int32_t leaf(int s, int e) const { return ~((static_cast<int32_t>(s) << 4) | (e - s)); }
+
+    // Builds the subtree over idx[s, e) and returns its child reference.
+    int32_t build(int s, int e, int d) {
+        depth = std::max(depth, d);
+        int n = e - s;
+        if (n <= leaf_max || d >= 60)
+            return n <= 15 ? leaf(s, e) : split_median(s, e, d);
+        Box cb;
+        cb.reset();
+        for (int i = s; i < e; ++i)
+            cb.grow(&cen[3 * idx[i]]);
+        constexpr int B = 16;
+        double best_cost = std::numeric_limits<double>::infinity();
+        int best_axis = -1, best_bin = -1;
+        for (int ax = 0; ax < 3; ++ax) {
+            double ext = cb.hi[ax] - cb.lo[ax];
+            if (!(ext > 0.0))
+                continue;
+            Box bb[B];
+            int cnt[B] = {0};
+            for (auto &b : bb)
+                b.reset();
+            for (int i = s; i < e; ++i) {
+                int t = idx[i];
+                int bi = std::min(B - 1, static_cast<int>((cen[3 * t + ax] - cb.lo[ax]) / ext * B));
+                bb[bi].grow(tb[t]);
+                ++cnt[bi];
+            }
+            double la[B], ra[B];
+            int lc[B], rc[B];
+            Box acc;
+            acc.reset();
+            int c = 0;
+            for (int i = 0; i < B; ++i) {
+                acc.grow(bb[i]);
+                c += cnt[i];
+                la[i] = acc.area();
+                lc[i] = c;
+            }
+            acc.reset();
+            c = 0;
+            for (int i = B - 1; i >= 0; --i) {
+                acc.grow(bb[i]);
+                c += cnt[i];
+                ra[i] = acc.area();
+                rc[i] = c;
+            }
+            for (int i = 0; i + 1 < B; ++i) {
+                if (lc[i] == 0 || rc[i + 1] == 0)
+                    continue;
+                double cost = la[i] * lc[i] + ra[i + 1] * rc[i + 1];
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best_axis = ax;
+                    best_bin = i;
+                }
+            }
+        }
+        if (best_axis < 0)
+            return n <= 15 ? leaf(s, e) : split_median(s, e, d);
+        double ext = cb.hi[best_axis] - cb.lo[best_axis];
+        auto mid = std::partition(idx.begin() + s, idx.begin() + e, [&](int t) {
+            int bi = std::min(B - 1, static_cast<int>((cen[3 * t + best_axis] - cb.lo[best_axis]) / ext * B));
+            return bi <= best_bin;
+        });
+        int m = static_cast<int>(mid - idx.begin());
+        if (m == s || m == e)
+            return split_median(s, e, d);
+        return node(s, m, e, d);
+    }
+
+    int32_t split_median(int s, int e, int d) {
+        Box cb;
+        cb.reset();
+        for (int i = s; i < e; ++i)
+            cb.grow(&cen[3 * idx[i]]);
+        int ax = 0;
+        for (int k = 1; k < 3; ++k)
+            if (cb.hi[k] - cb.lo[k] > cb.hi[ax] - cb.lo[ax])
+                ax = k;
+        int m = (s + e) / 2;
+        std::nth_element(idx.begin() + s, idx.begin() + m, idx.begin() + e,
+                         [&](int a, int b) { return cen[3 * a + ax] < cen[3 * b + ax]; });
+        return node(s, m, e, d);
+    }
+
+    int32_t node(int s, int m, int e, int d) {
+        int self = static_cast<int>(nodes.size());
+        nodes.emplace_back();
+        Box l = range_box(s, m), r = range_box(m, e);
+        pad(l);
+        pad(r);
+        int32_t c0 = build(s, m, d + 1);
+        int32_t c1 = build(m, e, d + 1);
+        BvhBuildNode &nd = nodes[self];
+        std::memcpy(nd.lo[0], l.lo, sizeof(l.lo));
+        std::memcpy(nd.hi[0], l.hi, sizeof(l.hi));
+        std::memcpy(nd.lo[1], r.lo, sizeof(r.lo));
+        std::memcpy(nd.hi[1], r.hi, sizeof(r.hi));
+        nd.child[0] = c0;
+        nd.child[1] = c1;
+        return self;
+    }
+};
+
+}  // namespace
+
+BvhBuild build_bvh(const double *tris, size_t n, int leaf_max) {
+    if (n == 0)
+        throw std::invalid_argument("build_bvh: no triangles");
+    if (n >= (size_t(1) << 27))
+        throw std::invalid_argument("build_bvh: too many triangles");
+    Builder b;
+    b.tris = tris;
+    b.leaf_max = std::min(std::max(leaf_max, 1), 15);
+    b.tb.resize(n);
+    b.cen.resize(3 * n);
+    b.idx.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        Box bx;
+        bx.reset();
+        for (int v = 0; v < 3; ++v)
+            bx.grow(tris + 9 * i + 3 * v);
+        b.tb[i] = bx;
+        for (int k = 0; k < 3; ++k)
+            b.cen[3 * i + k] = 0.5 * (bx.lo[k] + bx.hi[k]);
+        b.idx[i] = static_cast<int32_t>(i);
+    }
+    b.nodes.reserve(2 * n / static_cast<size_t>(b.leaf_max) + 2);
+    // The root is always an internal node (a single leaf gets an empty sibling).
+    if (n <= static_cast<size_t>(b.leaf_max)) {
+        BvhBuildNode root;
+        Box bx = b.range_box(0, static_cast<int>(n));
+        Builder::pad(bx);
+        std::memcpy(root.lo[0], bx.lo, sizeof(bx.lo));
+        std::memcpy(root.hi[0], bx.hi, sizeof(bx.hi));
+        for (int k = 0; k < 3; ++k) {
+            root.lo[1][k] = 1.0;   // empty box: lo > hi never intersects
+            root.hi[1][k] = -1.0;
+        }
+        root.child[0] = b.leaf(0, static_cast<int>(n));
+        root.child[1] = b.leaf(0, 0);
+        b.nodes.push_back(root);
+    } else {
+        int32_t r = b.build(0, static_cast<int>(n), 0);
+        if (r < 0) {   // degenerate set collapsed into one leaf: wrap it
+            BvhBuildNode root;
+            Box bx = b.range_box(0, static_cast<int>(n));
+            Builder::pad(bx);
+            std::memcpy(root.lo[0], bx.lo, sizeof(bx.lo));
+            std::memcpy(root.hi[0], bx.hi, sizeof(bx.hi));
+            for (int k = 0; k < 3; ++k) {
+                root.lo[1][k] = 1.0;
+                root.hi[1][k] = -1.0;
+            }
+            root.child[0] = r;
+            root.child[1] = b.leaf(0, 0);
+            b.nodes.push_back(root);
+        }
+    }
+    BvhBuild out;
+    out.nodes = std::move(b.nodes);
+    out.order = std::move(b.idx);
+    out.depth = b.depth;
+    return out;
+}
+
+}  // namespace ramlt_b200

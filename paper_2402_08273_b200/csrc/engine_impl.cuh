@@ -2,6 +2,7 @@
 // barriers of run_render (core/driver.cpp:177-342) around the sm_100a kernels.
 #pragma once
 
+#include "bvh.h"
 #include "engine.h"
 #include "ramlt_kernels.cuh"
 #include "ramlt_step_co.cuh"
@@ -129,6 +130,9 @@ private:
     DBuf<rd::SphD<R>> sph_;
     DBuf<rd::MatD<R>> mat_;
     DBuf<rd::V3<R>> emit_;
+    DBuf<rd::BvhNodeD<R>> bvh_;
+    bool use_bvh_ = false;
+    int bvh_depth_ = 0;
     // chains
     DBuf<rd::GV<R>> verts_;
     DBuf<int> klen_;
@@ -217,6 +221,11 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         G_ = C_ <= 8192 ? 32 : 1;
     if (G_ != 1 && G_ != 2 && G_ != 4 && G_ != 8 && G_ != 16 && G_ != 32)
         throw std::invalid_argument("lanes_per_chain must be a power of two <= 32");
+    if (d.accel == RAMLT_ACCEL_BVH || (d.accel == RAMLT_ACCEL_AUTO && scene.tri.size() > 128))
+        G_ = 1;   // BVH traversal is per thread (lanes_per_chain applies to the brute-force path)
+    if (const char *v = std::getenv("RAMLT_ACCEL"))
+        if (std::string(v) == "bvh")
+            G_ = 1;
     ctl_ = d.strategy == RAMLT_FIXED ? 0 : (d.strategy == RAMLT_GLOBAL ? 1 : 2);
     pkind_ = 0;
     if (ctl_ == 2)
@@ -249,6 +258,58 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         tris[i].n = v3c<R>(n);
         tris[i].mat = t.material;
         tris[i].emi = t.emitter;
+        tris[i].orig = static_cast<int>(i);
+        tris[i].pad_ = 0;
+    }
+    // triangle accelerator: brute force from shared memory for small scenes,
+    // SAH BVH2 from L2/HBM above 128 triangles (identical results, see bvh.h)
+    {
+        int accel = d.accel;
+        if (const char *v = std::getenv("RAMLT_ACCEL"))
+            accel = std::string(v) == "bvh" ? RAMLT_ACCEL_BVH : (std::string(v) == "brute" ? RAMLT_ACCEL_BRUTE : accel);
+        use_bvh_ = !tris.empty() && (accel == RAMLT_ACCEL_BVH || (accel == RAMLT_ACCEL_AUTO && tris.size() > 128));
+    }
+    if (use_bvh_) {
+        std::vector<double> coords(9 * hs_.tri.size());
+        for (size_t i = 0; i < hs_.tri.size(); ++i) {
+            std::memcpy(&coords[9 * i + 0], hs_.tri[i].a, 3 * sizeof(double));
+            std::memcpy(&coords[9 * i + 3], hs_.tri[i].b, 3 * sizeof(double));
+            std::memcpy(&coords[9 * i + 6], hs_.tri[i].c, 3 * sizeof(double));
+        }
+        BvhBuild bb = build_bvh(coords.data(), hs_.tri.size(), 4);
+        bvh_depth_ = bb.depth;
+        if (bb.depth > 62)
+            throw std::runtime_error("BVH deeper than the traversal stack");
+        std::vector<rd::TriD<R>> ordered(tris.size());
+        for (size_t i = 0; i < tris.size(); ++i)
+            ordered[i] = tris[static_cast<size_t>(bb.order[i])];
+        tris.swap(ordered);
+        auto down = [](double x) {
+            R r = static_cast<R>(x);
+            if (static_cast<double>(r) > x)
+                r = std::nextafter(r, -std::numeric_limits<R>::infinity());
+            return r;
+        };
+        auto up = [](double x) {
+            R r = static_cast<R>(x);
+            if (static_cast<double>(r) < x)
+                r = std::nextafter(r, std::numeric_limits<R>::infinity());
+            return r;
+        };
+        std::vector<rd::BvhNodeD<R>> nodes(bb.nodes.size());
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            const BvhBuildNode &b = bb.nodes[i];
+            for (int k = 0; k < 3; ++k) {
+                nodes[i].lo0[k] = down(b.lo[0][k]);
+                nodes[i].hi0[k] = up(b.hi[0][k]);
+                nodes[i].lo1[k] = down(b.lo[1][k]);
+                nodes[i].hi1[k] = up(b.hi[1][k]);
+            }
+            nodes[i].c0 = b.child[0];
+            nodes[i].c1 = b.child[1];
+        }
+        bvh_.alloc(nodes.size());
+        RAMLT_CUDA(cudaMemcpy(bvh_.p, nodes.data(), nodes.size() * sizeof(nodes[0]), cudaMemcpyHostToDevice));
     }
     std::vector<rd::SphD<R>> sphs(hs_.sph.size());
     for (size_t i = 0; i < hs_.sph.size(); ++i) {
@@ -279,7 +340,8 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         RAMLT_CUDA(cudaMemcpy(mat_.p, mats.data(), mats.size() * sizeof(mats[0]), cudaMemcpyHostToDevice));
     if (!emit.empty())
         RAMLT_CUDA(cudaMemcpy(emit_.p, emit.data(), emit.size() * sizeof(emit[0]), cudaMemcpyHostToDevice));
-    smem_ = ((sphs.size() * sizeof(rd::SphD<R>) + 15) & ~size_t(15)) + tris.size() * sizeof(rd::TriD<R>);
+    smem_ = ((sphs.size() * sizeof(rd::SphD<R>) + 15) & ~size_t(15)) +
+            (use_bvh_ ? 0 : tris.size() * sizeof(rd::TriD<R>));
     if (smem_ > 200 * 1024)
         throw std::invalid_argument("scene too large for the shared-memory primitive path (" +
                                     std::to_string(hs_.tri.size()) + " triangles)");
@@ -489,6 +551,7 @@ template <class R> rd::StepParams<R> EngineT<R>::params() const {
     P.scene.cam.aspect = static_cast<R>(cb_.aspect);
     P.scene.cam.area = static_cast<R>(cb_.area);
     P.scene.cam.sensor = static_cast<R>(cb_.sensor);
+    P.scene.bvh = use_bvh_ ? bvh_.p : nullptr;
     P.C = C_;
     P.C_total = Ctot_;
     P.chain_off = off_;
@@ -597,7 +660,9 @@ template <class R> void EngineT<R>::estimate_b_partials(uint64_t begin, uint64_t
     rd::StepParams<R> P = params();
     unsigned blocks = static_cast<unsigned>((end - begin + 127) / 128);
     if (end > begin) {
-        auto kern = d_.rng == RAMLT_RNG_PHILOX ? rd::k_bsub<R, rd::RNG_PHILOX> : rd::k_bsub<R, rd::RNG_PCG>;
+        auto kern = d_.rng == RAMLT_RNG_PHILOX
+                        ? (use_bvh_ ? rd::k_bsub<R, rd::RNG_PHILOX, 0> : rd::k_bsub<R, rd::RNG_PHILOX, 1>)
+                        : (use_bvh_ ? rd::k_bsub<R, rd::RNG_PCG, 0> : rd::k_bsub<R, rd::RNG_PCG, 1>);
         RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
         kern<<<blocks, 128, smem_, stream_>>>(P, d_.b_samples, S, begin, end, part.p);
         ++launches_;
@@ -638,7 +703,9 @@ template <class R> void EngineT<R>::estimate_b(double *b, double *se) {
 
 template <class R> void EngineT<R>::init_chains() {
     rd::StepParams<R> P = params();
-    auto kern = d_.rng == RAMLT_RNG_PHILOX ? rd::k_init<R, rd::RNG_PHILOX> : rd::k_init<R, rd::RNG_PCG>;
+    auto kern = d_.rng == RAMLT_RNG_PHILOX
+                    ? (use_bvh_ ? rd::k_init<R, rd::RNG_PHILOX, 0> : rd::k_init<R, rd::RNG_PHILOX, 1>)
+                    : (use_bvh_ ? rd::k_init<R, rd::RNG_PCG, 0> : rd::k_init<R, rd::RNG_PCG, 1>);
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
     kern<<<static_cast<unsigned>((C_ + 127) / 128), 128, smem_, stream_>>>(P, 50000000ull);
     ++launches_;
@@ -666,7 +733,8 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
     void (*kern)(rd::StepParams<R>) = nullptr;
 #define RAMLT_PICK(RK)                                                                              \
-    switch (G_) {                                                                                   \
+    switch (use_bvh_ ? 0 : G_) {                                                                    \
+    case 0: kern = rd::k_step<R, RK, 0>; break;                                                     \
     case 1: kern = rd::k_step<R, RK, 1>; break;                                                     \
     case 2: kern = rd::k_step<R, RK, 2>; break;                                                     \
     case 4: kern = rd::k_step<R, RK, 4>; break;                                                     \
@@ -699,7 +767,9 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
 }
 
 template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P) {
-    auto kern = d_.rng == RAMLT_RNG_PHILOX ? rd::k_step_co<R, rd::RNG_PHILOX> : rd::k_step_co<R, rd::RNG_PCG>;
+    auto kern = d_.rng == RAMLT_RNG_PHILOX
+                    ? (use_bvh_ ? rd::k_step_co<R, rd::RNG_PHILOX, true> : rd::k_step_co<R, rd::RNG_PHILOX, false>)
+                    : (use_bvh_ ? rd::k_step_co<R, rd::RNG_PCG, true> : rd::k_step_co<R, rd::RNG_PCG, false>);
     size_t scene = (smem_ + 15) & ~size_t(15);
     size_t smem = scene + static_cast<size_t>(128) * d_.max_vertices * sizeof(rd::GV<R>);
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -740,7 +810,8 @@ bool EngineT<R>::launch_coop(int j0, int j1, unsigned long long span_start, unsi
             coop_state_ = 0;
     void (*kern)(rd::StepParams<R>, rd::CoopArgs<R>) = nullptr;
 #define RAMLT_PICK(RK)                                                                              \
-    switch (G_) {                                                                                   \
+    switch (use_bvh_ ? 0 : G_) {                                                                    \
+    case 0: kern = rd::k_step_coop<R, RK, 0>; break;                                                \
     case 1: kern = rd::k_step_coop<R, RK, 1>; break;                                                \
     case 2: kern = rd::k_step_coop<R, RK, 2>; break;                                                \
     case 4: kern = rd::k_step_coop<R, RK, 4>; break;                                                \

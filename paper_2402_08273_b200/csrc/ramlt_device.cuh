@@ -182,6 +182,15 @@ enum { EV_NONE = 0, EV_REFLECT = 1, EV_TRANSMIT = 2 };
 template <class R> struct TriD {   // a, e1 = b - a, e2 = c - a, n = normalize(cross(e1, e2))
     V3<R> a, e1, e2, n;
     int mat, emi;
+    int orig;   // index in the scene's triangle order (BVH leaves are reordered)
+    int pad_;
+};
+
+// BVH2 node: both children's boxes (padded outward at build time); child >= 0
+// internal node, < 0 leaf ~((first << 4) | count) into the reordered triangles.
+template <class R> struct alignas(16) BvhNodeD {
+    R lo0[3], hi0[3], lo1[3], hi1[3];
+    int c0, c1;
 };
 template <class R> struct SphD {
     V3<R> c;
@@ -205,6 +214,7 @@ template <class R> struct SceneView {
     const V3<R> *emit;
     int ntri, nsph;
     CamD<R> cam;
+    const BvhNodeD<R> *bvh;   // null: brute force over (smem-staged) triangles
 };
 
 template <class R> struct Hit {
@@ -213,14 +223,21 @@ template <class R> struct Hit {
     R t;
 };
 
-// Cooperative lane groups: G lanes share one chain; G = 1 is one chain per thread.
+// Cooperative lane groups: G lanes share one chain; G = 1 is one chain per
+// thread.  G = 0 is the BVH instantiation: one chain per thread, triangles
+// traversed through the BVH (a compile-time choice, so the brute-force kernels
+// carry no traversal code or stack).
+template <int G> struct Lanes {
+    static constexpr int n = G == 0 ? 1 : G;
+};
 template <int G> struct Group {
     unsigned mask;
     int lane;
     __device__ __forceinline__ Group() {
+        constexpr int N = Lanes<G>::n;
         int wl = threadIdx.x & 31;
-        lane = wl & (G - 1);
-        mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (wl & ~(G - 1)));
+        lane = wl & (N - 1);
+        mask = N == 32 ? 0xffffffffu : (((1u << N) - 1u) << (wl & ~(N - 1)));
     }
 };
 
@@ -271,6 +288,95 @@ __device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &
     return false;
 }
 
+// ---- BVH traversal ------------------------------------------------------------------
+// The result equals the reference's linear scan (core/scene.cpp:57-92): the
+// winner is the lexicographic minimum of (t, original primitive index) over all
+// hits below `lim`, and padded boxes plus a relative slack on the slab test
+// never cull a primitive the exact test accepts.
+template <class R> struct Slack;
+template <> struct Slack<float> {
+    static __device__ __forceinline__ float v() { return 1.0f + 2e-6f; }
+};
+template <> struct Slack<double> {
+    static __device__ __forceinline__ double v() { return 1.0 + 1e-13; }
+};
+
+template <class R>
+__device__ __forceinline__ bool slab(const R lo[3], const R hi[3], V3<R> o, V3<R> inv, R tcap, R &tnear) {
+    R tx0 = (lo[0] - o.x) * inv.x, tx1 = (hi[0] - o.x) * inv.x;
+    R ty0 = (lo[1] - o.y) * inv.y, ty1 = (hi[1] - o.y) * inv.y;
+    R tz0 = (lo[2] - o.z) * inv.z, tz1 = (hi[2] - o.z) * inv.z;
+    R tmin = fmax(fmax(fmin(tx0, tx1), fmin(ty0, ty1)), fmin(tz0, tz1));
+    R tmax = fmin(fmin(fmax(tx0, tx1), fmax(ty0, ty1)), fmax(tz0, tz1));
+    tmax = tmax * Slack<R>::v();
+    tnear = tmin;
+    return tmax >= tmin && tmax >= R(0) && tmin <= tcap * Slack<R>::v();
+}
+
+template <class R> __device__ __forceinline__ V3<R> safe_inv(V3<R> d) {
+    const R tiny = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
+    R x = M<R>::abs(d.x) < tiny ? M<R>::copysign(tiny, d.x) : d.x;
+    R y = M<R>::abs(d.y) < tiny ? M<R>::copysign(tiny, d.y) : d.y;
+    R z = M<R>::abs(d.z) < tiny ? M<R>::copysign(tiny, d.z) : d.z;
+    return mk(R(1) / x, R(1) / y, R(1) / z);
+}
+
+// Returns the winner's position in s.tri (BVH order) or -1; `key` carries the
+// combined original index (spheres first) used for ties.  With any_hit, stops
+// at the first primitive below lim (visibility).
+template <class R>
+__device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best, int &key, bool any_hit) {
+    V3<R> inv = safe_inv(d);
+    int pos = -1;
+    int stack[64];
+    int sp = 0;
+    int node = 0;
+    for (;;) {
+        const BvhNodeD<R> &n = s.bvh[node];
+        R t0, t1;
+        bool h0 = slab(n.lo0, n.hi0, o, inv, best, t0);
+        bool h1 = slab(n.lo1, n.hi1, o, inv, best, t1);
+        int c[2] = {n.c0, n.c1};
+        bool h[2] = {h0, h1};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (h[q] && c[q] < 0) {
+                int code = ~c[q];
+                int first = code >> 4, cnt = code & 15;
+                for (int k = first; k < first + cnt; ++k) {
+                    const TriD<R> &tr = s.tri[k];
+                    R t;
+                    if (!hit_tri(tr, o, d, t))
+                        continue;
+                    int kk = s.nsph + tr.orig;
+                    if (t < best || (t == best && kk < key)) {
+                        best = t;
+                        key = kk;
+                        pos = k;
+                        if (any_hit)
+                            return pos;
+                    }
+                }
+                h[q] = false;
+            }
+        }
+        if (h[0] && h[1]) {
+            bool first0 = t0 <= t1;
+            stack[sp++] = first0 ? c[1] : c[0];
+            node = first0 ? c[0] : c[1];
+        } else if (h[0]) {
+            node = c[0];
+        } else if (h[1]) {
+            node = c[1];
+        } else {
+            if (sp == 0)
+                break;
+            node = stack[--sp];
+        }
+    }
+    return pos;
+}
+
 // Closest hit (core/scene.cpp:57-92).  Primitive order = spheres then
 // triangles; each lane scans its stride-G subset in increasing order with
 // strict '<', and the (t, index) lexicographic minimum across lanes is the
@@ -278,6 +384,36 @@ __device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &
 template <class R, int G>
 __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> d, Hit<R> &h,
                                           const Group<G> &g) {
+    if constexpr (G == 0) {
+        // every lane of a group traverses the same ray: identical results, no reduction
+        R best = M<R>::inf();
+        int key = 0x7fffffff, spos = -1;
+        for (int i = 0; i < s.nsph; ++i) {
+            R t;
+            if (hit_sphere(s.sph[i], o, d, t) && t < best) {
+                best = t;
+                key = i;
+                spos = i;
+            }
+        }
+        int tpos = bvh_trace(s, o, d, best, best, key, false);
+        if (tpos < 0 && spos < 0)
+            return false;
+        h.t = best;
+        h.p = add(o, scl(d, best));
+        if (tpos < 0) {
+            const SphD<R> &sp = s.sph[spos];
+            h.n = unit(sub(h.p, sp.c));
+            h.mat = sp.mat;
+            h.emi = sp.emi;
+        } else {
+            const TriD<R> &tr = s.tri[tpos];
+            h.n = tr.n;
+            h.mat = tr.mat;
+            h.emi = tr.emi;
+        }
+        return true;
+    } else {
     R best = M<R>::inf();
     int bi = 0x7fffffff;
     for (int i = g.lane; i < s.nsph; i += G) {
@@ -321,6 +457,7 @@ __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> 
         h.emi = tr.emi;
     }
     return true;
+    }
 }
 
 // visible (core/scene.cpp:94-102) as an any-hit query: the reference's
@@ -334,6 +471,19 @@ __device__ __forceinline__ bool visible(const SceneView<R> &s, V3<R> a, V3<R> b,
     d = dvs(d, dist);
     R lim = dist - R(kEpsD);
     bool occ = false;
+    if constexpr (G == 0) {
+        for (int i = 0; i < s.nsph && !occ; ++i) {
+            R t;
+            if (hit_sphere(s.sph[i], a, d, t) && t < lim)
+                occ = true;
+        }
+        if (!occ) {
+            R best = lim;
+            int key = 0x7fffffff;
+            occ = bvh_trace(s, a, d, lim, best, key, true) >= 0;
+        }
+        return !occ;
+    } else {
     for (int i = g.lane; i < s.nsph && !occ; i += G) {
         R t;
         if (hit_sphere(s.sph[i], a, d, t) && t < lim)
@@ -347,6 +497,7 @@ __device__ __forceinline__ bool visible(const SceneView<R> &s, V3<R> a, V3<R> b,
     if (G > 1)
         occ = __any_sync(g.mask, occ);
     return !occ;
+    }
 }
 
 // ---- camera (core/camera.cpp:32-64) ---------------------------------------------------

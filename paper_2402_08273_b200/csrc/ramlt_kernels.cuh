@@ -529,7 +529,7 @@ template <class R> __device__ __forceinline__ size_t stage_bytes_sph(int nsph) {
 template <class R> __device__ SceneView<R> stage_scene(const SceneView<R> &g, char *smem) {
     SceneView<R> s = g;
     size_t bs = static_cast<size_t>(g.nsph) * sizeof(SphD<R>);
-    size_t bt = static_cast<size_t>(g.ntri) * sizeof(TriD<R>);
+    size_t bt = g.bvh ? 0 : static_cast<size_t>(g.ntri) * sizeof(TriD<R>);   // BVH: triangles stay in L2
     size_t off = stage_bytes_sph<R>(g.nsph);
     const unsigned *src_s = reinterpret_cast<const unsigned *>(g.sph);
     const unsigned *src_t = reinterpret_cast<const unsigned *>(g.tri);
@@ -541,7 +541,8 @@ template <class R> __device__ SceneView<R> stage_scene(const SceneView<R> &g, ch
         dst_t[i] = __ldg(src_t + i);
     __syncthreads();
     s.sph = reinterpret_cast<const SphD<R> *>(smem);
-    s.tri = reinterpret_cast<const TriD<R> *>(smem + off);
+    if (!g.bvh)
+        s.tri = reinterpret_cast<const TriD<R> *>(smem + off);
     return s;
 }
 
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(128) k_step(StepParams<R> P) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     Group<G> g;
-    const int c = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / G);
+    const int c = static_cast<int>((static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / Lanes<G>::n);
     if (c >= P.C)
         return;
     const long long gc = P.chain_off + c;
@@ -795,11 +796,11 @@ __global__ void __launch_bounds__(128) k_step(StepParams<R> P) {
 }
 
 // ---- chain initialisation (core/driver.cpp:219-242) -----------------------------------------
-template <class R, int RK>
+template <class R, int RK, int G>
 __global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long long max_attempts) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    Group<1> g;
+    Group<G> g;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P.C)
         return;
@@ -849,13 +850,13 @@ __global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long lon
 }
 
 // ---- estimate_b substreams (core/driver.cpp:31-57) --------------------------------------------
-template <class R, int RK>
+template <class R, int RK, int G>
 __global__ void __launch_bounds__(128) k_bsub(StepParams<R> P, unsigned long long n_samples,
                                               unsigned long long S_total, unsigned long long s_begin,
                                               unsigned long long s_end, double *partials) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    Group<1> g;
+    Group<G> g;
     unsigned long long s = s_begin + blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
     if (s >= s_end)
         return;
@@ -1423,7 +1424,7 @@ __global__ void __launch_bounds__(128) k_step_coop(StepParams<R> P, CoopArgs<R> 
     SceneView<R> S = stage_scene(P.scene, smem);
     Group<G> g;
     const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int c = static_cast<int>(tid / G);
+    const int c = static_cast<int>(tid / Lanes<G>::n);
     const bool active = c < P.C;
     const long long gc = P.chain_off + c;
     const unsigned long long my_steps = P.per + (static_cast<unsigned long long>(gc) < P.rem ? 1ull : 0ull);

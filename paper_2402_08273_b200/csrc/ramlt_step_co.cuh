@@ -27,8 +27,23 @@ template <class R> struct RayReq {
 
 // Closest hit below `lim` over spheres then triangles (core/scene.cpp:57-92);
 // ties resolved to the lowest primitive index exactly as the reference loop.
-template <class R>
+template <class R, bool BVH>
 __device__ __forceinline__ int trace_ray(const SceneView<R> &s, const RayReq<R> &r, R &t_out) {
+    if constexpr (BVH) {
+        R best = r.lim;
+        int key = 0x7fffffff, spos = -1;
+        for (int i = 0; i < s.nsph; ++i) {
+            R t;
+            if (hit_sphere(s.sph[i], r.o, r.d, t) && t < best) {
+                best = t;
+                key = i;
+                spos = i;
+            }
+        }
+        int tpos = bvh_trace(s, r.o, r.d, best, best, key, false);
+        t_out = best;
+        return tpos >= 0 ? s.nsph + tpos : spos;   // hit_record indexes s.tri by position
+    } else {
     R best = r.lim;
     int bi = -1;
     for (int i = 0; i < s.nsph; ++i) {
@@ -48,6 +63,7 @@ __device__ __forceinline__ int trace_ray(const SceneView<R> &s, const RayReq<R> 
     }
     t_out = best;
     return bi;
+    }
 }
 
 template <class R> __device__ __forceinline__ void hit_record(const SceneView<R> &s, const RayReq<R> &r, int prim,
@@ -607,11 +623,12 @@ __device__ __forceinline__ void co_store(const StepCo<R, RK> &co, const StepPara
 }
 
 // Persistent, work-stealing chain-step kernel.  `work` is a zeroed counter.
-template <class R, int RK>
+template <class R, int RK, bool BVH>
 __global__ void __launch_bounds__(128) k_step_co(StepParams<R> P, unsigned int *work) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    size_t scene_bytes = stage_bytes_sph<R>(P.scene.nsph) + static_cast<size_t>(P.scene.ntri) * sizeof(TriD<R>);
+    size_t scene_bytes = stage_bytes_sph<R>(P.scene.nsph) +
+                         (P.scene.bvh ? 0 : static_cast<size_t>(P.scene.ntri) * sizeof(TriD<R>));
     scene_bytes = (scene_bytes + 15) & ~size_t(15);
     PvSmem<R> pv{reinterpret_cast<GV<R> *>(smem + scene_bytes) + threadIdx.x, static_cast<int>(blockDim.x)};
     const unsigned lane = threadIdx.x & 31;
@@ -674,7 +691,7 @@ __global__ void __launch_bounds__(128) k_step_co(StepParams<R> P, unsigned int *
             break;
         if (want) {
             R t;
-            co.res_prim = trace_ray(S, co.ray, t);
+            co.res_prim = trace_ray<R, BVH>(S, co.ray, t);
             co.res_t = t;
             want = false;
         }

@@ -23,6 +23,7 @@ PERTURBATIONS = {"lens": 0, "multi-chain": 1}
 PRECISIONS = {"f32": 0, "f64": 1}
 RNGS = {"pcg32": 0, "philox": 1}
 ADAPT_MODES = {"auto": -1, "literal": 0, "pooled": 1}
+ACCELS = {"auto": 0, "brute": 1, "bvh": 2}
 
 
 class LogicError(RuntimeError):
@@ -87,6 +88,7 @@ class RenderConfig:
     region_capacity: int = 0
     b_substreams: int = 0
     profile_kernels: bool = False
+    accel: str = "auto"           # "brute" | "bvh"
 
     def to_c(self) -> _capi.ramlt_render_desc:
         d = _capi.ramlt_render_desc()
@@ -103,6 +105,8 @@ class RenderConfig:
                 v = RNGS[v]
             elif f.name == "adapt_mode":
                 v = ADAPT_MODES[v]
+            elif f.name == "accel":
+                v = ACCELS[v]
             elif isinstance(v, bool):
                 v = int(v)
             setattr(d, f.name, v)

@@ -184,4 +184,5 @@ SCENES = {
     "cornell": cornell_box,
     "caustic": caustic_box,
     "mirror": mirror_box,
+    "clusters": cluster_room,
 }
