@@ -23,13 +23,24 @@ sys.path.insert(0, ROOT)
 # BASELINE.json configs; "strategy/perturbation" follow the
 # reference defaults (RA-quadtree) and the survey's per-config perturbation.
 WORKLOADS = {
-    "c3": dict(scene="caustic", chains=262144, steps_per_chain=1 << 16, width=512, height=512,
-               max_vertices=17, strategy="ra-quadtree", perturbation="multi-chain",
+    "c3": dict(scene="caustic", scene_args={}, chains=262144, steps_per_chain=1 << 16, width=512,
+               height=512, max_vertices=17, strategy="ra-quadtree", perturbation="multi-chain",
+               bound="fp32", scaling="weak", e2e_steps=256, cpu_sample=1 << 21, cpu_b=4096,
                desc="C3 caustic box: 36 tri + glass sphere, 1% light, 512^2, path length 16, "
                     "262,144 chains"),
-    "c1": dict(scene="cornell", chains=1024, steps_per_chain=1 << 20, width=256, height=256,
-               max_vertices=9, strategy="ra-quadtree", perturbation="lens",
+    "c1": dict(scene="cornell", scene_args={}, chains=1024, steps_per_chain=1 << 20, width=256,
+               height=256, max_vertices=9, strategy="ra-quadtree", perturbation="lens",
+               bound="fp32", scaling="weak", e2e_steps=256, cpu_sample=1 << 21, cpu_b=4096,
                desc="C1 Cornell box: 36 tri, 256^2, path length 8, 1,024 chains"),
+    "c4": dict(scene="clusters", scene_args={"n_tris": 1 << 20}, chains=1 << 20, steps_per_chain=1 << 12,
+               width=1024, height=1024, max_vertices=13, strategy="ra-quadtree", perturbation="lens",
+               bound="hbm", scaling="weak", e2e_steps=32, cpu_sample=256, cpu_b=16,
+               desc="C4 clustered room: 2^20 + 20 tri (64 clusters, 4 lights), 1024^2, path length 12, "
+                    "1,048,576 chains, SAH BVH"),
+    "c5": dict(scene="clusters", scene_args={"n_tris": 1 << 20}, chains=1 << 23, steps_per_chain=1 << 12,
+               width=2048, height=2048, max_vertices=13, strategy="ra-quadtree", perturbation="lens",
+               bound="hbm", scaling="strong", e2e_steps=8, cpu_sample=256, cpu_b=16,
+               desc="C5 scaling config: the C4 scene at 2048^2, 8,388,608 chains split across the GPUs"),
 }
 METRIC = "MLT mutations/sec"
 UNIT = "mutations/s"
@@ -99,8 +110,9 @@ def oracle_rays_per_mutation(wl: dict, scene_text: str) -> float:
     counted by the CPU oracle on a small sample of the same variant and scene
     (SURVEY.md §8(d))."""
     from oracle.abi import OracleConfig, OracleLib
+    per = 60 if wl["scene"] == "clusters" else 300
     cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=64,
-                       mutations=64 * 300, width=wl["width"], height=wl["height"],
+                       mutations=64 * per, width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=20000, seed=3, rng="philox",
                        adapt_mode="pooled", m_refine=64 * 100, m_split=500)
     o = OracleLib().render(scene_text, cfg)
@@ -115,7 +127,7 @@ def cpu_reference_run(wl: dict, scene_text: str, mutations: int, threads: int):
     from oracle.abi import OracleConfig, RefLib, OracleLib, REF_SO
     cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=threads,
                        mutations=mutations, width=wl["width"], height=wl["height"],
-                       max_vertices=wl["max_vertices"], b_samples=4096, seed=1,
+                       max_vertices=wl["max_vertices"], b_samples=wl.get("cpu_b", 4096), seed=1,
                        metrics_interval=mutations, m_refine=10_000_000)
     if os.path.exists(REF_SO):
         out = RefLib(log=False).render(scene_text, cfg)
@@ -214,7 +226,7 @@ def run_e2e(args, wl):
     from paper_2402_08273_b200.render import RenderConfig
     lib = _capi.load()
     Cn = wl["chains"]
-    steps = max(args.steps, 256)
+    steps = max(args.steps, wl["e2e_steps"])
     cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=Cn,
                        mutations=Cn * steps, width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=2,
@@ -240,9 +252,9 @@ def run_e2e(args, wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=256)
-    ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="mutations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -251,31 +263,32 @@ def main():
 
     from paper_2402_08273_b200 import scenes
     wl = dict(WORKLOADS[args.workload])
-    wl["scene_text"] = scenes.SCENES[wl["scene"]]()
+    wl["scene_text"] = scenes.SCENES[wl["scene"]](**wl["scene_args"])
     world, rank, local = dist_env()
     threads = os.cpu_count() or 1
     config = {"workload": args.workload, "desc": wl["desc"], "chains": wl["chains"],
               "strategy": wl["strategy"], "perturbation": wl["perturbation"],
               "image": [wl["width"], wl["height"]], "max_vertices": wl["max_vertices"],
               "step": "one lockstep mutation of every chain",
-              "l2": "chain state exceeds the 126 MB L2 (c3: ~150 MB of path SoA); no flush",
+              "l2": "inputs larger than the 126 MB L2, no flush (chain path SoA: c3 134 MB, c4 400 MB, "
+                    "c5 3.2 GB; c4/c5 BVH + triangles ~120 MB)",
               "rng": "philox4x32-10", "adaptation": "pooled" if wl["chains"] > 4096 else "literal"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        sample = args.cpu_sample or (1 << 21)
+        sample = args.cpu_sample or wl["cpu_sample"]
         vals, times = [], []
         for _ in range(args.warmup if args.warmup < 3 else 1):
-            cpu_reference_run(wl, wl["scene_text"], sample // 8, threads)
-        for _ in range(args.steps if args.steps <= 8 else 8):
+            cpu_reference_run(wl, wl["scene_text"], max(sample // 8, threads), threads)
+        for _ in range(min(args.steps, 8 if wl["bound"] == "fp32" else 2)):
             v, kind, cores, t, chains = cpu_reference_run(wl, wl["scene_text"], sample, threads)
             vals.append(v)
             times.append(t)
         v = sum(vals) / len(vals)
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": len(vals),
                 "warmup": 1, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "impl": "reference", "config": dict(config, chains_cpu=chains),
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                                  "sample": f"{sample} mutations of the {args.workload} scene/variant "
@@ -288,7 +301,11 @@ def main():
     if res["rank"] != 0:
         return
     peaks = load_peaks()
-    r_m = oracle_rays_per_mutation(wl, wl["scene_text"])
+    rm_text = wl["scene_text"]
+    if wl["scene"] == "clusters":
+        from paper_2402_08273_b200 import scenes as _sc
+        rm_text = _sc.cluster_room(n_tris=4096)
+    r_m = oracle_rays_per_mutation(wl, rm_text)
     from paper_2402_08273_b200 import parse_scene
     n_mat, n_sph, n_tri, n_emi = parse_scene(wl["scene_text"]).counts
     flop_per_mut = r_m * (45.0 * n_tri + 20.0 * n_sph)
@@ -306,28 +323,46 @@ def main():
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic,
-                "peak_source": "nominal FP32 issue: 148 SM x 128 lanes x 2 x sm_max_mhz "
-                               "(MEASURED_PEAKS.json has no FP32 figure)",
-                "work_per_unit": f"R_m x (45 N_tri + 20 N_sph) = {r_m:.3f} x (45x{n_tri} + 20x{n_sph}) "
-                                 f"= {flop_per_mut:.0f} FLOP/mutation (R_m oracle-counted)",
-                "kernel": "k_step (chain-step megakernel)",
-                "kernel_share": res["step_ms"] / res["ms"] if res["ms"] else None}
+    if wl["bound"] == "fp32":
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak, "traffic": traffic,
+                    "peak_source": "nominal FP32 issue: 148 SM x 128 lanes x 2 x sm_max_mhz "
+                                   "(MEASURED_PEAKS.json has no FP32 figure)",
+                    "work_per_unit": f"R_m x (45 N_tri + 20 N_sph) = {r_m:.3f} x (45x{n_tri} + 20x{n_sph}) "
+                                     f"= {flop_per_mut:.0f} FLOP/mutation (R_m oracle-counted)"}
+    else:
+        # B = R_m x B_ray + B_state per mutation, B_ray = one
+        # BVH root-to-leaf descent (64 B per level) + 4 triangles x 48 B
+        import math
+        levels = max(1, math.ceil(math.log2(max(n_tri / 4.0, 2.0))))
+        b_ray = 64.0 * levels + 4 * 48.0
+        k_bar = 6.0
+        b_state = 2.0 * (16.0 * k_bar + 48.0) + 32.0
+        bytes_per_mut = r_m * b_ray + b_state
+        ach = per_launch_muts * bytes_per_mut / mean_launch_s / 1e9
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": traffic,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
+                    "work_per_unit": f"R_m x B_ray + B_state = {r_m:.3f} x {b_ray:.0f} B + {b_state:.0f} B "
+                                     f"= {bytes_per_mut:.0f} B/mutation (B_ray: {levels} BVH levels x 64 B + "
+                                     f"4 x 48 B; R_m oracle-counted on a 4096-triangle sample of the scene)"}
+    roofline.update({"kernel": "k_step (chain-step megakernel)",
+                     "kernel_share": res["step_ms"] / res["ms"] if res["ms"] else None})
     cpu = None
     if not args.no_cpu_baseline and res["world"] == 1:
-        sample = args.cpu_sample or (1 << 21)
+        sample = args.cpu_sample or wl["cpu_sample"]
         v, kind, cores, t, chains = cpu_reference_run(wl, wl["scene_text"], sample, threads)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{sample} mutations, chains = {chains} host threads, loop-only time "
                          f"{t:.2f} s (core/driver.cpp:246,262)"}
     e2e_v, h2d, d2h, _ = run_e2e(args, wl) if res["world"] == 1 else (None, 0, 0, 0)
-    e2e_steps = max(args.steps, 256)
+    e2e_steps = max(args.steps, wl["e2e_steps"])
     steps = args.steps
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": res["world"],
         "steps": steps, "warmup": args.warmup, "ms_per_step": res["ms"] / steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded stand-in scene, BASELINE.json config)", "config": config,
         "rays_per_s": {"device": res["rays_dev"] / (res["ms"] / 1e3) * res["world"],
                        "reference_equivalent": res["value"] * r_m, "r_m": r_m},

@@ -707,7 +707,14 @@ template <class R> void EngineT<R>::init_chains() {
                     ? (use_bvh_ ? rd::k_init<R, rd::RNG_PHILOX, 0> : rd::k_init<R, rd::RNG_PHILOX, 1>)
                     : (use_bvh_ ? rd::k_init<R, rd::RNG_PCG, 0> : rd::k_init<R, rd::RNG_PCG, 1>);
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
-    kern<<<static_cast<unsigned>((C_ + 127) / 128), 128, smem_, stream_>>>(P, 50000000ull);
+    int per_sm = 0, dev = 0, sms = 148;
+    RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem_));
+    RAMLT_CUDA(cudaGetDevice(&dev));
+    RAMLT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    unsigned blocks = std::min<unsigned>(static_cast<unsigned>((C_ + 127) / 128),
+                                         static_cast<unsigned>(std::max(per_sm, 1) * sms));
+    RAMLT_CUDA(cudaMemsetAsync(work_.p, 0, sizeof(unsigned), stream_));
+    kern<<<blocks, 128, smem_, stream_>>>(P, 50000000ull, work_.p);
     ++launches_;
     RAMLT_CUDA(cudaGetLastError());
     check_err("init");

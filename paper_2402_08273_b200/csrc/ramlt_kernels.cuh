@@ -797,18 +797,13 @@ __global__ void __launch_bounds__(128) k_step(StepParams<R> P) {
 
 // ---- chain initialisation (core/driver.cpp:219-242) -----------------------------------------
 template <class R, int RK, int G>
-__global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long long max_attempts) {
-    extern __shared__ __align__(16) char smem[];
-    SceneView<R> S = stage_scene(P.scene, smem);
+__device__ void init_chain(const StepParams<R> &P, const SceneView<R> &S, int c, unsigned long long max_attempts,
+                           RayCount &rc) {
     Group<G> g;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= P.C)
-        return;
     const long long gc = P.chain_off + c;
     Rng<RK> init;
     init.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(gc) * 2ull);
     Vx<R> pv[kMaxV];
-    RayCount rc;
     bool ok = false;
     for (unsigned long long t = 0; t < max_attempts; ++t) {
         int k;
@@ -847,6 +842,22 @@ __global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long lon
     Rng<RK> rng;
     rng.reseed(P.seed, static_cast<unsigned long long>(gc));
     RngIO<RK>::store(rng, P.ch.rng0, P.ch.rng1, c);
+}
+
+// Persistent, work-stealing chain initialisation: the number of attempts per
+// chain is geometric, so a lane that finishes takes the next chain instead of
+// idling until the warp's unluckiest chain is done.  `work` is zeroed.
+template <class R, int RK, int G>
+__global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long long max_attempts, unsigned int *work) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    RayCount rc;
+    for (;;) {
+        unsigned c = atomicAdd(work, 1u);
+        if (c >= static_cast<unsigned>(P.C))
+            break;
+        init_chain<R, RK, G>(P, S, static_cast<int>(c), max_attempts, rc);
+    }
 }
 
 // ---- estimate_b substreams (core/driver.cpp:31-57) --------------------------------------------

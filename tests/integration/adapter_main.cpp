@@ -4,6 +4,8 @@
 #include "scene.hpp"
 #include "ramlt_b200_adapter.hpp"
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <fstream>
 #include <sstream>
@@ -28,5 +30,8 @@ int main(int argc, char **argv) {
     ramlt::RenderResult cpu = ramlt::run_render(ramlt::parse_scene(ss.str()), cfg);
     std::printf("gpu acc=%.6f lum=%.3f  cpu acc=%.6f lum=%.3f  b gpu=%.4f cpu=%.4f\n", gpu.mean_acceptance,
                 gpu.film_luminance, cpu.mean_acceptance, cpu.film_luminance, gpu.b.b, cpu.b.b);
-    return gpu.mean_acceptance == cpu.mean_acceptance ? 0 : 1;
+    // Fixed strategy, reference PCG streams, fp64: identical decisions; only the
+    // cross-chain summation order of the mean differs.
+    double rel = std::abs(gpu.mean_acceptance - cpu.mean_acceptance) / std::max(cpu.mean_acceptance, 1e-300);
+    return rel < 1e-12 && gpu.total_mutations == cpu.total_mutations ? 0 : 1;
 }
