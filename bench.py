@@ -145,12 +145,19 @@ def run_ours(args, wl, scene_text):
     import torch
     import torch.distributed as dist
     from paper_2402_08273_b200 import Engine, RenderConfig
-    from paper_2402_08273_b200.distributed import ShardPlan, exchange_adaptation, all_gather_b
+    from paper_2402_08273_b200.distributed import ShardPlan, sharded_sync, all_gather_b
 
     world, rank, local = dist_env()
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # RAMLT_DIST_BACKEND=gloo runs the same N > 1 code path with ranks sharing
+        # a GPU (functional check on a 1-GPU box); production is NCCL.
+        backend = os.environ.get("RAMLT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     C = wl["chains"]
     plan = ShardPlan(C, world, rank)
     total_steps = args.warmup + args.steps
@@ -174,7 +181,7 @@ def run_ours(args, wl, scene_text):
     def step():
         eng.run(C)
         if world > 1:
-            exchange_adaptation(eng)
+            sharded_sync(eng)
 
     for _ in range(args.warmup):
         step()
@@ -249,6 +256,38 @@ def run_e2e(args, wl):
     return Cn * steps / (t1 - t0), len(text), img.nbytes, float(img.mean())
 
 
+def run_e2e_sharded(args, wl):
+    """N > 1 end to end through the public sharded API
+    (paper_2402_08273_b200.distributed.ShardedRender): scene text from host
+    memory, per-rank create, gathered b, init, K lockstep steps with the pooled
+    adaptation exchange, film SUM all-reduce, rank 0 copies the film to the host.
+    Wall clock, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2402_08273_b200.distributed import ShardedRender
+    from paper_2402_08273_b200.render import RenderConfig
+    Cn = wl["chains"]
+    steps = max(args.steps, wl["e2e_steps"])
+    cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=Cn,
+                       mutations=Cn * steps, width=wl["width"], height=wl["height"],
+                       max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=2,
+                       precision="f32", rng="philox", metrics_interval=Cn * steps)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sr = ShardedRender(wl["scene_text"], cfg)
+    film = sr.render()
+    host = film.cpu().numpy() if dist.get_rank() == 0 else None
+    torch.cuda.synchronize()
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                     device=torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sr.engine.close()
+    nbytes = host.nbytes if host is not None else 0
+    return Cn * steps / float(t.item()), len(wl["scene_text"]), nbytes, 0.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -298,6 +337,8 @@ def main():
         return
 
     res = run_ours(args, wl, wl["scene_text"])
+    if res["world"] > 1:
+        res["e2e"] = run_e2e_sharded(args, wl)
     if res["rank"] != 0:
         return
     peaks = load_peaks()
@@ -356,7 +397,7 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{sample} mutations, chains = {chains} host threads, loop-only time "
                          f"{t:.2f} s (core/driver.cpp:246,262)"}
-    e2e_v, h2d, d2h, _ = run_e2e(args, wl) if res["world"] == 1 else (None, 0, 0, 0)
+    e2e_v, h2d, d2h, _ = run_e2e(args, wl) if res["world"] == 1 else res["e2e"]
     e2e_steps = max(args.steps, wl["e2e_steps"])
     steps = args.steps
     line = {
@@ -369,8 +410,11 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu,
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,
-                "path": "ramlt_gpu_create_from_text + ramlt_gpu_render (b, init, K steps) + "
-                        "ramlt_gpu_read_image, host buffers, wall clock"},
+                "path": ("ramlt_gpu_create_from_text + ramlt_gpu_render (b, init, K steps) + "
+                         "ramlt_gpu_read_image, host buffers, wall clock") if res["world"] == 1 else
+                        ("distributed.ShardedRender: per-rank create from host scene text, gathered b, "
+                         "init, K steps with pooled exchange, film all-reduce, rank-0 D2H; wall clock, "
+                         "max over ranks")},
         "gpu_launches": res["launches"], "clocks": res["clocks"],
     }
     print(json.dumps(line), flush=True)

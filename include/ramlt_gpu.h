@@ -259,8 +259,15 @@ RAMLT_API int ramlt_gpu_adapt_exchange(ramlt_gpu *h, uint64_t **counts, uint64_t
                              uint64_t **last_index, uint64_t *n_regions);
 RAMLT_API int ramlt_gpu_adapt_apply(ramlt_gpu *h);
 /* Split a run into externally synchronised chunks: the engine pauses for an
- * exchange every `steps` lockstep steps (0 = never). */
+ * exchange every `steps` lockstep steps (0 = never).  In this mode quadtree
+ * refinement at m_refine barriers is deferred: the caller SUM-all-reduces the
+ * per-region visit counts (ramlt_gpu_visits_device) and calls
+ * ramlt_gpu_refine on every rank (identical partitions); keep_counts = 0 on all
+ * ranks but one so carried-over counts are summed once. */
 RAMLT_API int ramlt_gpu_set_exchange_interval(ramlt_gpu *h, uint32_t steps);
+RAMLT_API int ramlt_gpu_visits_device(ramlt_gpu *h, uint64_t **visits, uint64_t *n_regions);
+RAMLT_API int ramlt_gpu_refine_pending(ramlt_gpu *h, int32_t *pending);
+RAMLT_API int ramlt_gpu_refine(ramlt_gpu *h, int32_t keep_counts);
 
 RAMLT_API const char *ramlt_gpu_last_error(ramlt_gpu *h);
 RAMLT_API void ramlt_gpu_destroy(ramlt_gpu *h);

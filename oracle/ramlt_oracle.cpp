@@ -1115,7 +1115,8 @@ struct Out {
     double loop_s = 0.0;
 };
 
-static inline uint64_t to_fx(double a) { return static_cast<uint64_t>(a * 4294967296.0 + 0.5); }
+// pooled rule: 2^-24 fixed point, the GPU engine's resolution (k_adapt_pool_accum)
+static inline uint64_t to_fx(double a) { return static_cast<uint64_t>(a * 16777216.0 + 0.5); }
 
 // Single-sample b estimator value (core/driver.cpp:36-50).
 static double b_sample(const Scene &s, Rng &rng, int maxv) {
@@ -1297,7 +1298,7 @@ struct Render {
                 Region &r = reg[kv.first];
                 if (r.pend_n < static_cast<uint32_t>(ad.L))
                     continue;
-                double ah = std::clamp(static_cast<double>(r.pend_fx) / 4294967296.0 /
+                double ah = std::clamp(static_cast<double>(r.pend_fx) / 16777216.0 /
                                            static_cast<double>(r.pend_n), 0.0, 1.0);
                 uint64_t n = r.n;
                 r.lambda = lambda_next(r.lambda, ah, n, ad);
@@ -1558,7 +1559,7 @@ struct Render {
         out.done = done;
         out.mean_acc = out.npert > 0 ? acc / static_cast<double>(out.npert) : 0.0;
         for (Region &r : reg) {
-            double ta = c.adapt_mode == 1 ? static_cast<double>(r.tot_fx) / 4294967296.0 : r.tot_acc;
+            double ta = c.adapt_mode == 1 ? static_cast<double>(r.tot_fx) / 16777216.0 : r.tot_acc;
             out.tallies.push_back({ta, r.tot_vis});
         }
         // global_acceptance_identity (core/adaptation.cpp:103-125)

@@ -113,6 +113,9 @@ SIGNATURES = {
                                            P(P(C.c_uint64)), P(C.c_uint64)]),
     "ramlt_gpu_adapt_apply": (C.c_int, [H]),
     "ramlt_gpu_set_exchange_interval": (C.c_int, [H, C.c_uint32]),
+    "ramlt_gpu_visits_device": (C.c_int, [H, P(P(C.c_uint64)), P(C.c_uint64)]),
+    "ramlt_gpu_refine_pending": (C.c_int, [H, P(C.c_int32)]),
+    "ramlt_gpu_refine": (C.c_int, [H, C.c_int32]),
     "ramlt_gpu_last_error": (C.c_char_p, [H]),
     "ramlt_gpu_destroy": (None, [H]),
 }

@@ -55,6 +55,9 @@ public:
     virtual void adapt_exchange(uint64_t **cnt, uint64_t **fx, uint64_t **last, uint64_t *n) = 0;
     virtual void adapt_apply() = 0;
     virtual void set_exchange_interval(uint32_t steps) = 0;
+    virtual void visits_device(uint64_t **visits, uint64_t *n) = 0;
+    virtual bool refine_pending() = 0;
+    virtual void refine_now(bool keep_counts) = 0;
 
     std::string last_error;
 };

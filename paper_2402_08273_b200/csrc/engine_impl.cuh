@@ -89,6 +89,20 @@ public:
     }
     void adapt_apply() override;
     void set_exchange_interval(uint32_t steps) override { exchange_interval_ = steps; }
+    void visits_device(uint64_t **visits, uint64_t *n) override {
+        *visits = reinterpret_cast<uint64_t *>(visits_.p);
+        *n = static_cast<uint64_t>(n_regions_host_);
+    }
+    bool refine_pending() override { return refine_pending_; }
+    void refine_now(bool keep_counts) override {
+        if (!refine_pending_)
+            return;
+        refine_pending_ = false;
+        refine();
+        if (!keep_counts)
+            RAMLT_CUDA(cudaMemsetAsync(visits_.p, 0, static_cast<size_t>(n_regions_host_) * sizeof(unsigned long long),
+                                       stream_));
+    }
 
 private:
     rd::StepParams<R> params() const;
@@ -124,6 +138,7 @@ private:
     cudaStream_t stream_ = nullptr;
     bool own_stream_ = true;
     uint32_t exchange_interval_ = 0;
+    bool refine_pending_ = false;   // sharded runs: refine after the visit all-reduce
 
     // scene
     DBuf<rd::TriD<R>> tri_;
@@ -1000,7 +1015,10 @@ template <class R> void EngineT<R>::run(uint64_t mutations) {
         }
         done_ += span;
         if (done_ == next_refine_) {
-            refine();
+            if (exchange_interval_ && (pkind_ == 2 || pkind_ == 4))
+                refine_pending_ = true;   // caller all-reduces visits, then ramlt_gpu_refine
+            else
+                refine();
             next_refine_ += d_.m_refine;
         }
         if (done_ == next_metrics_ || done_ == d_.mutations) {

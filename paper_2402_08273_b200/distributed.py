@@ -102,6 +102,28 @@ def exchange_adaptation(engine):
     engine.adapt_apply()
 
 
+def sync_refine(engine):
+    """Deferred quadtree refine of a sharded run: SUM the
+    per-region visit counts, refine identically on every rank, and keep the
+    carried-over counts on rank 0 only."""
+    import torch
+    import torch.distributed as dist
+    if not engine.refine_pending():
+        return False
+    ptr, n = engine.visits_device()
+    if n:
+        v = device_tensor(ptr, n, "<u8").view(dtype=torch.int64)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+    engine.refine(keep_counts=dist.get_rank() == 0)
+    return True
+
+
+def sharded_sync(engine):
+    """Everything a sharded run exchanges after a lockstep step."""
+    exchange_adaptation(engine)
+    sync_refine(engine)
+
+
 def reduce_film(engine):
     """SUM all-reduce of the fp64 film in place on every rank (NCCL)."""
     import torch.distributed as dist
@@ -152,7 +174,7 @@ class ShardedRender:
         while done < mutations:
             m = min(step, mutations - done)
             self.engine.run(m)
-            exchange_adaptation(self.engine)
+            sharded_sync(self.engine)
             done += m
 
     def render(self):

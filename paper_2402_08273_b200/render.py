@@ -318,6 +318,20 @@ class Engine:
     def set_exchange_interval(self, steps: int):
         self._check(self.lib.ramlt_gpu_set_exchange_interval(self.h, steps))
 
+    def visits_device(self):
+        p = C.POINTER(C.c_uint64)()
+        n = C.c_uint64()
+        self._check(self.lib.ramlt_gpu_visits_device(self.h, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value, n.value
+
+    def refine_pending(self) -> bool:
+        f = C.c_int32()
+        self._check(self.lib.ramlt_gpu_refine_pending(self.h, C.byref(f)))
+        return bool(f.value)
+
+    def refine(self, keep_counts: bool):
+        self._check(self.lib.ramlt_gpu_refine(self.h, int(keep_counts)))
+
     def result(self) -> RenderResult:
         s = self.stats()
         return RenderResult(
