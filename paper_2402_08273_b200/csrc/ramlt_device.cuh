@@ -324,55 +324,74 @@ template <class R> __device__ __forceinline__ V3<R> safe_inv(V3<R> d) {
 // Returns the winner's position in s.tri (BVH order) or -1; `key` carries the
 // combined original index (spheres first) used for ties.  With any_hit, stops
 // at the first primitive below lim (visibility).
+//
+// "While-while" traversal with one postponed leaf (Aila & Laine 2009): lanes
+// descend internal nodes until every still-traversing lane holds a leaf, then
+// all of them test their leaf's triangles together, so the slab tests and the
+// triangle tests each run with the warp's lanes converged.  Every box that
+// overlaps [0, best] is still visited, so the result is exactly the linear
+// scan's.
 template <class R>
 __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best, int &key, bool any_hit) {
+    constexpr int DONE = 0x7fffffff;
     V3<R> inv = safe_inv(d);
+    (void)lim;
     int pos = -1;
     int stack[64];
     int sp = 0;
-    int node = 0;
+    int node = 0;    // >= 0 internal node, < 0 leaf code, DONE
+    int leaf = 0;    // postponed leaf code (< 0) or 0
     for (;;) {
-        const BvhNodeD<R> &n = s.bvh[node];
-        R t0, t1;
-        bool h0 = slab(n.lo0, n.hi0, o, inv, best, t0);
-        bool h1 = slab(n.lo1, n.hi1, o, inv, best, t1);
-        int c[2] = {n.c0, n.c1};
-        bool h[2] = {h0, h1};
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            if (h[q] && c[q] < 0) {
-                int code = ~c[q];
-                int first = code >> 4, cnt = code & 15;
-                for (int k = first; k < first + cnt; ++k) {
-                    const TriD<R> &tr = s.tri[k];
-                    R t;
-                    if (!hit_tri(tr, o, d, t))
-                        continue;
-                    int kk = s.nsph + tr.orig;
-                    if (t < best || (t == best && kk < key)) {
-                        best = t;
-                        key = kk;
-                        pos = k;
-                        if (any_hit)
-                            return pos;
-                    }
+        while (node >= 0 && node != DONE) {
+            const BvhNodeD<R> &n = s.bvh[node];
+            R t0, t1;
+            bool h0 = slab(n.lo0, n.hi0, o, inv, best, t0);
+            bool h1 = slab(n.lo1, n.hi1, o, inv, best, t1);
+            if (h0 && h1) {
+                bool near0 = t0 <= t1;
+                stack[sp++] = near0 ? n.c1 : n.c0;
+                node = near0 ? n.c0 : n.c1;
+            } else if (h0) {
+                node = n.c0;
+            } else if (h1) {
+                node = n.c1;
+            } else {
+                node = sp ? stack[--sp] : DONE;
+            }
+            if (node < 0) {   // reached a leaf
+                if (leaf != 0)
+                    break;    // slot busy: test the postponed leaf first
+                leaf = node;
+                node = sp ? stack[--sp] : DONE;
+            }
+            if (__all_sync(__activemask(), leaf != 0))
+                break;
+        }
+        while (leaf < 0) {
+            int code = ~leaf;
+            int first = code >> 4, cnt = code & 15;
+            for (int k = first; k < first + cnt; ++k) {
+                const TriD<R> &tr = s.tri[k];
+                R t;
+                if (!hit_tri(tr, o, d, t))
+                    continue;
+                int kk = s.nsph + tr.orig;
+                if (t < best || (t == best && kk < key)) {
+                    best = t;
+                    key = kk;
+                    pos = k;
+                    if (any_hit)
+                        return pos;
                 }
-                h[q] = false;
+            }
+            leaf = 0;
+            if (node < 0) {   // the next popped entry was a leaf too
+                leaf = node;
+                node = sp ? stack[--sp] : DONE;
             }
         }
-        if (h[0] && h[1]) {
-            bool first0 = t0 <= t1;
-            stack[sp++] = first0 ? c[1] : c[0];
-            node = first0 ? c[0] : c[1];
-        } else if (h[0]) {
-            node = c[0];
-        } else if (h[1]) {
-            node = c[1];
-        } else {
-            if (sp == 0)
-                break;
-            node = stack[--sp];
-        }
+        if (node == DONE)
+            break;
     }
     return pos;
 }
