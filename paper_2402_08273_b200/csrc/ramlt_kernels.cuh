@@ -165,7 +165,7 @@ struct RayCount {
 // core/path.cpp:7-17
 template <class R, int G>
 __device__ __forceinline__ R geom_term(const SceneView<R> &S, const Vx<R> &a, const Vx<R> &b,
-                                       const Group<G> &g, RayCount &rc) {
+                                       const Group<G> &g, RayCount &rc, bool known_visible = false) {
     V3<R> d = sub(b.p, a.p);
     R d2 = dot(d, d);
     if (d2 <= R(0))
@@ -174,6 +174,8 @@ __device__ __forceinline__ R geom_term(const SceneView<R> &S, const Vx<R> &a, co
     R gt = M<R>::abs(dot(a.n, dir)) * M<R>::abs(dot(b.n, dir)) / d2;
     if (gt <= R(0))
         return R(0);
+    if (known_visible)
+        return gt;
     ++rc.v;
     return visible(S, a.p, b.p, g) ? gt : R(0);
 }
@@ -181,7 +183,7 @@ __device__ __forceinline__ R geom_term(const SceneView<R> &S, const Vx<R> &a, co
 // core/path.cpp:19-29
 template <class R, int G>
 __device__ __forceinline__ R area_conv(const SceneView<R> &S, V3<R> from, const Vx<R> &b,
-                                       const Group<G> &g, RayCount &rc) {
+                                       const Group<G> &g, RayCount &rc, bool known_visible = false) {
     V3<R> d = sub(b.p, from);
     R d2 = dot(d, d);
     if (d2 <= R(0))
@@ -190,6 +192,8 @@ __device__ __forceinline__ R area_conv(const SceneView<R> &S, V3<R> from, const 
     R c = M<R>::abs(dot(b.n, dir)) / d2;
     if (c <= R(0))
         return R(0);
+    if (known_visible)
+        return c;
     ++rc.v;
     return visible(S, from, b.p, g) ? c : R(0);
 }
@@ -200,9 +204,12 @@ template <class R> struct Contrib {
 };
 
 // eval_contribution (core/path.cpp:40-82)
+// vis_from: segments (i, i+1) with i >= vis_from are segments of the chain's
+// current path (bit-identical vertices).  That path has pi > 0, so their
+// visibility test already passed: the ray is skipped, the value is unchanged.
 template <class R, int G, class P>
 __device__ Contrib<R> evaluate(const SceneView<R> &S, const P &path, int k, const Group<G> &g,
-                               RayCount &rc) {
+                               RayCount &rc, int vis_from = 0x7fffffff) {
     Contrib<R> z;
     z.f = mk(R(0), R(0), R(0));
     z.pi = R(0);
@@ -225,7 +232,7 @@ __device__ Contrib<R> evaluate(const SceneView<R> &S, const P &path, int k, cons
         Vx<R> b = path.get(i + 1);
         if (i > 0 && a.emi >= 0)
             return z;
-        R seg = a.spec ? area_conv(S, a.p, b, g, rc) : geom_term(S, a, b, g, rc);
+        R seg = a.spec ? area_conv(S, a.p, b, g, rc, i >= vis_from) : geom_term(S, a, b, g, rc, i >= vis_from);
         if (seg <= R(0))
             return z;
         f = scl(f, seg);
@@ -643,7 +650,7 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
             PropPath<R> prop{pv, head_end, &cur};
             tf = pert_density(cur, prop, pmask, endpoint, kt.k1, kt.k2);
             tr = pert_density(prop, cur, pmask, endpoint, kt.k1, kt.k2);
-            pc = evaluate(S, prop, cs.k, g, rc);
+            pc = evaluate(S, prop, cs.k, g, rc, endpoint + 1);
             if (pc.pi > R(0)) {
                 if (P.ctl == 2) {
                     R pu = R(0), pv_ = R(0);

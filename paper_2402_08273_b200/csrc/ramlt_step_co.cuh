@@ -377,6 +377,10 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                                : M<R>::abs(dot(av.n, dir)) * M<R>::abs(dot(bv.n, dir)) / d2;
                 if (eseg <= R(0))
                     goto eval_fail;
+                // unchanged tail segment of a perturbation: visibility already held
+                // for the current path (pi > 0), so no ray (see evaluate)
+                if (choose && ei > endpoint)
+                    goto eval_seg_visible;
                 ++rc.v;
                 // visible(a, b) (scene.cpp:94-102)
                 R dist = len(dd);
@@ -387,9 +391,10 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                 ep = dist - R(kEpsD);
             }
             CO_RAY(o, d, ep, 3);
+            if (res_prim >= 0)
+                goto eval_fail;
+        eval_seg_visible:
             {
-                if (res_prim >= 0)
-                    goto eval_fail;
                 ef = scl(ef, eseg);
                 if (ei > 0) {
                     PropS<R> prop{pv, head_end, &cur};
