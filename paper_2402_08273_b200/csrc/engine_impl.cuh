@@ -152,7 +152,8 @@ private:
     DBuf<rd::GV<R>> verts_;
     DBuf<int> klen_;
     DBuf<unsigned> smask_;
-    DBuf<R> cf_, cr_, eyeden_;
+    DBuf<R> cf_, cr_;
+    DBuf<double> eyeden_;
     DBuf<unsigned long long> rng0_, rng1_;
     DBuf<double> acc_, iacc_, lum_;
     DBuf<unsigned long long> npert_, nlarge_, ipert_, nsteps_;

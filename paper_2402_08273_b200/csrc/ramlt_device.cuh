@@ -630,7 +630,9 @@ template <class R> __device__ __forceinline__ R kern_pdf(const Kern<R> &k, R th)
 }
 template <class R> __device__ __forceinline__ R kern_pdf_sa(const Kern<R> &k, R alpha) {
     R s = M<R>::sin(alpha);
-    const R floor_ = sizeof(R) == 8 ? R(1e-300) : R(1e-37);
+    // fp32: pdf <= 0.4 / sigma <= 1.4e6 for sigma >= e^-15, so 1e-30 keeps the
+    // quotient finite when a direction did not move in fp32 (alpha = 0).
+    const R floor_ = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
     s = s > floor_ ? s : floor_;
     return kern_pdf(k, alpha) / (R(kPiD) * s);
 }

@@ -76,7 +76,7 @@ template <class R> struct ChainArrays {
     unsigned int *smask;
     R *cf;          // [4][C]: f.x f.y f.z pi
     R *cr;          // [2][C]: raster u v
-    R *eyeden;      // cached eye_path_density(current), NaN = unknown
+    double *eyeden; // cached eye_path_density(current), NaN = unknown
     unsigned long long *rng0, *rng1;
     double *acc, *iacc, *lum;
     unsigned long long *npert, *nlarge, *ipert, *nsteps;
@@ -268,9 +268,12 @@ __device__ Contrib<R> evaluate(const SceneView<R> &S, const P &path, int k, cons
 
 // trace_eye_subpath (core/path.cpp:84-142) into pv[0..k-1]; tf = prod of
 // dir_pdf * area_conv (large_step t_forward, mutations.cpp:63-66).
+// Transition densities and the Metropolis ratio are carried in fp64 in every
+// build (as in the reference): products of up to 16 area conversions and the
+// truncated-normal pdf at tiny sigma overflow fp32.
 template <class R, int G, class RNG>
 __device__ bool trace_eye(const SceneView<R> &S, RNG &rng, int maxv, Vx<R> *pv, int &k,
-                          unsigned &sm, R &tf, const Group<G> &g, RayCount &rc) {
+                          unsigned &sm, double &tf, const Group<G> &g, RayCount &rc) {
     Vx<R> cv;
     cv.p = S.cam.pos;
     cv.n = S.cam.fwd;
@@ -281,7 +284,7 @@ __device__ bool trace_eye(const SceneView<R> &S, RNG &rng, int maxv, Vx<R> *pv, 
     pv[0] = cv;
     k = 1;
     sm = 0;
-    tf = R(1);
+    tf = 1.0;
     if (maxv < 2)
         return false;
     R u = Unit<R>::draw(rng);
@@ -302,7 +305,7 @@ __device__ bool trace_eye(const SceneView<R> &S, RNG &rng, int maxv, Vx<R> *pv, 
         const MatD<R> m = S.mat[h.mat];
         x.spec = h.emi < 0 && (m.kind == MAT_MIRROR || m.kind == MAT_DIELECTRIC);
         x.ev = EV_NONE;
-        tf *= dpdf * (M<R>::abs(dot(h.n, dir)) / (h.t * h.t));
+        tf *= static_cast<double>(dpdf * (M<R>::abs(dot(h.n, dir)) / (h.t * h.t)));
         pv[k] = x;
         if (x.spec)
             sm |= 1u << k;
@@ -324,30 +327,30 @@ __device__ bool trace_eye(const SceneView<R> &S, RNG &rng, int maxv, Vx<R> *pv, 
 
 // eye_path_density (core/path.cpp:144-170)
 template <class R, int G, class P>
-__device__ R eye_density(const SceneView<R> &S, const P &path, int k, const Group<G> &g, RayCount &rc) {
+__device__ double eye_density(const SceneView<R> &S, const P &path, int k, const Group<G> &g, RayCount &rc) {
     if (k < 2)
-        return R(0);
+        return 0.0;
     if (path.get(k - 1).emi < 0)
-        return R(0);
-    R p = cam_dir_pdf(S.cam, pdir<R>(path, 0));
-    if (p <= R(0))
-        return R(0);
+        return 0.0;
+    double p = static_cast<double>(cam_dir_pdf(S.cam, pdir<R>(path, 0)));
+    if (p <= 0.0)
+        return 0.0;
     Vx<R> prev = path.get(0);
     Vx<R> a = path.get(1);
-    p *= area_conv(S, prev.p, a, g, rc);
+    p *= static_cast<double>(area_conv(S, prev.p, a, g, rc));
     for (int i = 1; i + 1 < k; ++i) {
         if (a.emi >= 0)
-            return R(0);
+            return 0.0;
         Vx<R> b = path.get(i + 1);
         const MatD<R> m = S.mat[a.mat];
         V3<R> wi = unit(sub(prev.p, a.p));
         V3<R> wo = unit(sub(b.p, a.p));
         R q = a.spec ? spec_prob(m, wi, a.n, a.ev) : bsdf_pdf(m, wi, wo, a.n);
         if (q <= R(0))
-            return R(0);
-        p *= q * area_conv(S, a.p, b, g, rc);
-        if (p <= R(0))
-            return R(0);
+            return 0.0;
+        p *= static_cast<double>(q * area_conv(S, a.p, b, g, rc));
+        if (p <= 0.0)
+            return 0.0;
         prev = a;
         a = b;
     }
@@ -438,10 +441,14 @@ __device__ bool retrace(const SceneView<R> &S, const CurPath<R> &ref, int kref, 
 }
 
 // perturbation_density (core/mutations.cpp:176-196)
+template <class R> __device__ __forceinline__ Kern<double> kern_d(const Kern<R> &k) {
+    return Kern<double>{static_cast<double>(k.sigma), static_cast<double>(k.lo), static_cast<double>(k.mass)};
+}
+
 template <class R, class PF, class PT>
-__device__ __noinline__ R pert_density(const PF &from, const PT &to, unsigned pmask, int endpoint,
+__device__ __noinline__ double pert_density(const PF &from, const PT &to, unsigned pmask, int endpoint,
                           const Kern<R> &k1, const Kern<R> &k2) {
-    R q = R(1);
+    double q = 1.0;
     unsigned m = pmask;
     while (m) {
         int idx = __ffs(m) - 1;
@@ -449,7 +456,7 @@ __device__ __noinline__ R pert_density(const PF &from, const PT &to, unsigned pm
         V3<R> a = pdir<R>(from, idx);
         V3<R> b = pdir<R>(to, idx);
         R alpha = M<R>::atan2(len(cross(a, b)), dot(a, b));
-        q *= kern_pdf_sa(idx == 0 ? k1 : k2, alpha);
+        q *= static_cast<double>(kern_pdf_sa(idx == 0 ? k1 : k2, alpha));
     }
     Vx<R> p0 = to.get(0);
     for (int i = 0; i < endpoint; ++i) {
@@ -457,21 +464,21 @@ __device__ __noinline__ R pert_density(const PF &from, const PT &to, unsigned pm
         V3<R> d = sub(p1.p, p0.p);
         R d2 = dot(d, d);
         if (d2 <= R(0))
-            return R(0);
-        q *= M<R>::abs(dot(p1.n, d)) / (d2 * M<R>::sqrt(d2));
+            return 0.0;
+        q *= static_cast<double>(M<R>::abs(dot(p1.n, d)) / (d2 * M<R>::sqrt(d2)));
         p0 = p1;
     }
     return q;
 }
 
 // mh_accept (core/mutations.cpp:198-208); pi_current > 0 holds for every chain.
-template <class R> __device__ __forceinline__ R mh_accept(R pc, R pp, R tf, R tr, R sf, R sr) {
-    if (!(pp > R(0)) || !(tf > R(0)) || !(sf > R(0)))
-        return R(0);
-    R r = (pp * tr * sr) / (pc * tf * sf);
-    if (M<R>::isnan(r))
-        return R(0);
-    return r < R(1) ? r : R(1);
+__device__ __forceinline__ double mh_accept(double pc, double pp, double tf, double tr, double sf, double sr) {
+    if (!(pp > 0.0) || !(tf > 0.0) || !(sf > 0.0))
+        return 0.0;
+    double r = (pp * tr * sr) / (pc * tf * sf);
+    if (::isnan(r))
+        return 0.0;
+    return r < 1.0 ? r : 1.0;
 }
 
 // ---- partitions (core/partition.cpp) --------------------------------------------------------
@@ -558,7 +565,8 @@ template <class R> struct ChainRegs {
     int k;
     unsigned sm;
     V3<R> f;
-    R pi, ru, rv, eyeden;
+    R pi, ru, rv;
+    double eyeden;
     double acc, iacc, lum;
     unsigned long long npert, nlarge, ipert, nsteps;
 };
@@ -600,7 +608,7 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
     int head_end = 0;
     int kp = cs.k;
     unsigned smp = cs.sm;
-    R tf = R(0), tr = R(0);
+    double tf = 0.0, tr = 0.0;
     const int pk = P.pk;
 
     // suitability (core/mutations.cpp:47-56)
@@ -618,7 +626,7 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
     const R s_pert = elig ? R(0.5) : R(0);
     const bool choose = elig && Unit<R>::draw(rng) < s_pert;
 
-    R a = R(0);
+    double a = 0.0;
     Contrib<R> pc;
     pc.pi = R(0);
     int region = -1;
@@ -665,8 +673,8 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
         }
         if (g.lane == 0 && P.ctl == 2)
             atomicAdd(&P.part.visits[region], 1ull);
-        cs.acc += static_cast<double>(a);
-        cs.iacc += static_cast<double>(a);
+        cs.acc += a;
+        cs.iacc += a;
         ++cs.npert;
         ++cs.ipert;
     } else {
@@ -689,17 +697,18 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
 
     // splat (core/driver.cpp:59-64) -- the group leader writes
     if (g.lane == 0) {
-        if (a < R(1) && cs.pi > R(0))
-            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - a) / cs.pi), cs.lum);
-        if (pc.pi > R(0) && a > R(0))
-            film_add(P, pc.u, pc.v, scl(pc.f, a / pc.pi), cs.lum);
+        const R ar = static_cast<R>(a);
+        if (a < 1.0 && cs.pi > R(0))
+            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - ar) / cs.pi), cs.lum);
+        if (pc.pi > R(0) && a > 0.0)
+            film_add(P, pc.u, pc.v, scl(pc.f, ar / pc.pi), cs.lum);
     } else {
         // keep the lum accumulator identical on all lanes (leader's value is stored)
     }
 
     // accept / commit (core/driver.cpp:168-171)
     bool accepted = false;
-    if (a > R(0) && Unit<R>::draw(rng) < a) {
+    if (a > 0.0 && static_cast<double>(Unit<R>::draw(rng)) < a) {
         accepted = true;
         if (g.lane == 0)
             for (int i = 1; i <= head_end; ++i)
@@ -710,18 +719,18 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
         cs.pi = pc.pi;
         cs.ru = pc.u;
         cs.rv = pc.v;
-        cs.eyeden = M<R>::inf() - M<R>::inf();   // NaN
+        cs.eyeden = __longlong_as_double(0x7ff8000000000000LL);   // NaN
     }
 
     if (g.lane == 0) {
         if (cs.nsteps < P.ch.log_K) {
             size_t o = static_cast<size_t>(cs.nsteps) * P.C + c;
-            P.ch.log_a[o] = static_cast<double>(a);
+            P.ch.log_a[o] = a;
             P.ch.log_f[o] = static_cast<unsigned char>((accepted ? 1 : 0) | (choose ? 2 : 0) | 4);
         }
         if (P.record_visits) {
             P.ch.vreg[c] = (choose && P.ctl != 0) ? region : -1;
-            P.ch.va[c] = static_cast<double>(a);
+            P.ch.va[c] = a;
         }
     }
     ++cs.nsteps;
@@ -815,7 +824,7 @@ __device__ void init_chain(const StepParams<R> &P, const SceneView<R> &S, int c,
     for (unsigned long long t = 0; t < max_attempts; ++t) {
         int k;
         unsigned sm;
-        R tf;
+        double tf;
         if (!trace_eye(S, init, P.maxv, pv, k, sm, tf, g, rc))
             continue;
         CurPath<R> dummy{P.ch.verts, P.C, c, &S.cam};
@@ -838,7 +847,7 @@ __device__ void init_chain(const StepParams<R> &P, const SceneView<R> &S, int c,
     }
     if (!ok)
         atomicExch(P.ch.err, 1);
-    P.ch.eyeden[c] = M<R>::inf() - M<R>::inf();
+    P.ch.eyeden[c] = __longlong_as_double(0x7ff8000000000000LL);
     P.ch.acc[c] = 0.0;
     P.ch.iacc[c] = 0.0;
     P.ch.lum[c] = 0.0;
@@ -886,15 +895,15 @@ __global__ void __launch_bounds__(128) k_bsub(StepParams<R> P, unsigned long lon
     for (unsigned long long j = s; j < n_samples; j += S_total) {
         int k;
         unsigned sm;
-        R tf;
+        double tf;
         double v = 0.0;
         if (trace_eye(S, rng, P.maxv, pv, k, sm, tf, g, rc)) {
             CurPath<R> dummy{P.ch.verts, P.C, 0, &S.cam};
             PropPath<R> path{pv, k - 1, &dummy};
             Contrib<R> con = evaluate(S, path, k, g, rc);
             if (con.pi > R(0)) {
-                if (tf > R(0))
-                    v = static_cast<double>(con.pi / tf);
+                if (tf > 0.0)
+                    v = static_cast<double>(con.pi) / tf;
             }
         }
         sum += v;

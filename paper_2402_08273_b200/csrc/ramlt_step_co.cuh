@@ -153,14 +153,16 @@ template <class R, int RK> struct StepCo {
     R res_t;
     // ---- per-step state ----
     bool choose, ok, accepted;
-    R s_pert, tf, tr, a, dpdf;
+    R s_pert, dpdf;
+    double tf, tr, a;   // transition densities and acceptance: fp64 in every build
     int endpoint, first, idx, next, i, region, kp, head_end;
     unsigned pmask, m, smp;
     V3<R> o, d;
     Contrib<R> pcb;
     // evaluate / eye density sub-state
     V3<R> ef;
-    R ep, eseg;
+    double ep;
+    R eseg;
     int ek, ei;
 
     __device__ __forceinline__ int advance(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
@@ -188,7 +190,7 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
             s_pert = elig ? R(0.5) : R(0);
             choose = elig && Unit<R>::draw(rng) < s_pert;
         }
-        a = R(0);
+        a = 0.0;
         pcb.pi = R(0);
         region = -1;
         ok = false;
@@ -284,7 +286,7 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
             pv.set(0, cv);
             kp = 1;
             smp = 0;
-            tf = R(1);
+            tf = 1.0;
             ok = false;
             if (P.maxv < 2)
                 goto finish;
@@ -310,7 +312,7 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                 x.emi = h.emi;
                 x.spec = h.emi < 0 && (mt.kind == MAT_MIRROR || mt.kind == MAT_DIELECTRIC);
                 x.ev = EV_NONE;
-                tf *= dpdf * (M<R>::abs(dot(h.n, d)) / (h.t * h.t));
+                tf *= static_cast<double>(dpdf * (M<R>::abs(dot(h.n, d)) / (h.t * h.t)));
                 if (x.spec)
                     smp |= 1u << kp;
                 if (h.emi >= 0) {
@@ -388,9 +390,9 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                     goto eval_fail;
                 o = av.p;
                 d = dvs(dd, dist);
-                ep = dist - R(kEpsD);
+                ray.lim = dist - R(kEpsD);
             }
-            CO_RAY(o, d, ep, 3);
+            CO_RAY(o, d, ray.lim, 3);
             if (res_prim >= 0)
                 goto eval_fail;
         eval_seg_visible:
@@ -452,14 +454,14 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
         if (cs.eyeden == cs.eyeden)   // cached eye_path_density(current)
             goto large_accept;
         // eye_path_density (path.cpp:144-170) of the current path
-        ep = R(0);
+        ep = 0.0;
         {
             if (cs.k < 2 || cur.get(cs.k - 1).emi < 0)
                 goto ed_done;
             R p0 = cam_dir_pdf(S.cam, pdir<R>(cur, 0));
             if (p0 <= R(0))
                 goto ed_done;
-            ep = p0;
+            ep = static_cast<double>(p0);
         }
         for (ei = 0; ei + 1 < cs.k; ++ei) {
             {
@@ -467,7 +469,7 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                 Vx<R> bv = cur.get(ei + 1);
                 if (ei > 0) {
                     if (av.emi >= 0) {
-                        ep = R(0);
+                        ep = 0.0;
                         goto ed_done;
                     }
                     Vx<R> pr = cur.get(ei - 1);
@@ -476,7 +478,7 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                     V3<R> wo = unit(sub(bv.p, av.p));
                     eseg = av.spec ? spec_prob(mt, wi, av.n, av.ev) : bsdf_pdf(mt, wi, wo, av.n);
                     if (eseg <= R(0)) {
-                        ep = R(0);
+                        ep = 0.0;
                         goto ed_done;
                     }
                 }
@@ -511,11 +513,11 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
                 ef.x = R(0);
         ed_apply:
             if (ei == 0)
-                ep *= ef.x;                 // p *= area_conversion(path[0], path[1])
+                ep *= static_cast<double>(ef.x);          // p *= area_conversion(path[0], path[1])
             else
-                ep *= eseg * ef.x;          // p *= q * area_conversion(...)
-            if (ep <= R(0)) {
-                ep = R(0);
+                ep *= static_cast<double>(eseg * ef.x);   // p *= q * area_conversion(...)
+            if (ep <= 0.0) {
+                ep = 0.0;
                 goto ed_done;
             }
         }
@@ -533,20 +535,20 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
     pert_record:
         if (P.ctl == 2)
             atomicAdd(&P.part.visits[region], 1ull);
-        cs.acc += static_cast<double>(a);
-        cs.iacc += static_cast<double>(a);
+        cs.acc += a;
+        cs.iacc += a;
         ++cs.npert;
         ++cs.ipert;
 
     finish:
         // splat (driver.cpp:59-64)
-        if (a < R(1) && cs.pi > R(0))
-            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - a) / cs.pi), cs.lum);
-        if (pcb.pi > R(0) && a > R(0))
-            film_add(P, pcb.u, pcb.v, scl(pcb.f, a / pcb.pi), cs.lum);
+        if (a < 1.0 && cs.pi > R(0))
+            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - static_cast<R>(a)) / cs.pi), cs.lum);
+        if (pcb.pi > R(0) && a > 0.0)
+            film_add(P, pcb.u, pcb.v, scl(pcb.f, static_cast<R>(a) / pcb.pi), cs.lum);
         // accept / commit (driver.cpp:168-171)
         accepted = false;
-        if (a > R(0) && Unit<R>::draw(rng) < a) {
+        if (a > 0.0 && static_cast<double>(Unit<R>::draw(rng)) < a) {
             accepted = true;
             for (int q = 1; q <= head_end; ++q)
                 store_gv(&P.ch.verts[static_cast<size_t>(q - 1) * P.C + c], pv.get(q));
@@ -556,16 +558,16 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
             cs.pi = pcb.pi;
             cs.ru = pcb.u;
             cs.rv = pcb.v;
-            cs.eyeden = M<R>::inf() - M<R>::inf();
+            cs.eyeden = __longlong_as_double(0x7ff8000000000000LL);
         }
         if (cs.nsteps < P.ch.log_K) {
             size_t ofs = static_cast<size_t>(cs.nsteps) * P.C + c;
-            P.ch.log_a[ofs] = static_cast<double>(a);
+            P.ch.log_a[ofs] = a;
             P.ch.log_f[ofs] = static_cast<unsigned char>((accepted ? 1 : 0) | (choose ? 2 : 0) | 4);
         }
         if (P.record_visits) {
             P.ch.vreg[c] = (choose && P.ctl != 0) ? region : -1;
-            P.ch.va[c] = static_cast<double>(a);
+            P.ch.va[c] = a;
         }
         ++cs.nsteps;
         (void)index;
