@@ -146,6 +146,7 @@ private:
     DBuf<rd::MatD<R>> mat_;
     DBuf<rd::V3<R>> emit_;
     DBuf<rd::BvhNodeD<R>> bvh_;
+    DBuf<rd::TriT<R>> trt_;
     bool use_bvh_ = false;
     int bvh_depth_ = 0;
     // chains
@@ -292,7 +293,10 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
             std::memcpy(&coords[9 * i + 3], hs_.tri[i].b, 3 * sizeof(double));
             std::memcpy(&coords[9 * i + 6], hs_.tri[i].c, 3 * sizeof(double));
         }
-        BvhBuild bb = build_bvh(coords.data(), hs_.tri.size(), 4);
+        int leaf_max = 4;
+        if (const char *v = std::getenv("RAMLT_BVH_LEAF"))
+            leaf_max = std::max(1, std::min(15, std::atoi(v)));
+        BvhBuild bb = build_bvh(coords.data(), hs_.tri.size(), leaf_max);
         bvh_depth_ = bb.depth;
         if (bb.depth > 62)
             throw std::runtime_error("BVH deeper than the traversal stack");
@@ -300,6 +304,16 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         for (size_t i = 0; i < tris.size(); ++i)
             ordered[i] = tris[static_cast<size_t>(bb.order[i])];
         tris.swap(ordered);
+        std::vector<rd::TriT<R>> trt(tris.size());
+        for (size_t i = 0; i < tris.size(); ++i) {
+            const rd::TriD<R> &t = tris[i];
+            trt[i].a[0] = t.a.x, trt[i].a[1] = t.a.y, trt[i].a[2] = t.a.z;
+            trt[i].e1[0] = t.e1.x, trt[i].e1[1] = t.e1.y, trt[i].e1[2] = t.e1.z;
+            trt[i].e2[0] = t.e2.x, trt[i].e2[1] = t.e2.y, trt[i].e2[2] = t.e2.z;
+            trt[i].orig = t.orig;
+        }
+        trt_.alloc(trt.size());
+        RAMLT_CUDA(cudaMemcpy(trt_.p, trt.data(), trt.size() * sizeof(trt[0]), cudaMemcpyHostToDevice));
         auto down = [](double x) {
             R r = static_cast<R>(x);
             if (static_cast<double>(r) > x)
@@ -568,6 +582,7 @@ template <class R> rd::StepParams<R> EngineT<R>::params() const {
     P.scene.cam.area = static_cast<R>(cb_.area);
     P.scene.cam.sensor = static_cast<R>(cb_.sensor);
     P.scene.bvh = use_bvh_ ? bvh_.p : nullptr;
+    P.scene.trt = use_bvh_ ? trt_.p : nullptr;
     P.C = C_;
     P.C_total = Ctot_;
     P.chain_off = off_;

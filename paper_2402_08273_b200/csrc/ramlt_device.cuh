@@ -40,6 +40,7 @@ template <> struct M<double> {
     static __device__ __forceinline__ bool finite(double x) { return ::isfinite(x); }
     static __device__ __forceinline__ bool isnan(double x) { return ::isnan(x); }
     static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+    static __device__ __forceinline__ double fma(double a, double b, double c) { return ::fma(a, b, c); }
     static __device__ __forceinline__ double inf() { return __longlong_as_double(0x7ff0000000000000LL); }
 };
 template <> struct M<float> {
@@ -57,6 +58,7 @@ template <> struct M<float> {
     static __device__ __forceinline__ bool finite(float x) { return ::isfinite(x); }
     static __device__ __forceinline__ bool isnan(float x) { return ::isnan(x); }
     static __device__ __forceinline__ float rcp(float x) { return 1.0f / x; }
+    static __device__ __forceinline__ float fma(float a, float b, float c) { return ::fmaf(a, b, c); }
     static __device__ __forceinline__ float inf() { return __int_as_float(0x7f800000); }
 };
 
@@ -186,6 +188,13 @@ template <class R> struct TriD {   // a, e1 = b - a, e2 = c - a, n = normalize(c
     int pad_;
 };
 
+// Leaf-test record of a BVH-ordered triangle: only what Moeller-Trumbore reads
+// (48 B in fp32); the hit record (normal, material, emitter) comes from TriD.
+template <class R> struct alignas(16) TriT {
+    R a[3], e1[3], e2[3];
+    int orig;
+};
+
 // BVH2 node: both children's boxes (padded outward at build time); child >= 0
 // internal node, < 0 leaf ~((first << 4) | count) into the reordered triangles.
 template <class R> struct alignas(16) BvhNodeD {
@@ -215,6 +224,7 @@ template <class R> struct SceneView {
     int ntri, nsph;
     CamD<R> cam;
     const BvhNodeD<R> *bvh;   // null: brute force over (smem-staged) triangles
+    const TriT<R> *trt;       // BVH-ordered leaf-test records (with bvh)
 };
 
 template <class R> struct Hit {
@@ -288,6 +298,33 @@ __device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &
     return false;
 }
 
+// Moeller-Trumbore on the compact record: identical arithmetic to hit_tri.
+template <class R>
+__device__ __forceinline__ bool hit_tri_t(const TriT<R> &tr, V3<R> o, V3<R> d, R &t) {
+    const V3<R> a = mk(tr.a[0], tr.a[1], tr.a[2]);
+    const V3<R> e1 = mk(tr.e1[0], tr.e1[1], tr.e1[2]);
+    const V3<R> e2 = mk(tr.e2[0], tr.e2[1], tr.e2[2]);
+    V3<R> p = cross(d, e2);
+    R det = dot(e1, p);
+    if (M<R>::abs(det) < R(1e-14))
+        return false;
+    R inv = R(1) / det;
+    V3<R> tv = sub(o, a);
+    R u = dot(tv, p) * inv;
+    if (u < R(0) || u > R(1))
+        return false;
+    V3<R> q = cross(tv, e1);
+    R v = dot(d, q) * inv;
+    if (v < R(0) || u + v > R(1))
+        return false;
+    R tt = dot(e2, q) * inv;
+    if (tt > R(kEpsD)) {
+        t = tt;
+        return true;
+    }
+    return false;
+}
+
 // ---- BVH traversal ------------------------------------------------------------------
 // The result equals the reference's linear scan (core/scene.cpp:57-92): the
 // winner is the lexicographic minimum of (t, original primitive index) over all
@@ -301,11 +338,13 @@ template <> struct Slack<double> {
     static __device__ __forceinline__ double v() { return 1.0 + 1e-13; }
 };
 
+// Slab test as fma(lo, inv, -o*inv): one FFMA per plane; the outward padding
+// and the relative slack absorb the different rounding.
 template <class R>
-__device__ __forceinline__ bool slab(const R lo[3], const R hi[3], V3<R> o, V3<R> inv, R tcap, R &tnear) {
-    R tx0 = (lo[0] - o.x) * inv.x, tx1 = (hi[0] - o.x) * inv.x;
-    R ty0 = (lo[1] - o.y) * inv.y, ty1 = (hi[1] - o.y) * inv.y;
-    R tz0 = (lo[2] - o.z) * inv.z, tz1 = (hi[2] - o.z) * inv.z;
+__device__ __forceinline__ bool slab(const R lo[3], const R hi[3], V3<R> oinv, V3<R> inv, R tcap, R &tnear) {
+    R tx0 = M<R>::fma(lo[0], inv.x, -oinv.x), tx1 = M<R>::fma(hi[0], inv.x, -oinv.x);
+    R ty0 = M<R>::fma(lo[1], inv.y, -oinv.y), ty1 = M<R>::fma(hi[1], inv.y, -oinv.y);
+    R tz0 = M<R>::fma(lo[2], inv.z, -oinv.z), tz1 = M<R>::fma(hi[2], inv.z, -oinv.z);
     R tmin = fmax(fmax(fmin(tx0, tx1), fmin(ty0, ty1)), fmin(tz0, tz1));
     R tmax = fmin(fmin(fmax(tx0, tx1), fmax(ty0, ty1)), fmax(tz0, tz1));
     tmax = tmax * Slack<R>::v();
@@ -335,6 +374,7 @@ template <class R>
 __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best, int &key, bool any_hit) {
     constexpr int DONE = 0x7fffffff;
     V3<R> inv = safe_inv(d);
+    V3<R> oinv = mul(o, inv);
     (void)lim;
     int pos = -1;
     int stack[64];
@@ -345,8 +385,8 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
         while (node >= 0 && node != DONE) {
             const BvhNodeD<R> &n = s.bvh[node];
             R t0, t1;
-            bool h0 = slab(n.lo0, n.hi0, o, inv, best, t0);
-            bool h1 = slab(n.lo1, n.hi1, o, inv, best, t1);
+            bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
+            bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
             if (h0 && h1) {
                 bool near0 = t0 <= t1;
                 stack[sp++] = near0 ? n.c1 : n.c0;
@@ -371,9 +411,9 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
             int code = ~leaf;
             int first = code >> 4, cnt = code & 15;
             for (int k = first; k < first + cnt; ++k) {
-                const TriD<R> &tr = s.tri[k];
+                const TriT<R> &tr = s.trt[k];
                 R t;
-                if (!hit_tri(tr, o, d, t))
+                if (!hit_tri_t(tr, o, d, t))
                     continue;
                 int kk = s.nsph + tr.orig;
                 if (t < best || (t == best && kk < key)) {
