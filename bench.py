@@ -350,7 +350,7 @@ def main():
     from paper_2402_08273_b200 import parse_scene
     n_mat, n_sph, n_tri, n_emi = parse_scene(wl["scene_text"]).counts
     flop_per_mut = r_m * (45.0 * n_tri + 20.0 * n_sph)
-    # dominant kernel: the chain-step megakernel; algorithmic FLOPs per launch
+    # dominant kernel: the chain-step kernel; algorithmic work per launch
     # = mutations per launch (all chains of this rank) x W, / its mean event time
     per_launch_muts = res["mutations_per_rank"] / max(res["step_launches"], 1)
     mean_launch_s = (res["step_ms"] / max(res["step_launches"], 1)) / 1e3
@@ -388,7 +388,9 @@ def main():
                     "work_per_unit": f"R_m x B_ray + B_state = {r_m:.3f} x {b_ray:.0f} B + {b_state:.0f} B "
                                      f"= {bytes_per_mut:.0f} B/mutation (B_ray: {levels} BVH levels x 64 B + "
                                      f"4 x 48 B; R_m oracle-counted on a 4096-triangle sample of the scene)"}
-    roofline.update({"kernel": "k_step (chain-step megakernel)",
+    kname = ("k_step_co (coroutine chain-step kernel, BVH traversal with dynamic ray fetch)"
+             if wl["scene"] == "clusters" else "k_step (chain-step megakernel)")
+    roofline.update({"kernel": kname,
                      "kernel_share": res["step_ms"] / res["ms"] if res["ms"] else None})
     cpu = None
     if not args.no_cpu_baseline and res["world"] == 1:

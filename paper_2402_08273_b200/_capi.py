@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "_lib", "libramlt_gpu.so")
+LIB_PATH = os.environ.get("RAMLT_GPU_LIB") or os.path.join(PKG_DIR, "_lib", "libramlt_gpu.so")
 
 
 class ramlt_material(C.Structure):

@@ -151,6 +151,8 @@ private:
     int bvh_depth_ = 0;
     // chains
     DBuf<rd::GV<R>> verts_;
+    DBuf<rd::GV<R>> pv_scratch_;   // k_step_co proposal vertices in global memory (L1/L2-cached)
+    bool co_pv_global_ = true;     // RAMLT_CO_PV=smem: in shared memory (caps occupancy)
     DBuf<int> klen_;
     DBuf<unsigned> smask_;
     DBuf<R> cf_, cr_;
@@ -165,8 +167,9 @@ private:
     DBuf<int> err_;
     DBuf<unsigned long long> rays_;
     DBuf<unsigned> work_;     // work-stealing counter of k_step_co
-    bool use_co_ = false;     // G == 1: RAMLT_STEP_KERNEL=co selects the coroutine kernel
+    bool use_co_ = false;     // G == 1: the coroutine kernel (default with a BVH)
     int steal_ = 1;           // RAMLT_STEP_KERNEL=co_static: one chain per lane, no stealing
+    int refill_ = 8;          // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round
     // film
     DBuf<double> film64_;
     DBuf<float4> film32_;
@@ -406,10 +409,17 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     rays_.alloc(2);
     rays_.zero(stream_);
     work_.alloc(1);
+    // BVH scenes step with the coroutine kernel (dynamic ray fetch), brute-force
+    // scenes with the lane-group megakernel; RAMLT_STEP_KERNEL=mega|co|co_static overrides.
+    use_co_ = use_bvh_;
     if (const char *v = std::getenv("RAMLT_STEP_KERNEL")) {
         use_co_ = std::string(v) == "co" || std::string(v) == "co_static";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
     }
+    if (const char *v = std::getenv("RAMLT_CO_PV"))
+        co_pv_global_ = std::string(v) != "smem";
+    if (const char *v = std::getenv("RAMLT_CO_REFILL"))
+        refill_ = std::min(32, std::max(1, std::atoi(v)));
     size_t npix = static_cast<size_t>(d.width) * d.height;
     film64_.alloc(npix * 3);
     film64_.zero(stream_);
@@ -764,6 +774,7 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     P.record_visits = record ? 1 : 0;
     if (G_ == 1 && use_co_) {
         P.steal = steal_;
+        P.refill = refill_;
         launch_step_co(P);
         return;
     }
@@ -804,12 +815,13 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     }
 }
 
-template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P) {
+template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
+    rd::StepParams<R> P = P0;
     auto kern = d_.rng == RAMLT_RNG_PHILOX
                     ? (use_bvh_ ? rd::k_step_co<R, rd::RNG_PHILOX, true> : rd::k_step_co<R, rd::RNG_PHILOX, false>)
                     : (use_bvh_ ? rd::k_step_co<R, rd::RNG_PCG, true> : rd::k_step_co<R, rd::RNG_PCG, false>);
     size_t scene = (smem_ + 15) & ~size_t(15);
-    size_t smem = scene + static_cast<size_t>(128) * d_.max_vertices * sizeof(rd::GV<R>);
+    size_t smem = scene + (co_pv_global_ ? 0 : static_cast<size_t>(128) * d_.max_vertices * sizeof(rd::GV<R>));
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
@@ -818,6 +830,13 @@ template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P) {
     RAMLT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     unsigned want = static_cast<unsigned>((C_ + 127) / 128);
     unsigned blocks = P.steal ? std::min<unsigned>(want, static_cast<unsigned>(std::max(per_sm, 1) * sms)) : want;
+    P.pv_scratch = nullptr;
+    if (co_pv_global_) {
+        size_t need = static_cast<size_t>(blocks) * 128 * d_.max_vertices;
+        if (pv_scratch_.n < need)
+            pv_scratch_.alloc(need);
+        P.pv_scratch = pv_scratch_.p;
+    }
     RAMLT_CUDA(cudaMemsetAsync(work_.p, 0, sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d_.profile_kernels) {

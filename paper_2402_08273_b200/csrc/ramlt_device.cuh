@@ -360,6 +360,112 @@ template <class R> __device__ __forceinline__ V3<R> safe_inv(V3<R> d) {
     return mk(R(1) / x, R(1) / y, R(1) / z);
 }
 
+// BVH2 traversal state of one ray for the coroutine kernel (bvh_trace below is
+// the run-to-completion form used by the megakernel); same visit order, so
+// the same hits.
+//
+// `step` runs one "while-while" round (Aila & Laine 2009): descend internal
+// nodes until every still-traversing lane of the warp holds a leaf (one leaf
+// postponed per lane), then test the leaves with the lanes converged.  It
+// returns true when the ray is done.  The coroutine kernel interleaves rounds
+// with handing finished lanes a new ray (dynamic ray fetch) instead of idling
+// them until the warp's longest traversal ends.
+template <class R> struct BvhTrav {
+    static constexpr int DONE = 0x7fffffff;
+    static constexpr int STACK = 64;   // BVH2 depth <= 62 (checked at build)
+    V3<R> o, d, inv, oinv;
+    R best;
+    int key, pos, spos, node, leaf, sp;
+    bool any;
+    int *stc;   // the lane's stack (kept outside so the scalars stay in registers)
+
+    // Spheres first (linear scan, strict '<'), then the BVH below `best`.
+    __device__ __forceinline__ void begin(const SceneView<R> &s, V3<R> o_, V3<R> d_, R lim, bool any_hit) {
+        o = o_;
+        d = d_;
+        any = any_hit;
+        best = lim;
+        key = 0x7fffffff;
+        spos = -1;
+        pos = -1;
+        for (int i = 0; i < s.nsph; ++i) {
+            R t;
+            if (hit_sphere(s.sph[i], o, d, t) && t < best) {
+                best = t;
+                key = i;
+                spos = i;
+            }
+        }
+        inv = safe_inv(d);
+        oinv = mul(o, inv);
+        sp = 0;
+        leaf = 0;
+        node = (any && spos >= 0) ? DONE : 0;
+    }
+
+    __device__ __forceinline__ int pop() { return sp > 0 ? stc[--sp] : DONE; }
+
+    __device__ __forceinline__ bool step(const SceneView<R> &s) {
+        while (node >= 0 && node != DONE) {
+            const BvhNodeD<R> &n = s.bvh[node];
+            R t0, t1;
+            bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
+            bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
+            if (h0 && h1) {
+                bool near0 = t0 <= t1;
+                stc[sp++] = near0 ? n.c1 : n.c0;
+                node = near0 ? n.c0 : n.c1;
+            } else if (h0) {
+                node = n.c0;
+            } else if (h1) {
+                node = n.c1;
+            } else {
+                node = pop();
+            }
+            if (node < 0) {   // reached a leaf
+                if (leaf != 0)
+                    break;    // slot busy: test the postponed leaf first
+                leaf = node;
+                node = pop();
+            }
+            if (__all_sync(__activemask(), leaf != 0))
+                break;
+        }
+        while (leaf < 0) {
+            int code = ~leaf;
+            int first = code >> 4, cnt = code & 15;
+            for (int k = first; k < first + cnt; ++k) {
+                const TriT<R> &tr = s.trt[k];
+                R t;
+                if (!hit_tri_t(tr, o, d, t))
+                    continue;
+                int kk = s.nsph + tr.orig;
+                if (t < best || (t == best && kk < key)) {
+                    best = t;
+                    key = kk;
+                    pos = k;
+                    if (any) {
+                        node = DONE;
+                        leaf = 0;
+                        return true;
+                    }
+                }
+            }
+            leaf = 0;
+            if (node < 0) {   // the next popped entry was a leaf too
+                leaf = node;
+                node = pop();
+            }
+        }
+        return node == DONE;
+    }
+
+    // Hit primitive index (spheres first, triangles by BVH position) or -1.
+    __device__ __forceinline__ int prim(const SceneView<R> &s) const {
+        return pos >= 0 ? s.nsph + pos : spos;
+    }
+};
+
 // Returns the winner's position in s.tri (BVH order) or -1; `key` carries the
 // combined original index (spheres first) used for ties.  With any_hit, stops
 // at the first primitive below lim (visibility).

@@ -106,6 +106,8 @@ template <class R> struct StepParams {
     int j0, j1;
     int record_visits;   // write vreg/va (adaptive)
     int steal;           // k_step_co: 1 = warp-aggregated work stealing, 0 = one chain per lane
+    int refill;          // k_step_co (BVH): idle lanes that end a traversal round
+    GV<R> *pv_scratch;   // k_step_co: proposal vertices in global memory (nullptr: smem)
     int ktab_l2;         // region kernel tables change inside this launch (cooperative): read via L2
     int pooled;          // fuse pooled accumulation into the step
     RegionArrays reg;
@@ -738,8 +740,19 @@ __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, lon
     (void)index;
 }
 
+#ifndef RAMLT_BVH_MINBLOCKS
+#define RAMLT_BVH_MINBLOCKS 10
+#endif
+#ifndef RAMLT_LANES_MINBLOCKS
+#define RAMLT_LANES_MINBLOCKS 4
+#endif
+// fp32 k_step trades registers for resident warps.  The BVH instantiation
+// (G == 0) is memory-latency bound -- c4 (fixed) at 1/5/6/7/8/10/12/16 blocks
+// per SM: 35.4/39.1/42.6/45.2/46.8/48.3/48.0/37.5 M mut/s; the lane-group
+// instantiations gain ~5% at 4 blocks (128 registers) on c5.
 template <class R, int RK, int G>
-__global__ void __launch_bounds__(128) k_step(StepParams<R> P) {
+__global__ void __launch_bounds__(128, sizeof(R) == 8 ? 1 : G == 0 ? RAMLT_BVH_MINBLOCKS : RAMLT_LANES_MINBLOCKS)
+k_step(StepParams<R> P) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     Group<G> g;
@@ -864,7 +877,8 @@ __device__ void init_chain(const StepParams<R> &P, const SceneView<R> &S, int c,
 // chain is geometric, so a lane that finishes takes the next chain instead of
 // idling until the warp's unluckiest chain is done.  `work` is zeroed.
 template <class R, int RK, int G>
-__global__ void __launch_bounds__(128) k_init(StepParams<R> P, unsigned long long max_attempts, unsigned int *work) {
+__global__ void __launch_bounds__(128, sizeof(R) == 4 && G == 0 ? RAMLT_BVH_MINBLOCKS : 1)
+k_init(StepParams<R> P, unsigned long long max_attempts, unsigned int *work) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     RayCount rc;

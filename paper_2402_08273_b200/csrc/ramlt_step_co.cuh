@@ -629,20 +629,33 @@ __device__ __forceinline__ void co_store(const StepCo<R, RK> &co, const StepPara
     RngIO<RK>::store(co.rng, P.ch.rng0, P.ch.rng1, c);
 }
 
+// fp32 BVH: 64 registers for 8 resident blocks -- c4 at 4/8/10/12 blocks per
+// SM: 46.8/54.9/54.4/46.4 M mut/s (Fixed strategy).
+#ifndef RAMLT_CO_MINBLOCKS
+#define RAMLT_CO_MINBLOCKS 8
+#endif
 // Persistent, work-stealing chain-step kernel.  `work` is a zeroed counter.
 template <class R, int RK, bool BVH>
-__global__ void __launch_bounds__(128) k_step_co(StepParams<R> P, unsigned int *work) {
+__global__ void __launch_bounds__(128, BVH && sizeof(R) == 4 ? RAMLT_CO_MINBLOCKS : 1)
+k_step_co(StepParams<R> P, unsigned int *work) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     size_t scene_bytes = stage_bytes_sph<R>(P.scene.nsph) +
                          (P.scene.bvh ? 0 : static_cast<size_t>(P.scene.ntri) * sizeof(TriD<R>));
     scene_bytes = (scene_bytes + 15) & ~size_t(15);
-    PvSmem<R> pv{reinterpret_cast<GV<R> *>(smem + scene_bytes) + threadIdx.x, static_cast<int>(blockDim.x)};
+    PvSmem<R> pv = P.pv_scratch
+                       ? PvSmem<R>{P.pv_scratch + blockIdx.x * blockDim.x + threadIdx.x,
+                                   static_cast<int>(gridDim.x * blockDim.x)}
+                       : PvSmem<R>{reinterpret_cast<GV<R> *>(smem + scene_bytes) + threadIdx.x,
+                                   static_cast<int>(blockDim.x)};
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
 
     StepCo<R, RK> co;
     RayCount rc;
+    BvhTrav<R> tv;   // BVH: resumable traversal of this lane's pending ray
+    int tv_stc[BvhTrav<R>::STACK];
+    tv.stc = tv_stc;
     bool have = false, exhausted = false, want = false;
     int j = 0, jend = 0;
     bool first_grab = true;
@@ -687,6 +700,8 @@ __global__ void __launch_bounds__(128) k_step_co(StepParams<R> P, unsigned int *
             int st = co.advance(P, S, pv, rc, index);
             if (st == CO_RAY_PENDING) {
                 want = true;
+                if constexpr (BVH)
+                    tv.begin(S, co.ray.o, co.ray.d, co.ray.lim, co.ray.lim < M<R>::inf());
             } else if (++j >= jend) {
                 co_store(co, P);
                 have = false;
@@ -696,7 +711,21 @@ __global__ void __launch_bounds__(128) k_step_co(StepParams<R> P, unsigned int *
         __syncwarp();
         if (!__any_sync(0xffffffffu, want || !exhausted))
             break;
-        if (want) {
+        if constexpr (BVH) {
+            // while-while rounds until the warp is done or enough lanes can
+            // take a new ray (their chains' next ray, or a new chain)
+            for (;;) {
+                unsigned busy = __ballot_sync(0xffffffffu, want);
+                unsigned idle = __ballot_sync(0xffffffffu, !want && (have || !exhausted));
+                if (!busy || __popc(idle) >= P.refill)
+                    break;
+                if (want && tv.step(S)) {
+                    co.res_prim = tv.prim(S);
+                    co.res_t = tv.best;
+                    want = false;
+                }
+            }
+        } else if (want) {
             R t;
             co.res_prim = trace_ray<R, BVH>(S, co.ray, t);
             co.res_t = t;
