@@ -112,7 +112,7 @@ private:
     void launch_step(int j0, int j1, unsigned long long span_start, unsigned long long per,
                      unsigned long long rem, bool record);
     void adapt_after_step(int j, unsigned long long span_start);
-    void launch_step_co(const rd::StepParams<R> &P);
+    template <bool INIT = false> void launch_step_co(const rd::StepParams<R> &P);
     bool launch_coop(int j0, int j1, unsigned long long span_start, unsigned long long per,
                      unsigned long long rem);
     int coop_state_ = -1;   // -1 unknown, 0 unavailable, 1 usable
@@ -168,6 +168,7 @@ private:
     DBuf<unsigned long long> rays_;
     DBuf<unsigned> work_;     // work-stealing counter of k_step_co
     bool use_co_ = false;     // G == 1: the coroutine kernel (default with a BVH)
+    bool use_co_init_ = false;  // chain initialisation with the coroutine kernel (default with a BVH)
     int steal_ = 1;           // RAMLT_STEP_KERNEL=co_static: one chain per lane, no stealing
     int refill_ = 8;          // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round
     // film
@@ -412,6 +413,9 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     // BVH scenes step with the coroutine kernel (dynamic ray fetch), brute-force
     // scenes with the lane-group megakernel; RAMLT_STEP_KERNEL=mega|co|co_static overrides.
     use_co_ = use_bvh_;
+    use_co_init_ = use_bvh_;
+    if (const char *v = std::getenv("RAMLT_INIT_KERNEL"))
+        use_co_init_ = std::string(v) == "co";
     if (const char *v = std::getenv("RAMLT_STEP_KERNEL")) {
         use_co_ = std::string(v) == "co" || std::string(v) == "co_static";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
@@ -744,6 +748,15 @@ template <class R> void EngineT<R>::estimate_b(double *b, double *se) {
 
 template <class R> void EngineT<R>::init_chains() {
     rd::StepParams<R> P = params();
+    if (use_co_init_) {   // BVH scenes: the coroutine kernel with dynamic ray fetch
+        P.steal = 1;
+        P.refill = refill_;
+        P.init_attempts = 50000000ull;
+        launch_step_co<true>(P);
+        check_err("init");
+        chains_ready_ = true;
+        return;
+    }
     auto kern = d_.rng == RAMLT_RNG_PHILOX
                     ? (use_bvh_ ? rd::k_init<R, rd::RNG_PHILOX, 0> : rd::k_init<R, rd::RNG_PHILOX, 1>)
                     : (use_bvh_ ? rd::k_init<R, rd::RNG_PCG, 0> : rd::k_init<R, rd::RNG_PCG, 1>);
@@ -815,11 +828,14 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     }
 }
 
-template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
+template <class R>
+template <bool INIT>
+void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
     rd::StepParams<R> P = P0;
     auto kern = d_.rng == RAMLT_RNG_PHILOX
-                    ? (use_bvh_ ? rd::k_step_co<R, rd::RNG_PHILOX, true> : rd::k_step_co<R, rd::RNG_PHILOX, false>)
-                    : (use_bvh_ ? rd::k_step_co<R, rd::RNG_PCG, true> : rd::k_step_co<R, rd::RNG_PCG, false>);
+                    ? (use_bvh_ ? rd::k_step_co<R, rd::RNG_PHILOX, true, INIT>
+                                : rd::k_step_co<R, rd::RNG_PHILOX, false, INIT>)
+                    : (use_bvh_ ? rd::k_step_co<R, rd::RNG_PCG, true, INIT> : rd::k_step_co<R, rd::RNG_PCG, false, INIT>);
     size_t scene = (smem_ + 15) & ~size_t(15);
     size_t smem = scene + (co_pv_global_ ? 0 : static_cast<size_t>(128) * d_.max_vertices * sizeof(rd::GV<R>));
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -839,7 +855,7 @@ template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) 
     }
     RAMLT_CUDA(cudaMemsetAsync(work_.p, 0, sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (d_.profile_kernels) {
+    if (d_.profile_kernels && !INIT) {
         if (ev_.size() >= 4096)
             drain_events();
         RAMLT_CUDA(cudaEventCreate(&e0));
@@ -849,7 +865,7 @@ template <class R> void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) 
     kern<<<blocks, 128, smem, stream_>>>(P, work_.p);
     ++launches_;
     RAMLT_CUDA(cudaGetLastError());
-    if (d_.profile_kernels) {
+    if (d_.profile_kernels && !INIT) {
         RAMLT_CUDA(cudaEventRecord(e1, stream_));
         ev_.emplace_back(e0, e1);
     }

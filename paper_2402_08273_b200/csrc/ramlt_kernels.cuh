@@ -107,6 +107,7 @@ template <class R> struct StepParams {
     int record_visits;   // write vreg/va (adaptive)
     int steal;           // k_step_co: 1 = warp-aggregated work stealing, 0 = one chain per lane
     int refill;          // k_step_co (BVH): idle lanes that end a traversal round
+    unsigned long long init_attempts;   // k_step_co<INIT>: attempts per chain before giving up
     GV<R> *pv_scratch;   // k_step_co: proposal vertices in global memory (nullptr: smem)
     int ktab_l2;         // region kernel tables change inside this launch (cooperative): read via L2
     int pooled;          // fuse pooled accumulation into the step

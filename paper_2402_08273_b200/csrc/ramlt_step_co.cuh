@@ -140,7 +140,10 @@ enum { CO_RAY_PENDING = 1, CO_STEP_DONE = 2 };
     case (N):;                                                                                     \
     } while (0)
 
-template <class R, int RK> struct StepCo {
+// INIT: the same coroutine runs chain initialisation (core/driver.cpp:219-242):
+// large-step eye paths from the chain's init stream until one has a nonzero
+// contribution, then the chain's state is written (as init_chain does).
+template <class R, int RK, bool INIT = false> struct StepCo {
     // ---- chain (persists over the chain's steps) ----
     int c;
     long long gc;
@@ -164,18 +167,55 @@ template <class R, int RK> struct StepCo {
     double ep;
     R eseg;
     int ek, ei;
+    unsigned long long attempts;   // INIT
 
     __device__ __forceinline__ int advance(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
                                            RayCount &rc, unsigned long long index);
+
+    // INIT: write the found path (vertices 1..kp-1, contribution) and the
+    // chain's fresh counters and step stream -- what init_chain stores.
+    __device__ __forceinline__ void init_commit(const StepParams<R> &P, const PvSmem<R> &pv) {
+        if (pcb.pi > R(0)) {
+            for (int q = 1; q < kp; ++q)
+                store_gv(&P.ch.verts[static_cast<size_t>(q - 1) * P.C + c], pv.get(q));
+            P.ch.klen[c] = kp;
+            P.ch.smask[c] = smp;
+            P.ch.cf[c] = pcb.f.x;
+            P.ch.cf[P.C + c] = pcb.f.y;
+            P.ch.cf[2 * P.C + c] = pcb.f.z;
+            P.ch.cf[3 * P.C + c] = pcb.pi;
+            P.ch.cr[c] = pcb.u;
+            P.ch.cr[P.C + c] = pcb.v;
+        }
+        P.ch.eyeden[c] = __longlong_as_double(0x7ff8000000000000LL);
+        P.ch.acc[c] = 0.0;
+        P.ch.iacc[c] = 0.0;
+        P.ch.lum[c] = 0.0;
+        P.ch.npert[c] = 0;
+        P.ch.nlarge[c] = 0;
+        P.ch.ipert[c] = 0;
+        P.ch.nsteps[c] = 0;
+        Rng<RK> fresh;
+        fresh.reseed(P.seed, static_cast<unsigned long long>(gc));
+        RngIO<RK>::store(fresh, P.ch.rng0, P.ch.rng1, c);
+    }
 };
 
-template <class R, int RK>
-__device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, const SceneView<R> &S,
+template <class R, int RK, bool INIT>
+__device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> &P, const SceneView<R> &S,
                                                       const PvSmem<R> &pv, RayCount &rc,
                                                       unsigned long long index) {
     CurPath<R> cur{P.ch.verts, P.C, c, &S.cam};
     switch (pc) {
     case 0: {
+        if constexpr (INIT) {
+            choose = false;
+            s_pert = R(0);
+            a = 0.0;
+            region = -1;
+            head_end = 0;
+            goto init_attempt;
+        }
         {
             // suitability (core/mutations.cpp:47-56) and strategy selection (driver.cpp:115-116)
             bool elig;
@@ -274,6 +314,8 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
 
     large_step:
         ++cs.nlarge;
+    init_attempt:
+        pcb.pi = R(0);
         // trace_eye_subpath (path.cpp:84-142) -- large_step (mutations.cpp:58-71)
         {
             Vx<R> cv;
@@ -434,6 +476,14 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
     eval_fail:
         pcb.pi = R(0);
     eval_done:
+        if constexpr (INIT) {
+            if (pcb.pi > R(0)) {
+                init_commit(P, pv);
+                pc = 0;
+                return CO_STEP_DONE;
+            }
+            goto finish;
+        }
         if (choose) {
             if (pcb.pi > R(0)) {
                 if (P.ctl == 2) {
@@ -541,6 +591,14 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
         ++cs.ipert;
 
     finish:
+        if constexpr (INIT) {   // failed attempt: the next one continues the init stream
+            if (++attempts < P.init_attempts)
+                goto init_attempt;
+            atomicExch(P.ch.err, 1);
+            init_commit(P, pv);
+            pc = 0;
+            return CO_STEP_DONE;
+        }
         // splat (driver.cpp:59-64)
         if (a < 1.0 && cs.pi > R(0))
             film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - static_cast<R>(a)) / cs.pi), cs.lum);
@@ -583,8 +641,8 @@ __device__ __forceinline__ int StepCo<R, RK>::advance(const StepParams<R> &P, co
 
 #undef CO_RAY
 
-template <class R, int RK>
-__device__ __forceinline__ void co_load(StepCo<R, RK> &co, const StepParams<R> &P, int c) {
+template <class R, int RK, bool I>
+__device__ __forceinline__ void co_load(StepCo<R, RK, I> &co, const StepParams<R> &P, int c) {
     co.c = c;
     co.gc = P.chain_off + c;
     ChainRegs<R> &cs = co.cs;
@@ -606,8 +664,8 @@ __device__ __forceinline__ void co_load(StepCo<R, RK> &co, const StepParams<R> &
     co.pc = 0;
 }
 
-template <class R, int RK>
-__device__ __forceinline__ void co_store(const StepCo<R, RK> &co, const StepParams<R> &P) {
+template <class R, int RK, bool I>
+__device__ __forceinline__ void co_store(const StepCo<R, RK, I> &co, const StepParams<R> &P) {
     const int c = co.c;
     const ChainRegs<R> &cs = co.cs;
     P.ch.klen[c] = cs.k;
@@ -635,7 +693,8 @@ __device__ __forceinline__ void co_store(const StepCo<R, RK> &co, const StepPara
 #define RAMLT_CO_MINBLOCKS 8
 #endif
 // Persistent, work-stealing chain-step kernel.  `work` is a zeroed counter.
-template <class R, int RK, bool BVH>
+// INIT: chain initialisation instead of steps (k_init's job, same results).
+template <class R, int RK, bool BVH, bool INIT = false>
 __global__ void __launch_bounds__(128, BVH && sizeof(R) == 4 ? RAMLT_CO_MINBLOCKS : 1)
 k_step_co(StepParams<R> P, unsigned int *work) {
     extern __shared__ __align__(16) char smem[];
@@ -651,7 +710,7 @@ k_step_co(StepParams<R> P, unsigned int *work) {
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
 
-    StepCo<R, RK> co;
+    StepCo<R, RK, INIT> co;
     RayCount rc;
     BvhTrav<R> tv;   // BVH: resumable traversal of this lane's pending ray
     int tv_stc[BvhTrav<R>::STACK];
@@ -677,7 +736,14 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                     mine = first_grab ? blockIdx.x * blockDim.x + threadIdx.x : 0xffffffffu;
                     first_grab = false;
                 }
-                if (mine < static_cast<unsigned>(P.C)) {
+                if (INIT && mine < static_cast<unsigned>(P.C)) {
+                    co.c = static_cast<int>(mine);
+                    co.gc = P.chain_off + co.c;
+                    co.rng.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(co.gc) * 2ull);
+                    co.pc = 0;
+                    co.attempts = 0;
+                    have = true;
+                } else if (mine < static_cast<unsigned>(P.C)) {
                     co_load(co, P, static_cast<int>(mine));
                     const unsigned long long my_steps =
                         P.per + (static_cast<unsigned long long>(co.gc) < P.rem ? 1ull : 0ull);
@@ -702,6 +768,8 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                 want = true;
                 if constexpr (BVH)
                     tv.begin(S, co.ray.o, co.ray.d, co.ray.lim, co.ray.lim < M<R>::inf());
+            } else if (INIT) {
+                have = false;   // the coroutine stored the chain
             } else if (++j >= jend) {
                 co_store(co, P);
                 have = false;
@@ -732,6 +800,8 @@ k_step_co(StepParams<R> P, unsigned int *work) {
             want = false;
         }
     }
+    if (INIT)   // ray statistics cover mutations only (as with k_init)
+        return;
     unsigned act = __activemask();
     unsigned sc = __reduce_add_sync(act, static_cast<unsigned>(rc.c));
     unsigned sv = __reduce_add_sync(act, static_cast<unsigned>(rc.v));
