@@ -2,10 +2,12 @@
 #include "bvh.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
+#include <thread>
 
 namespace ramlt_b200 {
 
@@ -39,14 +41,29 @@ struct Box {
     }
 };
 
-struct Builder {
-    const double *tris;
+struct Shared {
     std::vector<Box> tb;          // per-triangle bounds
     std::vector<double> cen;      // centroids, 3 per triangle
-    std::vector<int32_t> idx;     // working order
+    std::vector<int32_t> idx;     // working order (subtrees partition disjoint ranges)
+};
+
+// A subtree deferred to the parallel phase: idx[s, e) below child `slot` of `parent`.
+struct Task {
+    int s, e, d, parent, slot;
+};
+
+struct Builder {
+    Shared *sh;
+    std::vector<Box> &tb;
+    std::vector<double> &cen;
+    std::vector<int32_t> &idx;
     std::vector<BvhBuildNode> nodes;
     int leaf_max;
     int depth = 0;
+    int par_depth = -1;                 // >= 0: defer subtrees starting at this depth
+    std::vector<Task> *tasks = nullptr;
+
+    Builder(Shared *s, int lm) : sh(s), tb(s->tb), cen(s->cen), idx(s->idx), leaf_max(lm) {}
 
     // Outward padding: a few ulps of the coordinate magnitude plus an absolute
     // floor, so fp32/fp64 slab tests (with their own slack) never cull a hit.
@@ -139,6 +156,14 @@ struct Builder {
         return node(s, m, e, d);
     }
 
+    int32_t child(int s, int e, int d, int parent, int slot) {
+        if (tasks && d == par_depth && e - s > leaf_max) {
+            tasks->push_back({s, e, d, parent, slot});
+            return 0;   // patched after the parallel phase
+        }
+        return build(s, e, d);
+    }
+
     int32_t split_median(int s, int e, int d) {
         Box cb;
         cb.reset();
@@ -160,8 +185,8 @@ struct Builder {
         Box l = range_box(s, m), r = range_box(m, e);
         pad(l);
         pad(r);
-        int32_t c0 = build(s, m, d + 1);
-        int32_t c1 = build(m, e, d + 1);
+        int32_t c0 = child(s, m, d + 1, self, 0);
+        int32_t c1 = child(m, e, d + 1, self, 1);
         BvhBuildNode &nd = nodes[self];
         std::memcpy(nd.lo[0], l.lo, sizeof(l.lo));
         std::memcpy(nd.hi[0], l.hi, sizeof(l.hi));
@@ -180,57 +205,83 @@ BvhBuild build_bvh(const double *tris, size_t n, int leaf_max) {
         throw std::invalid_argument("build_bvh: no triangles");
     if (n >= (size_t(1) << 27))
         throw std::invalid_argument("build_bvh: too many triangles");
-    Builder b;
-    b.tris = tris;
-    b.leaf_max = std::min(std::max(leaf_max, 1), 15);
-    b.tb.resize(n);
-    b.cen.resize(3 * n);
-    b.idx.resize(n);
+    Shared sh;
+    sh.tb.resize(n);
+    sh.cen.resize(3 * n);
+    sh.idx.resize(n);
     for (size_t i = 0; i < n; ++i) {
         Box bx;
         bx.reset();
         for (int v = 0; v < 3; ++v)
             bx.grow(tris + 9 * i + 3 * v);
-        b.tb[i] = bx;
+        sh.tb[i] = bx;
         for (int k = 0; k < 3; ++k)
-            b.cen[3 * i + k] = 0.5 * (bx.lo[k] + bx.hi[k]);
-        b.idx[i] = static_cast<int32_t>(i);
+            sh.cen[3 * i + k] = 0.5 * (bx.lo[k] + bx.hi[k]);
+        sh.idx[i] = static_cast<int32_t>(i);
     }
+    Builder b(&sh, std::min(std::max(leaf_max, 1), 15));
     b.nodes.reserve(2 * n / static_cast<size_t>(b.leaf_max) + 2);
-    // The root is always an internal node (a single leaf gets an empty sibling).
-    if (n <= static_cast<size_t>(b.leaf_max)) {
+    auto wrap_leaf = [&](int32_t code) {   // the root is always an internal node
         BvhBuildNode root;
         Box bx = b.range_box(0, static_cast<int>(n));
         Builder::pad(bx);
         std::memcpy(root.lo[0], bx.lo, sizeof(bx.lo));
         std::memcpy(root.hi[0], bx.hi, sizeof(bx.hi));
         for (int k = 0; k < 3; ++k) {
-            root.lo[1][k] = 1.0;   // empty box: lo > hi never intersects
+            root.lo[1][k] = 1.0;   // empty sibling; its leaf has no triangles
             root.hi[1][k] = -1.0;
         }
-        root.child[0] = b.leaf(0, static_cast<int>(n));
+        root.child[0] = code;
         root.child[1] = b.leaf(0, 0);
         b.nodes.push_back(root);
+    };
+    if (n <= static_cast<size_t>(b.leaf_max)) {
+        wrap_leaf(b.leaf(0, static_cast<int>(n)));
     } else {
+        // Top levels serially; the subtrees below depth `par_depth` on worker
+        // threads (disjoint idx ranges), appended in task order -- the tree
+        // does not depend on the thread count.
+        std::vector<Task> tasks;
+        unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        if (n >= 65536) {
+            b.par_depth = 6;
+            b.tasks = &tasks;
+        }
         int32_t r = b.build(0, static_cast<int>(n), 0);
-        if (r < 0) {   // degenerate set collapsed into one leaf: wrap it
-            BvhBuildNode root;
-            Box bx = b.range_box(0, static_cast<int>(n));
-            Builder::pad(bx);
-            std::memcpy(root.lo[0], bx.lo, sizeof(bx.lo));
-            std::memcpy(root.hi[0], bx.hi, sizeof(bx.hi));
-            for (int k = 0; k < 3; ++k) {
-                root.lo[1][k] = 1.0;
-                root.hi[1][k] = -1.0;
+        if (r < 0)   // degenerate set collapsed into one leaf
+            wrap_leaf(r);
+        std::vector<Builder *> subs(tasks.size(), nullptr);
+        std::vector<int32_t> roots(tasks.size(), 0);
+        std::vector<std::thread> pool;
+        std::atomic<size_t> next{0};
+        unsigned nthreads = static_cast<unsigned>(std::min<size_t>(hw, tasks.size()));
+        for (size_t t = 0; t < tasks.size(); ++t)
+            subs[t] = new Builder(&sh, b.leaf_max);
+        for (unsigned w = 0; w < nthreads; ++w)
+            pool.emplace_back([&] {
+                for (size_t t; (t = next.fetch_add(1)) < tasks.size();)
+                    roots[t] = subs[t]->build(tasks[t].s, tasks[t].e, tasks[t].d);
+            });
+        for (auto &th : pool)
+            th.join();
+        for (size_t t = 0; t < tasks.size(); ++t) {
+            Builder &sb = *subs[t];
+            int32_t base = static_cast<int32_t>(b.nodes.size());
+            for (BvhBuildNode nd : sb.nodes) {
+                for (int k = 0; k < 2; ++k)
+                    if (nd.child[k] >= 0)
+                        nd.child[k] += base;
+                b.nodes.push_back(nd);
             }
-            root.child[0] = r;
-            root.child[1] = b.leaf(0, 0);
-            b.nodes.push_back(root);
+            int32_t root = roots[t] >= 0 ? roots[t] + base : roots[t];
+            b.nodes[static_cast<size_t>(tasks[t].parent)].child[tasks[t].slot] = root;
+            b.depth = std::max(b.depth, sb.depth);
+            delete subs[t];
         }
     }
     BvhBuild out;
     out.nodes = std::move(b.nodes);
-    out.order = std::move(b.idx);
+    out.order = std::move(sh.idx);
     out.depth = b.depth;
     return out;
 }

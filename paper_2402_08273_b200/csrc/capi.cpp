@@ -4,6 +4,7 @@
 // contraction so the camera basis rounds exactly like the reference's.
 #include "engine.h"
 
+#include <charconv>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -73,23 +74,102 @@ CameraBasis make_camera(const double cam[10], int width, int height) {
     return c;
 }
 
+// Fast path for the bulk records ("tri", "sphere"): whitespace-separated
+// tokens with std::from_chars, which rounds exactly like the stream's strtod.
+// Anything unusual (a '+' sign, a token from_chars does not consume whole,
+// out-of-range values, missing tokens) returns false and the line goes
+// through the istringstream path, so results and errors match the reference.
+namespace {
+inline bool is_ws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r'; }
+struct Tok {
+    const char *p, *e;
+    bool next(const char *&b, const char *&t) {
+        while (p < e && is_ws(*p))
+            ++p;
+        if (p == e)
+            return false;
+        b = p;
+        while (p < e && !is_ws(*p))
+            ++p;
+        t = p;
+        return true;
+    }
+    bool num(double &x) {
+        const char *b, *t;
+        if (!next(b, t) || *b == '+')
+            return false;
+        for (const char *c = b; c < t; ++c)   // plain decimal only (no inf/nan/hex)
+            if (!((*c >= '0' && *c <= '9') || *c == '.' || *c == 'e' || *c == 'E' || *c == '-' || *c == '+'))
+                return false;
+        auto r = std::from_chars(b, t, x);
+        return r.ec == std::errc() && r.ptr == t;
+    }
+};
+}  // namespace
+
 // parse_scene mirror (core/scene.cpp:104-234): same grammar, same messages.
 static HostScene parse_scene(const std::string &text, const std::string &origin) {
     HostScene s;
     std::map<std::string, int> ids;
     bool have_camera = false;
     std::vector<std::pair<bool, int>> order;
-    std::istringstream stream(text);
     std::string line;
     int ln = 0;
     auto fail = [&](int l, const std::string &msg) {
         throw std::runtime_error(origin + ":" + std::to_string(l) + ": " + msg);
     };
-    while (std::getline(stream, line)) {
+    const char *cur = text.data(), *end = text.data() + text.size();
+    while (cur < end) {
+        const char *eol = static_cast<const char *>(std::memchr(cur, '\n', static_cast<size_t>(end - cur)));
+        if (!eol)
+            eol = end;
+        const char *lb = cur;
+        cur = eol < end ? eol + 1 : end;
         ++ln;
-        size_t start = line.find_first_not_of(" \t\r");
-        if (start == std::string::npos || line[start] == '#')
-            continue;
+        {
+            const char *q = lb;
+            while (q < eol && (*q == ' ' || *q == '\t' || *q == '\r'))
+                ++q;
+            if (q == eol || *q == '#')
+                continue;
+            Tok tk{q, eol};
+            const char *tb = q, *te = q;
+            tk.next(tb, te);
+            std::string_view tg(tb, static_cast<size_t>(te - tb));
+            if (tg == "tri") {
+                ramlt_triangle t{};
+                double *v[9] = {&t.a[0], &t.a[1], &t.a[2], &t.b[0], &t.b[1], &t.b[2], &t.c[0], &t.c[1], &t.c[2]};
+                bool ok = true;
+                for (double *x : v)
+                    ok = ok && tk.num(*x);
+                const char *mb, *me;
+                if (ok && tk.next(mb, me)) {
+                    auto it = ids.find(std::string(mb, static_cast<size_t>(me - mb)));
+                    if (it != ids.end()) {
+                        t.material = it->second;
+                        t.emitter = -1;
+                        order.emplace_back(false, static_cast<int>(s.tri.size()));
+                        s.tri.push_back(t);
+                        continue;
+                    }
+                }
+            } else if (tg == "sphere") {
+                ramlt_sphere sp{};
+                bool ok = tk.num(sp.center[0]) && tk.num(sp.center[1]) && tk.num(sp.center[2]) && tk.num(sp.radius);
+                const char *mb, *me;
+                if (ok && sp.radius > 0.0 && tk.next(mb, me)) {
+                    auto it = ids.find(std::string(mb, static_cast<size_t>(me - mb)));
+                    if (it != ids.end()) {
+                        sp.material = it->second;
+                        sp.emitter = -1;
+                        order.emplace_back(true, static_cast<int>(s.sph.size()));
+                        s.sph.push_back(sp);
+                        continue;
+                    }
+                }
+            }
+        }
+        line.assign(lb, static_cast<size_t>(eol - lb));
         std::istringstream ls(line);
         std::string tag;
         ls >> tag;

@@ -131,3 +131,74 @@ def test_invalid_config_errors_before_device():
             Engine(scenes.cornell_box(), RenderConfig(**bad))
     with pytest.raises(ValueError):
         Engine(scenes.cornell_box(), RenderConfig(max_vertices=40))
+
+
+def _parsed_prims(text):
+    from paper_2402_08273_b200 import parse_scene
+    sc = parse_scene(text, "<s>")
+    d = sc.desc
+    tris = [(tuple(t.a) + tuple(t.b) + tuple(t.c), t.material, t.emitter)
+            for t in (d.triangles[i] for i in range(d.n_triangles))]
+    sphs = [(tuple(s.center) + (s.radius,), s.material, s.emitter)
+            for s in (d.spheres[i] for i in range(d.n_spheres))]
+    return tris, sphs
+
+
+def _py_prims(text):
+    """Independent parse of the geometry records: Python's float() is
+    correctly rounded, like the reference stream's strtod."""
+    mats, tris, sphs, order = {}, [], [], []
+    for line in text.split("\n"):
+        tok = line.split()
+        if not tok or tok[0].startswith("#"):
+            continue
+        if tok[0] == "material":
+            mats[tok[1]] = len(mats)
+        elif tok[0] == "tri":
+            order.append(("t", len(tris)))
+            tris.append([tuple(float(x) for x in tok[1:10]), mats[tok[10]], -1])
+        elif tok[0] == "sphere":
+            order.append(("s", len(sphs)))
+            sphs.append([tuple(float(x) for x in tok[1:5]), mats[tok[5]], -1])
+        elif tok[0] == "emitter":
+            kind, i = order[int(tok[1])]
+            (tris if kind == "t" else sphs)[i][2] = sum(1 for t in tris if t[2] >= 0) + \
+                sum(1 for s in sphs if s[2] >= 0)
+    return [tuple(t) for t in tris], [tuple(s) for s in sphs]
+
+
+def test_scene_parse_values_bit_exact():
+    """The from_chars fast path and the stream path parse every coordinate to
+    the correctly rounded double (bit-exact with the reference's strtod)."""
+    from paper_2402_08273_b200 import scenes
+    odd = ("camera 0 0 -3 0 0 0 0 1 0 45\nmaterial m diffuse 0.5 0.5 0.5\n"
+           "tri +1 .5 1. 1E3 -0 0.1000000000000000055511151231257827 1e-5 2.5e+2 7 m\n"
+           "tri 0.3 0.30000000000000004 1e-320 3 4 5 6 7 8   m   trailing tokens\n"
+           "  \t sphere 0 0 3 1 m\r\n# comment\n\nsphere +0 -0 3.0 .25 m\nemitter 3 1 1 1\n")
+    texts = [fn() for fn in (scenes.cornell_box, scenes.caustic_box, scenes.mirror_box)]
+    texts += [scenes.cluster_room(n_tris=2000), odd]
+    for text in texts:
+        tris, sphs = _parsed_prims(text)
+        ptris, psphs = _py_prims(text)
+        assert len(tris) == len(ptris) and len(sphs) == len(psphs)
+        for got, want in zip(tris + sphs, ptris + psphs):
+            assert got[0] == want[0] and got[1] == want[1]
+
+
+@pytest.mark.parametrize("rec", ["tri 0 0 0 1 0 0 0 1 inf m", "tri 0 0 0 1 0 0 0 1 nan m",
+                                 "tri 0 0 0 1 0 0 0 1 0x1p1 m", "tri 0 0 0 1 0 0 0 1 1e999 m",
+                                 "tri 0 0 0 1 0 0 0 1 m", "sphere 0 0 1e999 1 m", "tri 0 0 0 1 0 0 0 1 2,5 m"])
+def test_scene_parse_odd_numbers_match_reference(ref_lib, rec):
+    """Tokens the fast path does not take fall back to the stream path: same
+    result (accepted or the same error) as the reference parser."""
+    from paper_2402_08273_b200 import parse_scene
+    text = f"camera 0 0 -3 0 0 0 0 1 0 45\nmaterial m diffuse 0.5 0.5 0.5\nsphere 0 0 3 1 m\nemitter 0 1 1 1\n{rec}\n"
+    err = C.create_string_buffer(512)
+    counts = (C.c_int * 4)()
+    rc = ref_lib.lib.ref_parse(text.encode(), counts, err, 512)
+    if rc == 0:
+        assert parse_scene(text, "<s>").counts == tuple(counts)
+    else:
+        with pytest.raises(RuntimeError) as e:
+            parse_scene(text, "<s>")
+        assert str(e.value) == err.value.decode().replace("<scene>", "<s>")
