@@ -34,12 +34,12 @@ WORKLOADS = {
                desc="C1 Cornell box: 36 tri, 256^2, path length 8, 1,024 chains"),
     "c4": dict(scene="clusters", scene_args={"n_tris": 1 << 20}, chains=1 << 20, steps_per_chain=1 << 12,
                width=1024, height=1024, max_vertices=13, strategy="ra-quadtree", perturbation="lens",
-               bound="hbm", scaling="weak", e2e_steps=32, cpu_sample=256, cpu_b=16,
+               bound="hbm", scaling="weak", e2e_steps=128, cpu_sample=256, cpu_b=16,
                desc="C4 clustered room: 2^20 + 20 tri (64 clusters, 4 lights), 1024^2, path length 12, "
                     "1,048,576 chains, SAH BVH"),
     "c5": dict(scene="clusters", scene_args={"n_tris": 1 << 20}, chains=1 << 23, steps_per_chain=1 << 12,
                width=2048, height=2048, max_vertices=13, strategy="ra-quadtree", perturbation="lens",
-               bound="hbm", scaling="strong", e2e_steps=8, cpu_sample=256, cpu_b=16,
+               bound="hbm", scaling="strong", e2e_steps=128, cpu_sample=256, cpu_b=16,
                desc="C5 scaling config: the C4 scene at 2048^2, 8,388,608 chains split across the GPUs"),
 }
 METRIC = "MLT mutations/sec"

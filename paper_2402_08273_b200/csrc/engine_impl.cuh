@@ -838,6 +838,9 @@ void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
                     : (use_bvh_ ? rd::k_step_co<R, rd::RNG_PCG, true, INIT> : rd::k_step_co<R, rd::RNG_PCG, false, INIT>);
     size_t scene = (smem_ + 15) & ~size_t(15);
     size_t smem = scene + (co_pv_global_ ? 0 : static_cast<size_t>(128) * d_.max_vertices * sizeof(rd::GV<R>));
+    P.co_stack_off = static_cast<unsigned>(smem);
+    if (use_bvh_)
+        smem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
     RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));

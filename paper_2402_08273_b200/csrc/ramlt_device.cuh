@@ -201,6 +201,8 @@ template <class R> struct alignas(16) BvhNodeD {
     R lo0[3], hi0[3], lo1[3], hi1[3];
     int c0, c1;
 };
+static_assert(sizeof(BvhNodeD<float>) == 64, "ld_node reads 4 x 16 B");
+static_assert(sizeof(TriT<float>) == 48, "ld_trit reads 3 x 16 B");
 template <class R> struct SphD {
     V3<R> c;
     R r;
@@ -298,6 +300,33 @@ __device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &
     return false;
 }
 
+// Read-only vector loads of BVH records (fp32: 4 x 16 B per node, 3 x 16 B per
+// leaf triangle through the non-coherent path) instead of one scalar load per
+// field -- a quarter of the L1 requests.
+template <class R> __device__ __forceinline__ BvhNodeD<R> ld_node(const BvhNodeD<R> *p) { return *p; }
+template <> __device__ __forceinline__ BvhNodeD<float> ld_node(const BvhNodeD<float> *p) {
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), e = __ldg(q + 3);
+    BvhNodeD<float> n;
+    n.lo0[0] = a.x, n.lo0[1] = a.y, n.lo0[2] = a.z, n.hi0[0] = a.w;
+    n.hi0[1] = b.x, n.hi0[2] = b.y, n.lo1[0] = b.z, n.lo1[1] = b.w;
+    n.lo1[2] = c.x, n.hi1[0] = c.y, n.hi1[1] = c.z, n.hi1[2] = c.w;
+    n.c0 = __float_as_int(e.x);
+    n.c1 = __float_as_int(e.y);
+    return n;
+}
+template <class R> __device__ __forceinline__ TriT<R> ld_trit(const TriT<R> *p) { return *p; }
+template <> __device__ __forceinline__ TriT<float> ld_trit(const TriT<float> *p) {
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    TriT<float> t;
+    t.a[0] = a.x, t.a[1] = a.y, t.a[2] = a.z, t.e1[0] = a.w;
+    t.e1[1] = b.x, t.e1[2] = b.y, t.e2[0] = b.z, t.e2[1] = b.w;
+    t.e2[2] = c.x;
+    t.orig = __float_as_int(c.y);
+    return t;
+}
+
 // Moeller-Trumbore on the compact record: identical arithmetic to hit_tri.
 template <class R>
 __device__ __forceinline__ bool hit_tri_t(const TriT<R> &tr, V3<R> o, V3<R> d, R &t) {
@@ -377,7 +406,21 @@ template <class R> struct BvhTrav {
     R best;
     int key, pos, spos, node, leaf, sp;
     bool any;
-    int *stc;   // the lane's stack (kept outside so the scalars stay in registers)
+    // The lane's stack: the first SSTACK entries in shared memory at stride
+    // 128 (one bank per lane: conflict-free whatever each lane's depth), the
+    // rest in local memory.  Scattered per-lane depths made a local-only stack
+    // the top L1 miss / long-scoreboard stall.
+    static constexpr int SSTACK = 16;
+    int *ss;    // shared: entry i at ss[i * 128]
+    int *sl;    // local: entry i >= SSTACK at sl[i - SSTACK]
+
+    __device__ __forceinline__ void push(int v) {
+        if (sp < SSTACK)
+            ss[sp * 128] = v;
+        else
+            sl[sp - SSTACK] = v;
+        ++sp;
+    }
 
     // Spheres first (linear scan, strict '<'), then the BVH below `best`.
     __device__ __forceinline__ void begin(const SceneView<R> &s, V3<R> o_, V3<R> d_, R lim, bool any_hit) {
@@ -403,17 +446,22 @@ template <class R> struct BvhTrav {
         node = (any && spos >= 0) ? DONE : 0;
     }
 
-    __device__ __forceinline__ int pop() { return sp > 0 ? stc[--sp] : DONE; }
+    __device__ __forceinline__ int pop() {
+        if (sp == 0)
+            return DONE;
+        --sp;
+        return sp < SSTACK ? ss[sp * 128] : sl[sp - SSTACK];
+    }
 
     __device__ __forceinline__ bool step(const SceneView<R> &s) {
         while (node >= 0 && node != DONE) {
-            const BvhNodeD<R> &n = s.bvh[node];
+            const BvhNodeD<R> n = ld_node(s.bvh + node);
             R t0, t1;
             bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
             bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
             if (h0 && h1) {
                 bool near0 = t0 <= t1;
-                stc[sp++] = near0 ? n.c1 : n.c0;
+                push(near0 ? n.c1 : n.c0);
                 node = near0 ? n.c0 : n.c1;
             } else if (h0) {
                 node = n.c0;
@@ -435,7 +483,7 @@ template <class R> struct BvhTrav {
             int code = ~leaf;
             int first = code >> 4, cnt = code & 15;
             for (int k = first; k < first + cnt; ++k) {
-                const TriT<R> &tr = s.trt[k];
+                const TriT<R> tr = ld_trit(s.trt + k);
                 R t;
                 if (!hit_tri_t(tr, o, d, t))
                     continue;
@@ -489,7 +537,7 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
     int leaf = 0;    // postponed leaf code (< 0) or 0
     for (;;) {
         while (node >= 0 && node != DONE) {
-            const BvhNodeD<R> &n = s.bvh[node];
+            const BvhNodeD<R> n = ld_node(s.bvh + node);
             R t0, t1;
             bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
             bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
@@ -517,7 +565,7 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
             int code = ~leaf;
             int first = code >> 4, cnt = code & 15;
             for (int k = first; k < first + cnt; ++k) {
-                const TriT<R> &tr = s.trt[k];
+                const TriT<R> tr = ld_trit(s.trt + k);
                 R t;
                 if (!hit_tri_t(tr, o, d, t))
                     continue;

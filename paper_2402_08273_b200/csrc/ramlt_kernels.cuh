@@ -109,6 +109,7 @@ template <class R> struct StepParams {
     int refill;          // k_step_co (BVH): idle lanes that end a traversal round
     unsigned long long init_attempts;   // k_step_co<INIT>: attempts per chain before giving up
     GV<R> *pv_scratch;   // k_step_co: proposal vertices in global memory (nullptr: smem)
+    unsigned co_stack_off;   // k_step_co (BVH): byte offset of the shared traversal stacks
     int ktab_l2;         // region kernel tables change inside this launch (cooperative): read via L2
     int pooled;          // fuse pooled accumulation into the step
     RegionArrays reg;

@@ -713,8 +713,9 @@ k_step_co(StepParams<R> P, unsigned int *work) {
     StepCo<R, RK, INIT> co;
     RayCount rc;
     BvhTrav<R> tv;   // BVH: resumable traversal of this lane's pending ray
-    int tv_stc[BvhTrav<R>::STACK];
-    tv.stc = tv_stc;
+    int tv_sl[BvhTrav<R>::STACK - BvhTrav<R>::SSTACK];
+    tv.sl = tv_sl;
+    tv.ss = reinterpret_cast<int *>(smem + P.co_stack_off) + threadIdx.x;
     bool have = false, exhausted = false, want = false;
     int j = 0, jend = 0;
     bool first_grab = true;
