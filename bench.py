@@ -42,6 +42,11 @@ WORKLOADS = {
                bound="hbm", scaling="strong", e2e_steps=128, cpu_sample=256, cpu_b=16,
                desc="C5 scaling config: the C4 scene at 2048^2, 8,388,608 chains split across the GPUs"),
 }
+# configs[1]: the analytic-target adaptive MCMC harness (include/ramlt_mix.h);
+# a parity case of the metric's family, measured on its own line (not the default)
+C2 = dict(chains=65536, steps=4096, dim=8, n_comp=4, target_seed=0, strategy="global",
+          desc="C2 analytic target: 4 anisotropic Gaussians in [0,1]^8, 65,536 chains x 4,096 steps, "
+               "Global (scalar lambda) pooled adaptation")
 METRIC = "MLT mutations/sec"
 UNIT = "mutations/s"
 
@@ -288,17 +293,148 @@ def run_e2e_sharded(args, wl):
     return Cn * steps / float(t.item()), len(wl["scene_text"]), nbytes, 0.0
 
 
+def c2_flop_per_step(D: int, K: int) -> float:
+    """Algorithmic FP32 work of one chain step: K components x
+    (D sub + D(D+1)/2 mul + D(D-1)/2 add + 2D for |z|^2 + 2) + logsumexp (2K+1)
+    + D proposals x (Acklam central branch 24 + 2) + the MH ratio (2)."""
+    return K * (D * D + 3 * D + 2) + (2 * K + 1) + 26 * D + 2
+
+
+def bench_c2(args):
+    """configs[1] line: device-resident timing of K lockstep steps of all
+    chains (one cooperative launch per 1,024 steps), plus the e2e run through
+    the C-ABI with host buffers and the reference-composition CPU baseline."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2402_08273_b200 import _capi
+    from paper_2402_08273_b200.mix import MixConfig, MixEngine, MixTarget
+    world, rank, local = dist_env()
+    steps = args.steps
+    config = {"workload": "c2", "desc": C2["desc"], "chains": C2["chains"], "dim": C2["dim"],
+              "n_comp": C2["n_comp"], "strategy": C2["strategy"], "adaptation": "pooled",
+              "step": "one lockstep step (propose, evaluate, accept, adapt) of every chain",
+              "l2": "chain state (2.6 MB) is L2-resident by design: the kernel keeps chains in registers "
+                    "across steps, so no flush applies", "rng": "philox4x32-10"}
+    tgt = MixTarget.config2(C2["target_seed"], C2["dim"], C2["n_comp"])
+    D, K = C2["dim"], C2["n_comp"]
+    threads = os.cpu_count() or 1
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        line = c2_cpu_line(args, tgt, config)
+        print(json.dumps(line), flush=True)
+        return
+    if world > 1:
+        raise SystemExit("c2 is a single-GPU parity workload (replicas only); run it with --gpus 1")
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+    eng = MixEngine(tgt, MixConfig(strategy=C2["strategy"], chains=C2["chains"], seed=1, precision="f32",
+                                   rng="philox", adapt_mode="pooled", device=local, profile_kernels=True))
+    eng.set_stream(stream.cuda_stream)
+    eng.init_chains()
+    eng.run(args.warmup)
+    torch.cuda.synchronize()
+    s0 = eng.stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        eng.run(steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    s1 = eng.stats()
+    muts = steps * C2["chains"]
+    value = muts / (ms / 1e3)
+    launches = s1.kernel_launches - s0.kernel_launches
+    kms = s1.step_kernel_ms - s0.step_kernel_ms
+    kl = max(s1.step_kernel_launches - s0.step_kernel_launches, 1)
+    acc = s1.mean_acceptance
+    eng.close()
+    w = c2_flop_per_step(D, K)
+    sm_max = clk.summary().get("sm_max_mhz") or 1965.0
+    peak = 148 * 128 * 2 * float(sm_max) * 1e6 / 1e12
+    achieved = (muts / kl) * w / ((kms / kl) / 1e3) / 1e12
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": "nominal FP32 issue: 148 SM x 128 lanes x 2 x sm_max_mhz",
+                "work_per_unit": f"{w:.0f} FLOP per chain step (K(D^2+3D+2) + 2K+1 + 26D + 2, D={D}, K={K})",
+                "kernel": "k_mix_coop (persistent cooperative chain-step kernel)",
+                "kernel_share": kms / ms if ms else None}
+    # e2e through the C-ABI: host target arrays -> create/init/run -> host states
+    lib = _capi.load()
+    t_c, keep = tgt.to_c()
+    d = MixConfig(strategy=C2["strategy"], chains=C2["chains"], seed=2, precision="f32", rng="philox",
+                  adapt_mode="pooled", device=local).to_c()
+    xs = np.zeros((C2["chains"], D))
+    lps = np.zeros(C2["chains"])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h = C.c_void_p()
+    assert lib.ramlt_mix_create(C.byref(t_c), C.byref(d), C.byref(h)) == 0
+    assert lib.ramlt_mix_init_chains(h) == 0
+    assert lib.ramlt_mix_run(h, steps) == 0
+    dp = C.POINTER(C.c_double)
+    assert lib.ramlt_mix_read_state(h, xs.ctypes.data_as(dp), lps.ctypes.data_as(dp)) == 0
+    t1 = time.perf_counter()
+    lib.ramlt_mix_destroy(h)
+    h2d = sum(a.nbytes for a in keep)
+    cpu = None
+    if not args.no_cpu_baseline:
+        ref = c2_cpu_line(args, tgt, config)
+        cpu = ref["cpu_baseline"]
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded configs[1] target)", "config": config,
+            "mean_acceptance": acc, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": muts / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": h2d / steps,
+                    "d2h_bytes_per_step": (xs.nbytes + lps.nbytes) / steps, "steps": steps,
+                    "path": "ramlt_mix_create (host target) + init + run(K) + ramlt_mix_read_state, wall clock"},
+            "gpu_launches": launches, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
+def c2_cpu_line(args, tgt, config):
+    """The reference composition (oracle/_ref ref_mix_run: the reference's
+    controller, mh_accept, normal_quantile and PCG32) on one host thread, on a
+    bounded sample: 256 chains x 256 steps per measurement."""
+    from oracle.abi import OracleMixConfig, REF_SO, mix_run
+    reference = os.path.exists(REF_SO)
+    chains, steps = 256, 256
+    vals = []
+    for _ in range(min(max(args.steps // 512, 1), 4)):
+        t0 = time.perf_counter()
+        mix_run(tgt, OracleMixConfig(strategy=C2["strategy"], chains=chains, steps=steps, seed=1,
+                                     rng="pcg32", adapt_mode="literal"), reference=reference)
+        vals.append(chains * steps / (time.perf_counter() - t0))
+    v = sum(vals) / len(vals)
+    cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference" if reference else "port",
+           "sample": f"{chains} chains x {steps} lockstep steps of the c2 target, one host thread "
+                     f"(the reference's controller / accept / quantile / PCG32 composition)"}
+    return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": len(vals), "warmup": 0,
+            "ms_per_step": 1e3 * chains * steps / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded configs[1] target)",
+            "impl": "reference", "config": dict(config, chains_cpu=chains), "cpu_baseline": cpu,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default 16; c2: 4096)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS) + ["c2"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="mutations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        args.steps = C2["steps"] if args.workload == "c2" else 16
+    if args.workload == "c2":
+        bench_c2(args)
+        return
 
     from paper_2402_08273_b200 import scenes
     wl = dict(WORKLOADS[args.workload])

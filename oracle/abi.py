@@ -320,3 +320,109 @@ def oracle_b_partials(lib: "OracleLib", scene: str, cfg: OracleConfig, begin: in
 
 def dp(arr: np.ndarray):
     return arr.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ---- analytic-target harness (BASELINE.json configs[1]) -------------------------------------
+MIX_STRATEGIES = {"fixed": 0, "global": 1, "ra-grid": 2}
+
+
+class _CMixConfig(C.Structure):
+    _fields_ = [
+        ("strategy", C.c_int32), ("grid_n", C.c_int32), ("chains", C.c_int32),
+        ("batch_size", C.c_int32), ("gamma_max", C.c_double), ("gamma_scale", C.c_double),
+        ("target_acceptance", C.c_double), ("lambda_init", C.c_double), ("lambda_min", C.c_double),
+        ("seed", C.c_uint64), ("steps", C.c_uint64), ("rng", C.c_int32), ("adapt_mode", C.c_int32),
+        ("chain_offset", C.c_int64), ("chains_total", C.c_int64), ("log_steps", C.c_uint32),
+        ("dim", C.c_int32), ("n_comp", C.c_int32), ("pad_", C.c_int32),
+        ("weights", C.POINTER(C.c_double)), ("means", C.POINTER(C.c_double)),
+        ("covariances", C.POINTER(C.c_double)),
+    ]
+
+
+class _CMixOut(C.Structure):
+    _fields_ = [
+        ("x", C.POINTER(C.c_double)), ("log_pi", C.POINTER(C.c_double)),
+        ("log_a", C.POINTER(C.c_double)), ("log_f", C.POINTER(C.c_uint8)),
+        ("lambda_", C.POINTER(C.c_double)), ("n", C.POINTER(C.c_uint64)),
+        ("tally_accept", C.POINTER(C.c_double)), ("tally_visits", C.POINTER(C.c_uint64)),
+        ("cap_regions", C.c_uint64), ("trace", C.POINTER(_CTrace)), ("cap_trace", C.c_uint64),
+        ("n_trace", C.c_uint64), ("n_regions", C.c_uint64), ("accepted", C.c_uint64),
+        ("acceptance_sum", C.c_double),
+    ]
+
+
+@dataclass
+class OracleMixConfig:
+    strategy: str = "global"
+    grid_n: int = 4
+    chains: int = 1
+    batch_size: int = 10
+    gamma_max: float = 1.0
+    gamma_scale: float = 5.0
+    target_acceptance: float = 0.5
+    lambda_init: float = 1.0
+    lambda_min: float = -30.0
+    seed: int = 1
+    steps: int = 16
+    rng: str = "pcg32"
+    adapt_mode: str = "literal"
+    chain_offset: int = 0
+    chains_total: int = 0
+    log_steps: int = 0
+
+
+def mix_run(target, cfg: OracleMixConfig, reference: bool = False, cap_trace: int = 1 << 16) -> dict:
+    """Run the analytic-target chain loop on the CPU: the restatement
+    (oracle_mix_run) or the reference composition (ref_mix_run, PCG32 +
+    literal lockstep only).  ``target`` is a paper_2402_08273_b200.mix.MixTarget
+    (or anything with weights / means / covariances arrays)."""
+    path = REF_SO if reference else ORACLE_SO
+    lib = C.CDLL(path)
+    fn = getattr(lib, "ref_mix_run" if reference else "oracle_mix_run")
+    fn.restype = C.c_int
+    fn.argtypes = [C.POINTER(_CMixConfig), C.POINTER(_CMixOut), C.c_char_p, C.c_int]
+    w = np.ascontiguousarray(target.weights, np.float64)
+    mu = np.ascontiguousarray(target.means, np.float64)
+    cov = np.ascontiguousarray(target.covariances, np.float64)
+    K, D = mu.shape
+    c = _CMixConfig()
+    for f in fields(cfg):
+        v = getattr(cfg, f.name)
+        if f.name == "strategy":
+            v = MIX_STRATEGIES[v]
+        elif f.name == "rng":
+            v = RNGS[v]
+        elif f.name == "adapt_mode":
+            v = ADAPT_MODES[v]
+        setattr(c, f.name, v)
+    c.dim, c.n_comp = D, K
+    c.weights, c.means, c.covariances = dp(w), dp(mu), dp(cov)
+    nreg = cfg.grid_n * cfg.grid_n if cfg.strategy == "ra-grid" else 1
+    x = np.zeros((cfg.chains, D))
+    lp = np.zeros(cfg.chains)
+    L = max(cfg.log_steps, 1)
+    la = np.zeros((cfg.chains, L))
+    lf = np.zeros((cfg.chains, L), np.uint8)
+    lam, acc = np.zeros(nreg), np.zeros(nreg)
+    n, vis = np.zeros(nreg, np.uint64), np.zeros(nreg, np.uint64)
+    tr = (_CTrace * max(cap_trace, 1))()
+    o = _CMixOut()
+    o.x, o.log_pi, o.log_a = dp(x), dp(lp), dp(la)
+    o.log_f = lf.ctypes.data_as(C.POINTER(C.c_uint8))
+    o.lambda_, o.tally_accept = dp(lam), dp(acc)
+    o.n = n.ctypes.data_as(C.POINTER(C.c_uint64))
+    o.tally_visits = vis.ctypes.data_as(C.POINTER(C.c_uint64))
+    o.cap_regions = nreg
+    o.trace, o.cap_trace = tr, cap_trace
+    err = C.create_string_buffer(1024)
+    rc = fn(C.byref(c), C.byref(o), err, 1024)
+    if rc:
+        raise RenderError(rc, err.value.decode())
+    nt = min(o.n_trace, cap_trace)
+    trace = np.array([[tr[i].mutation_index, tr[i].region, tr[i].n, tr[i].lambda_, tr[i].alpha_hat]
+                      for i in range(nt)], np.float64).reshape(-1, 5)
+    props = cfg.chains * cfg.steps
+    return dict(x=x, log_pi=lp, log_a=la[:, : cfg.log_steps], log_f=lf[:, : cfg.log_steps],
+                lambda_=lam, n=n, tally_accept=acc, tally_visits=vis, trace=trace,
+                accepted=o.accepted, acceptance_sum=o.acceptance_sum,
+                mean_acceptance=o.acceptance_sum / props if props else 0.0)

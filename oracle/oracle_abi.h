@@ -104,6 +104,55 @@ typedef struct oracle_outputs {
     double *film;               /* optional raw fp64 film W*H*3 (restatement only) */
 } oracle_outputs;
 
+
+/* Analytic-target adaptive MCMC (BASELINE.json configs[1]; include/ramlt_mix.h).
+ * The chain loop of core/driver.cpp:113-171 with a Gaussian random-walk
+ * proposal on [0,1]^D and a Gaussian-mixture target; the controller, accept
+ * rule, quantile and RNG are the reference's (oracle_mix_run restates them,
+ * ref_mix_run calls them). */
+typedef struct oracle_mix_config {
+    int32_t strategy;      /* 0 fixed, 1 global, 2 ra-grid over (x0, x1) */
+    int32_t grid_n;
+    int32_t chains;
+    int32_t batch_size;
+    double gamma_max;
+    double gamma_scale;
+    double target_acceptance;
+    double lambda_init;
+    double lambda_min;
+    uint64_t seed;
+    uint64_t steps;        /* lockstep steps per chain */
+    int32_t rng;           /* restatement only: 0 pcg32, 1 philox */
+    int32_t adapt_mode;    /* restatement only: 0 literal, 1 pooled */
+    int64_t chain_offset;
+    int64_t chains_total;
+    uint32_t log_steps;
+    int32_t dim;
+    int32_t n_comp;
+    int32_t pad_;
+    const double *weights;      /* n_comp */
+    const double *means;        /* n_comp * dim */
+    const double *covariances;  /* n_comp * dim * dim */
+} oracle_mix_config;
+
+typedef struct oracle_mix_out {
+    double *x;                  /* chains * dim final states, or NULL */
+    double *log_pi;             /* chains, or NULL */
+    double *log_a;              /* chains * log_steps, or NULL */
+    uint8_t *log_f;             /* chains * log_steps, or NULL */
+    double *lambda;             /* cap_regions */
+    uint64_t *n;
+    double *tally_accept;
+    uint64_t *tally_visits;
+    uint64_t cap_regions;
+    oracle_trace_row *trace;    /* cap_trace */
+    uint64_t cap_trace;
+    uint64_t n_trace;           /* out */
+    uint64_t n_regions;         /* out */
+    uint64_t accepted;          /* out */
+    double acceptance_sum;      /* out */
+} oracle_mix_out;
+
 #ifdef __cplusplus
 }
 #endif

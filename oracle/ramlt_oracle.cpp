@@ -1591,6 +1591,258 @@ struct Render {
     }
 };
 
+
+// ---- analytic-target adaptive MCMC (BASELINE.json configs[1]) -------------------------------
+// Restates the GPU harness (include/ramlt_mix.h): run_chain_span's loop
+// (core/driver.cpp:113-171) with a Gaussian random walk on [0,1]^D and a
+// Gaussian-mixture target.  The target and the proposal have no reference
+// implementation (pinned at the controller / accept boundary);
+// everything else restates the reference: sigma_for (core/adaptation.cpp:44-50),
+// normal_quantile (core/sampling.cpp:20-60), mh_accept (core/mutations.cpp:198-208),
+// the accept draw (core/driver.cpp:168-171), record_acceptance / update_lambda
+// (core/adaptation.cpp:10-20, 60-92), Grid2D::cell_of (core/partition.cpp:16-20),
+// the chain / init streams (core/driver.cpp:20-21, 223-225).
+struct MixTarget {
+    int D = 0, K = 0;
+    std::vector<double> W, mu, ell;   // W_k = L_k^{-1} (Sigma_k = L_k L_k^T), row-major D x D
+};
+
+static MixTarget mix_prepare(int D, int K, const double *w, const double *mu, const double *cov) {
+    MixTarget t;
+    t.D = D;
+    t.K = K;
+    t.W.assign(static_cast<size_t>(K) * D * D, 0.0);
+    t.mu.assign(mu, mu + static_cast<size_t>(K) * D);
+    t.ell.assign(K, 0.0);
+    const double half_log_2pi = 0.5 * std::log(2.0 * 3.14159265358979323846);
+    for (int k = 0; k < K; ++k) {
+        if (!(w[k] > 0.0))
+            throw std::invalid_argument("mix: component weights must be positive and finite");
+        const double *S = cov + static_cast<size_t>(k) * D * D;
+        std::vector<double> L(static_cast<size_t>(D) * D, 0.0);
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j <= i; ++j) {
+                double s = S[i * D + j];
+                for (int q = 0; q < j; ++q)
+                    s = s - L[i * D + q] * L[j * D + q];
+                if (i == j) {
+                    if (!(s > 0.0))
+                        throw std::invalid_argument("mix: covariance is not positive definite");
+                    L[i * D + i] = std::sqrt(s);
+                } else {
+                    L[i * D + j] = s / L[j * D + j];
+                }
+            }
+        double *Wk = t.W.data() + static_cast<size_t>(k) * D * D;
+        for (int j = 0; j < D; ++j) {
+            Wk[j * D + j] = 1.0 / L[j * D + j];
+            for (int i = j + 1; i < D; ++i) {
+                double s = 0.0;
+                for (int q = j; q < i; ++q)
+                    s = s + L[i * D + q] * Wk[q * D + j];
+                Wk[i * D + j] = -s / L[i * D + i];
+            }
+        }
+        double e = std::log(w[k]);
+        for (int i = 0; i < D; ++i)
+            e = e - std::log(L[i * D + i]);
+        t.ell[k] = e - static_cast<double>(D) * half_log_2pi;
+    }
+    return t;
+}
+
+// log pi(x) = logsumexp_k (ell_k - |W_k (x - mu_k)|^2 / 2), fixed summation order.
+static double mix_log_target(const MixTarget &t, const double *x) {
+    const int D = t.D;
+    double e[16];
+    double m = -std::numeric_limits<double>::infinity();
+    for (int k = 0; k < t.K; ++k) {
+        const double *Wk = t.W.data() + static_cast<size_t>(k) * D * D;
+        const double *mk = t.mu.data() + static_cast<size_t>(k) * D;
+        double dif[16];
+        for (int j = 0; j < D; ++j)
+            dif[j] = x[j] - mk[j];
+        double s = 0.0;
+        for (int i = 0; i < D; ++i) {
+            double z = 0.0;
+            for (int j = 0; j <= i; ++j)
+                z = z + Wk[i * D + j] * dif[j];
+            s = s + z * z;
+        }
+        e[k] = t.ell[k] - 0.5 * s;
+        m = e[k] > m ? e[k] : m;
+    }
+    double acc = 0.0;
+    for (int k = 0; k < t.K; ++k)
+        acc = acc + std::exp(e[k] - m);
+    return m + std::log(acc);
+}
+
+struct MixRun {
+    const oracle_mix_config &c;
+    MixTarget t;
+    Adapt ad;
+    int C, D, nreg;
+    long long Ctot, off;
+    std::vector<double> x, lp, asum;
+    std::vector<uint64_t> nacc;
+    std::vector<Rng> rng;
+    std::vector<Region> reg;
+    std::vector<oracle_trace_row> trace;
+    std::vector<double> log_a;
+    std::vector<uint8_t> log_f;
+
+    explicit MixRun(const oracle_mix_config &cfg) : c(cfg) {
+        if (c.chains < 1)
+            throw std::logic_error("need at least one chain");
+        if (c.dim < 1 || c.dim > 16 || c.n_comp < 1 || c.n_comp > 16)
+            throw std::invalid_argument("mix: bad target size");
+        t = mix_prepare(c.dim, c.n_comp, c.weights, c.means, c.covariances);
+        ad.L = c.batch_size;
+        ad.gmax = c.gamma_max;
+        ad.gscale = c.gamma_scale;
+        ad.target = c.target_acceptance;
+        ad.linit = c.lambda_init;
+        ad.lmin = c.lambda_min;
+        C = c.chains;
+        D = c.dim;
+        Ctot = c.chains_total > 0 ? c.chains_total : c.chains;
+        off = c.chain_offset;
+        nreg = c.strategy == 2 ? c.grid_n * c.grid_n : 1;
+        reg.resize(nreg);
+        for (Region &r : reg) {
+            r.lambda = ad.linit;
+            r.n = 1;
+        }
+        x.assign(static_cast<size_t>(C) * D, 0.0);
+        lp.assign(C, 0.0);
+        asum.assign(C, 0.0);
+        nacc.assign(C, 0);
+        rng.resize(C);
+        log_a.assign(static_cast<size_t>(C) * c.log_steps, 0.0);
+        log_f.assign(static_cast<size_t>(C) * c.log_steps, 0);
+        for (int i = 0; i < C; ++i) {
+            uint64_t g = static_cast<uint64_t>(off + i);
+            Rng init;
+            init.kind = c.rng;
+            init.reseed(c.seed, STREAM_INIT + 2 * g);
+            bool ok = false;
+            for (int attempt = 0; attempt < 1000 && !ok; ++attempt) {
+                for (int d = 0; d < D; ++d)
+                    x[static_cast<size_t>(i) * D + d] = init.next_double();
+                lp[i] = mix_log_target(t, &x[static_cast<size_t>(i) * D]);
+                ok = std::isfinite(lp[i]);
+            }
+            if (!ok)
+                throw std::runtime_error("mix: chain initialisation found no state with finite log density");
+            rng[i].kind = c.rng;
+            rng[i].reseed(c.seed, g);
+        }
+    }
+
+    int region_of(const double *xi) const {
+        if (c.strategy != 2)
+            return 0;
+        return grid_cell(c.grid_n, xi[0], xi[1]);
+    }
+
+    void update(Region &r, int rid, double ah, uint64_t index) {
+        uint64_t n0 = r.n;
+        r.lambda = lambda_next(r.lambda, ah, n0, ad);
+        r.n = n0 + 1;
+        trace.push_back({index, rid, n0, r.lambda, ah});
+    }
+
+    void run() {
+        std::vector<int> vr(C);
+        std::vector<double> va(C);
+        std::vector<double> y(D);
+        for (uint64_t j = 0; j < c.steps; ++j) {
+            // every chain proposes with the lambda snapshot of the step start
+            for (int i = 0; i < C; ++i) {
+                double *xi = &x[static_cast<size_t>(i) * D];
+                int r = region_of(xi);
+                double lam = c.strategy == 0 ? ad.linit : reg[r].lambda;
+                double sigma = std::exp(0.5 * lam);
+                bool in = true;
+                for (int d = 0; d < D; ++d) {
+                    double u = rng[i].next_double();
+                    y[d] = xi[d] + sigma * nquantile(u);
+                    in = in && (y[d] >= 0.0 && y[d] <= 1.0);
+                }
+                double a = 0.0, lpy = 0.0;
+                if (in) {
+                    lpy = mix_log_target(t, y.data());
+                    a = mh(1.0, std::exp(lpy - lp[i]), 1.0, 1.0, 1.0, 1.0);
+                }
+                bool acc = a > 0.0 && rng[i].next_double() < a;
+                if (acc) {
+                    for (int d = 0; d < D; ++d)
+                        xi[d] = y[d];
+                    lp[i] = lpy;
+                }
+                asum[i] += a;
+                nacc[i] += acc ? 1 : 0;
+                if (j < c.log_steps) {
+                    log_a[static_cast<size_t>(i) * c.log_steps + j] = a;
+                    log_f[static_cast<size_t>(i) * c.log_steps + j] = static_cast<uint8_t>((acc ? 1 : 0) | 2 | 4);
+                }
+                vr[i] = r;
+                va[i] = a;
+            }
+            if (c.strategy == 0)
+                continue;
+            const uint64_t idx0 = j * static_cast<uint64_t>(Ctot) + static_cast<uint64_t>(off);
+            if (c.adapt_mode == 0) {
+                // literal: record_acceptance in chain order (core/adaptation.cpp:60-92)
+                for (int i = 0; i < C; ++i) {
+                    Region &R = reg[vr[i]];
+                    R.tot_acc += va[i];
+                    R.tot_vis += 1;
+                    R.pend_sum += va[i];
+                    R.pend_n += 1;
+                    if (R.pend_n >= static_cast<uint64_t>(ad.L)) {
+                        double ah = std::clamp(R.pend_sum / static_cast<double>(R.pend_n), 0.0, 1.0);
+                        update(R, vr[i], ah, idx0 + i);
+                        R.pend_sum = 0.0;
+                        R.pend_n = 0;
+                    }
+                }
+            } else {
+                // pooled: one update per region from the step's pooled alpha-hat
+                std::vector<uint64_t> cnt(nreg, 0), fx(nreg, 0), last(nreg, 0);
+                for (int i = 0; i < C; ++i) {
+                    cnt[vr[i]] += 1;
+                    fx[vr[i]] += to_fx(va[i]);
+                    last[vr[i]] = idx0 + i;
+                }
+                const size_t t0 = trace.size();
+                for (int r = 0; r < nreg; ++r) {
+                    if (!cnt[r])
+                        continue;
+                    Region &R = reg[r];
+                    R.tot_vis += cnt[r];
+                    R.tot_fx += fx[r];
+                    R.pend_n += cnt[r];
+                    R.pend_fx += fx[r];
+                    if (R.pend_n < static_cast<uint64_t>(ad.L))
+                        continue;
+                    double ah = static_cast<double>(R.pend_fx) / 16777216.0 / static_cast<double>(R.pend_n);
+                    ah = std::clamp(ah, 0.0, 1.0);
+                    update(R, r, ah, last[r]);
+                    R.pend_n = 0;
+                    R.pend_fx = 0;
+                }
+                // canonical trace order: by the mutation index of the last visit
+                std::stable_sort(trace.begin() + t0, trace.end(),
+                                 [](const oracle_trace_row &p, const oracle_trace_row &q) {
+                                     return p.mutation_index < q.mutation_index;
+                                 });
+            }
+        }
+    }
+};
+
 } // namespace orc
 
 // ---- C ABI -----------------------------------------------------------------------
@@ -1799,6 +2051,58 @@ int orc_camera(const double *cam, int w, int h, double u, double v, double *dir3
         return 0;
     } catch (...) {
         return 3;
+    }
+}
+
+// Analytic-target harness (oracle_abi.h oracle_mix_config): 0 ok, else the
+// ref_render status convention with err = what().
+int oracle_mix_run(const oracle_mix_config *c, oracle_mix_out *o, char *err, int errlen) {
+    try {
+        orc::MixRun m(*c);
+        m.run();
+        const int C = m.C, D = m.D;
+        if (o->x)
+            std::memcpy(o->x, m.x.data(), sizeof(double) * static_cast<size_t>(C) * D);
+        if (o->log_pi)
+            std::memcpy(o->log_pi, m.lp.data(), sizeof(double) * C);
+        if (o->log_a && c->log_steps)
+            std::memcpy(o->log_a, m.log_a.data(), sizeof(double) * m.log_a.size());
+        if (o->log_f && c->log_steps)
+            std::memcpy(o->log_f, m.log_f.data(), m.log_f.size());
+        o->n_regions = static_cast<uint64_t>(m.nreg);
+        for (uint64_t r = 0; r < std::min<uint64_t>(o->cap_regions, m.nreg); ++r) {
+            if (o->lambda)
+                o->lambda[r] = m.reg[r].lambda;
+            if (o->n)
+                o->n[r] = m.reg[r].n;
+            if (o->tally_accept)
+                o->tally_accept[r] = c->adapt_mode == 0 ? m.reg[r].tot_acc
+                                                        : static_cast<double>(m.reg[r].tot_fx) / 16777216.0;
+            if (o->tally_visits)
+                o->tally_visits[r] = m.reg[r].tot_vis;
+        }
+        o->n_trace = m.trace.size();
+        for (uint64_t i = 0; i < std::min<uint64_t>(o->cap_trace, m.trace.size()); ++i)
+            o->trace[i] = m.trace[i];
+        o->accepted = 0;
+        o->acceptance_sum = 0.0;
+        for (int i = 0; i < C; ++i) {
+            o->accepted += m.nacc[i];
+            o->acceptance_sum += m.asum[i];
+        }
+        return 0;
+    } catch (const std::invalid_argument &e) {
+        copy_err(err, errlen, e.what());
+        return 3;
+    } catch (const std::logic_error &e) {
+        copy_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::runtime_error &e) {
+        copy_err(err, errlen, e.what());
+        return 1;
+    } catch (const std::exception &e) {
+        copy_err(err, errlen, e.what());
+        return 4;
     }
 }
 

@@ -33,8 +33,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
+#include <limits>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <stdexcept>
@@ -497,6 +500,218 @@ int ref_quadtree(const double *uv, uint64_t n, uint64_t m_split, int rounds, cha
     std::strncpy(out, s.c_str(), static_cast<size_t>(cap) - 1);
     out[cap - 1] = '\0';
     return splits;
+}
+
+// Analytic-target harness (BASELINE.json configs[1]) composed from the
+// UNMODIFIED reference's own pieces: RandomSequence (core/rng.hpp),
+// normal_quantile (core/sampling.cpp:20-60), mh_accept (core/mutations.cpp:198-208),
+// KernelController::sigma_for / record_acceptance (core/adaptation.cpp:44-92),
+// Grid2D::cell_of (core/partition.cpp:16-20) and the chain / init stream ids
+// (core/driver.cpp:20-21, 223-225), driven in lockstep exactly as
+// run_chain_span drives one step (core/driver.cpp:113-171).  Only the target
+// density and the random-walk proposal are harness code (no reference
+// counterpart exists); they are written out here and in
+// oracle_mix_run independently with the same evaluation order.
+namespace {
+struct RefMixTarget {
+    int D = 0, K = 0;
+    std::vector<double> W, mu, ell;
+};
+
+RefMixTarget ref_mix_prepare(const oracle_mix_config *c) {
+    RefMixTarget t;
+    const int D = c->dim, K = c->n_comp;
+    t.D = D;
+    t.K = K;
+    t.W.assign(static_cast<size_t>(K) * D * D, 0.0);
+    t.mu.assign(c->means, c->means + static_cast<size_t>(K) * D);
+    t.ell.assign(K, 0.0);
+    const double half_log_2pi = 0.5 * std::log(2.0 * 3.14159265358979323846);
+    for (int k = 0; k < K; ++k) {
+        const double *S = c->covariances + static_cast<size_t>(k) * D * D;
+        std::vector<double> L(static_cast<size_t>(D) * D, 0.0);
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j <= i; ++j) {
+                double s = S[i * D + j];
+                for (int q = 0; q < j; ++q)
+                    s = s - L[i * D + q] * L[j * D + q];
+                if (i == j) {
+                    if (!(s > 0.0))
+                        throw std::invalid_argument("mix: covariance is not positive definite");
+                    L[i * D + i] = std::sqrt(s);
+                } else {
+                    L[i * D + j] = s / L[j * D + j];
+                }
+            }
+        double *Wk = t.W.data() + static_cast<size_t>(k) * D * D;
+        for (int j = 0; j < D; ++j) {
+            Wk[j * D + j] = 1.0 / L[j * D + j];
+            for (int i = j + 1; i < D; ++i) {
+                double s = 0.0;
+                for (int q = j; q < i; ++q)
+                    s = s + L[i * D + q] * Wk[q * D + j];
+                Wk[i * D + j] = -s / L[i * D + i];
+            }
+        }
+        double e = std::log(c->weights[k]);
+        for (int i = 0; i < D; ++i)
+            e = e - std::log(L[i * D + i]);
+        t.ell[k] = e - static_cast<double>(D) * half_log_2pi;
+    }
+    return t;
+}
+
+double ref_mix_log_target(const RefMixTarget &t, const double *x) {
+    const int D = t.D;
+    std::vector<double> e(t.K), dif(D);
+    double m = -std::numeric_limits<double>::infinity();
+    for (int k = 0; k < t.K; ++k) {
+        const double *Wk = t.W.data() + static_cast<size_t>(k) * D * D;
+        for (int j = 0; j < D; ++j)
+            dif[j] = x[j] - t.mu[static_cast<size_t>(k) * D + j];
+        double s = 0.0;
+        for (int i = 0; i < D; ++i) {
+            double z = 0.0;
+            for (int j = 0; j <= i; ++j)
+                z = z + Wk[i * D + j] * dif[j];
+            s = s + z * z;
+        }
+        e[k] = t.ell[k] - 0.5 * s;
+        m = e[k] > m ? e[k] : m;
+    }
+    double acc = 0.0;
+    for (int k = 0; k < t.K; ++k)
+        acc = acc + std::exp(e[k] - m);
+    return m + std::log(acc);
+}
+} // namespace
+
+int ref_mix_run(const oracle_mix_config *c, oracle_mix_out *o, char *err, int errlen) {
+    try {
+        if (c->chains < 1)
+            throw std::logic_error("need at least one chain");
+        constexpr uint64_t kStreamInit = 0x4000000000000001ULL;   // core/driver.cpp:21
+        RefMixTarget t = ref_mix_prepare(c);
+        const int C = c->chains, D = c->dim;
+        ramlt::AdaptationConfig ac;
+        ac.batch_size = c->batch_size;
+        ac.gamma_max = c->gamma_max;
+        ac.gamma_scale = c->gamma_scale;
+        ac.target_acceptance = c->target_acceptance;
+        ac.lambda_init = c->lambda_init;
+        ac.lambda_min = c->lambda_min;
+        ramlt::ControllerKind kind = c->strategy == 0   ? ramlt::ControllerKind::Fixed
+                                     : c->strategy == 1 ? ramlt::ControllerKind::Global
+                                                        : ramlt::ControllerKind::Regional;
+        ramlt::KernelController ctl(kind, ac);
+        std::unique_ptr<ramlt::Grid2D> grid;
+        if (c->strategy == 2) {
+            grid = std::make_unique<ramlt::Grid2D>(c->grid_n);
+            for (int r = 0; r < grid->cell_count(); ++r)
+                ctl.allocate_region();
+        }
+        std::vector<double> x(static_cast<size_t>(C) * D), lp(C), asum(C, 0.0);
+        std::vector<uint64_t> nacc(C, 0);
+        std::vector<ramlt::RandomSequence> rng;
+        rng.reserve(C);
+        for (int i = 0; i < C; ++i) {
+            uint64_t g = static_cast<uint64_t>(c->chain_offset + i);
+            ramlt::RandomSequence init(c->seed, kStreamInit + g * 2);
+            bool ok = false;
+            for (int attempt = 0; attempt < 1000 && !ok; ++attempt) {
+                for (int d = 0; d < D; ++d)
+                    x[static_cast<size_t>(i) * D + d] = init.next_double();
+                lp[i] = ref_mix_log_target(t, &x[static_cast<size_t>(i) * D]);
+                ok = std::isfinite(lp[i]);
+            }
+            if (!ok)
+                throw std::runtime_error("mix: chain initialisation found no state with finite log density");
+            rng.emplace_back(c->seed, g);
+        }
+        const uint64_t Ctot = c->chains_total > 0 ? static_cast<uint64_t>(c->chains_total) : C;
+        std::vector<oracle_trace_row> trace;
+        std::vector<ramlt::SigmaPair> sig(C);
+        std::vector<int> reg(C);
+        std::vector<double> y(D);
+        for (uint64_t j = 0; j < c->steps; ++j) {
+            // lockstep: the whole step reads the controller before any record
+            for (int i = 0; i < C; ++i) {
+                const double *xi = &x[static_cast<size_t>(i) * D];
+                reg[i] = grid ? grid->cell_of(ramlt::CanonicalPoint2{xi[0], xi[1]}) : 0;
+                sig[i] = ctl.sigma_for(reg[i]);
+            }
+            for (int i = 0; i < C; ++i) {
+                double *xi = &x[static_cast<size_t>(i) * D];
+                bool in = true;
+                for (int d = 0; d < D; ++d) {
+                    double u = rng[i].next_double();
+                    y[d] = xi[d] + sig[i].primary * ramlt::normal_quantile(u);
+                    in = in && (y[d] >= 0.0 && y[d] <= 1.0);
+                }
+                double a = 0.0, lpy = 0.0;
+                if (in) {
+                    lpy = ref_mix_log_target(t, y.data());
+                    a = ramlt::mh_accept(1.0, std::exp(lpy - lp[i]), 1.0, 1.0, 1.0, 1.0);
+                }
+                if (auto ev = ctl.record_acceptance(reg[i], a))
+                    trace.push_back({j * Ctot + static_cast<uint64_t>(c->chain_offset) + i, ev->region, ev->n,
+                                     ev->lambda, ev->alpha_hat});
+                bool acc = a > 0.0 && rng[i].next_double() < a;
+                if (acc) {
+                    for (int d = 0; d < D; ++d)
+                        xi[d] = y[d];
+                    lp[i] = lpy;
+                }
+                asum[i] += a;
+                nacc[i] += acc ? 1 : 0;
+                if (j < c->log_steps) {
+                    if (o->log_a)
+                        o->log_a[static_cast<size_t>(i) * c->log_steps + j] = a;
+                    if (o->log_f)
+                        o->log_f[static_cast<size_t>(i) * c->log_steps + j] =
+                            static_cast<uint8_t>((acc ? 1 : 0) | 2 | 4);
+                }
+            }
+        }
+        if (o->x)
+            std::memcpy(o->x, x.data(), sizeof(double) * x.size());
+        if (o->log_pi)
+            std::memcpy(o->log_pi, lp.data(), sizeof(double) * C);
+        auto tal = ctl.tallies();
+        o->n_regions = ctl.region_count();
+        for (uint64_t r = 0; r < std::min<uint64_t>(o->cap_regions, ctl.region_count()); ++r) {
+            if (o->lambda)
+                o->lambda[r] = ctl.lambda_of(static_cast<int>(r));
+            if (o->n)
+                o->n[r] = ctl.updates_of(static_cast<int>(r));
+            if (o->tally_accept)
+                o->tally_accept[r] = tal[r].accept_sum;
+            if (o->tally_visits)
+                o->tally_visits[r] = tal[r].visits;
+        }
+        o->n_trace = trace.size();
+        for (uint64_t i = 0; i < std::min<uint64_t>(o->cap_trace, trace.size()); ++i)
+            o->trace[i] = trace[i];
+        o->accepted = 0;
+        o->acceptance_sum = 0.0;
+        for (int i = 0; i < C; ++i) {
+            o->accepted += nacc[i];
+            o->acceptance_sum += asum[i];
+        }
+        return 0;
+    } catch (const std::runtime_error &e) {
+        copy_err(err, errlen, e.what());
+        return 1;
+    } catch (const std::invalid_argument &e) {
+        copy_err(err, errlen, e.what());
+        return 3;
+    } catch (const std::logic_error &e) {
+        copy_err(err, errlen, e.what());
+        return 2;
+    } catch (const std::exception &e) {
+        copy_err(err, errlen, e.what());
+        return 4;
+    }
 }
 
 } // extern "C"

@@ -76,6 +76,33 @@ class ramlt_trace_row(C.Structure):
                 ("lambda_", C.c_double), ("alpha_hat", C.c_double)]
 
 
+class ramlt_mix_target(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n_comp", C.c_int32), ("weights", C.POINTER(C.c_double)),
+                ("means", C.POINTER(C.c_double)), ("covariances", C.POINTER(C.c_double))]
+
+
+class ramlt_mix_desc(C.Structure):
+    _fields_ = [
+        ("strategy", C.c_int32), ("grid_n", C.c_int32), ("chains", C.c_int32),
+        ("batch_size", C.c_int32), ("gamma_max", C.c_double), ("gamma_scale", C.c_double),
+        ("target_acceptance", C.c_double), ("lambda_init", C.c_double),
+        ("lambda_min", C.c_double), ("seed", C.c_uint64), ("precision", C.c_int32),
+        ("rng", C.c_int32), ("adapt_mode", C.c_int32), ("device", C.c_int32),
+        ("chains_total", C.c_int64), ("chain_offset", C.c_int64), ("log_steps", C.c_uint32),
+        ("trace_enabled", C.c_int32), ("trace_capacity", C.c_uint64),
+        ("profile_kernels", C.c_int32), ("cooperative", C.c_int32),
+    ]
+
+
+class ramlt_mix_stats(C.Structure):
+    _fields_ = [
+        ("steps", C.c_uint64), ("proposals", C.c_uint64), ("accepted", C.c_uint64),
+        ("acceptance_sum", C.c_double), ("mean_acceptance", C.c_double),
+        ("region_count", C.c_uint64), ("n_trace", C.c_uint64), ("kernel_launches", C.c_uint64),
+        ("step_kernel_ms", C.c_double), ("step_kernel_launches", C.c_uint64),
+    ]
+
+
 P = C.POINTER
 vp = C.c_void_p
 H = C.c_void_p  # opaque ramlt_gpu*
@@ -118,6 +145,27 @@ SIGNATURES = {
     "ramlt_gpu_refine": (C.c_int, [H, C.c_int32]),
     "ramlt_gpu_last_error": (C.c_char_p, [H]),
     "ramlt_gpu_destroy": (None, [H]),
+    # include/ramlt_mix.h -- analytic-target adaptive MCMC (BASELINE.json configs[1])
+    "ramlt_mix_default_desc": (None, [P(ramlt_mix_desc)]),
+    "ramlt_mix_create": (C.c_int, [P(ramlt_mix_target), P(ramlt_mix_desc), P(H)]),
+    "ramlt_mix_last_create_error": (C.c_char_p, []),
+    "ramlt_mix_last_error": (C.c_char_p, [H]),
+    "ramlt_mix_destroy": (None, [H]),
+    "ramlt_mix_set_stream": (C.c_int, [H, vp]),
+    "ramlt_mix_init_chains": (C.c_int, [H]),
+    "ramlt_mix_run": (C.c_int, [H, C.c_uint64]),
+    "ramlt_mix_synchronize": (C.c_int, [H]),
+    "ramlt_mix_read_stats": (C.c_int, [H, P(ramlt_mix_stats)]),
+    "ramlt_mix_read_state": (C.c_int, [H, P(C.c_double), P(C.c_double)]),
+    "ramlt_mix_read_chain_tallies": (C.c_int, [H, P(C.c_double), P(C.c_uint64)]),
+    "ramlt_mix_read_regions": (C.c_int, [H, P(C.c_double), P(C.c_uint64), P(C.c_double),
+                                         P(C.c_uint64), C.c_uint64, P(C.c_uint64)]),
+    "ramlt_mix_read_trace": (C.c_int, [H, P(ramlt_trace_row), C.c_uint64, P(C.c_uint64)]),
+    "ramlt_mix_read_decisions": (C.c_int, [H, C.c_uint32, P(C.c_double), P(C.c_uint8)]),
+    "ramlt_mix_adapt_exchange": (C.c_int, [H, P(P(C.c_uint64)), P(P(C.c_uint64)),
+                                           P(P(C.c_uint64)), P(C.c_uint64)]),
+    "ramlt_mix_adapt_apply": (C.c_int, [H]),
+    "ramlt_mix_set_external_adaptation": (C.c_int, [H, C.c_int]),
 }
 
 _lib = None

@@ -10,11 +10,11 @@ import pytest
 
 from conftest import ROOT, has_gpu
 
-HEADER = os.path.join(ROOT, "include", "ramlt_gpu.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("ramlt_gpu.h", "ramlt_mix.h")]
 
 
 def declared_symbols():
-    text = open(HEADER).read()
+    text = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"RAMLT_API[^;(]*?\b(ramlt_\w+)\s*\(", text)))
 
 
@@ -50,6 +50,36 @@ def test_struct_layouts_match_header():
                                   _capi.ramlt_material, _capi.ramlt_triangle, _capi.ramlt_sphere,
                                   _capi.ramlt_trace_row)]
     assert sizes == mine
+    src = '#include "ramlt_mix.h"\n#include <stdio.h>\nint main(){printf("%zu %zu %zu",' \
+          'sizeof(ramlt_mix_target),sizeof(ramlt_mix_desc),sizeof(ramlt_mix_stats));}'
+    with tempfile.TemporaryDirectory() as d:
+        open(os.path.join(d, "p.c"), "w").write(src)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), os.path.join(d, "p.c"), "-o",
+                        os.path.join(d, "p")], check=True)
+        sizes = [int(x) for x in subprocess.run([os.path.join(d, "p")], capture_output=True,
+                                                 text=True).stdout.split()]
+    assert sizes == [C.sizeof(t) for t in (_capi.ramlt_mix_target, _capi.ramlt_mix_desc,
+                                           _capi.ramlt_mix_stats)]
+
+
+def test_target_harness_validation_before_device():
+    """ramlt_mix_create validates the target (Cholesky) and the config before
+    touching a device: std::invalid_argument / logic_error as the reference's
+    sampling.cpp:63 / RAMLT_CHECK would raise."""
+    from paper_2402_08273_b200 import LogicError
+    from paper_2402_08273_b200.mix import MixConfig, MixEngine, MixTarget
+    t = MixTarget.config2(0)
+    bad = MixTarget(t.weights, t.means, t.covariances.copy())
+    bad.covariances[2, 0, 0] = -1.0
+    bad.covariances[2] = 0.5 * (bad.covariances[2] + bad.covariances[2].T)
+    with pytest.raises(ValueError, match="positive definite"):
+        MixEngine(bad, MixConfig())
+    with pytest.raises(ValueError, match="weights"):
+        MixEngine(MixTarget(-t.weights, t.means, t.covariances), MixConfig())
+    with pytest.raises(LogicError):
+        MixEngine(t, MixConfig(chains=0))
+    with pytest.raises(LogicError):
+        MixEngine(t, MixConfig(strategy="ra-grid", grid_n=0))
 
 
 def test_default_desc_matches_reference_defaults():
