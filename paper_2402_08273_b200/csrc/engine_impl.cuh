@@ -185,6 +185,12 @@ private:
     DBuf<unsigned> pend_n_, x_touched_, touched_list_, n_touched_;
     DBuf<rd::NodeD> nodes_;
     DBuf<int> roots_, n_nodes_, n_regions_, scratch_cnt_, scratch_list_, splits_;
+    DBuf<int> rf_key_[2], rf_val_[2], rf_count_;   // parallel refine: sort keys / node ids
+    DBuf<unsigned char> rf_tmp_;
+    bool order_morton_ = false;   // RAMLT_CHAIN_ORDER=morton: visit chains in raster Morton order
+    DBuf<unsigned> ord_key_[2], ord_val_[2];
+    DBuf<unsigned char> ord_tmp_;
+    void sort_chains(rd::StepParams<R> &P);
     DBuf<unsigned long long> trace_count_, trace_index_, trace_n_;
     DBuf<long long> trace_region_;
     DBuf<double> trace_lambda_, trace_alpha_;
@@ -420,6 +426,8 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         use_co_ = std::string(v) == "co" || std::string(v) == "co_static";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
     }
+    if (const char *v = std::getenv("RAMLT_CHAIN_ORDER"))
+        order_morton_ = std::string(v) == "morton";
     if (const char *v = std::getenv("RAMLT_CO_PV"))
         co_pv_global_ = std::string(v) != "smem";
     if (const char *v = std::getenv("RAMLT_CO_REFILL"))
@@ -775,6 +783,27 @@ template <class R> void EngineT<R>::init_chains() {
     chains_ready_ = true;
 }
 
+template <class R> void EngineT<R>::sort_chains(rd::StepParams<R> &P) {
+    if (ord_key_[0].n < static_cast<size_t>(C_)) {
+        for (int q = 0; q < 2; ++q) {
+            ord_key_[q].alloc(C_);
+            ord_val_[q].alloc(C_);
+        }
+        size_t tmp = 0;
+        RAMLT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ord_key_[0].p, ord_key_[1].p, ord_val_[0].p,
+                                                   ord_val_[1].p, C_));
+        ord_tmp_.alloc(tmp);
+    }
+    rd::k_chain_keys<R><<<static_cast<unsigned>((C_ + 255) / 256), 256, 0, stream_>>>(cr_.p, C_, ord_key_[0].p,
+                                                                                       ord_val_[0].p);
+    RAMLT_CUDA(cudaGetLastError());
+    size_t tmp = ord_tmp_.n;
+    RAMLT_CUDA(cub::DeviceRadixSort::SortPairs(ord_tmp_.p, tmp, ord_key_[0].p, ord_key_[1].p, ord_val_[0].p,
+                                               ord_val_[1].p, C_, 0, 22, stream_));
+    launches_ += 2;
+    P.order = ord_val_[1].p;
+}
+
 template <class R>
 void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsigned long long per,
                              unsigned long long rem, bool record) {
@@ -788,6 +817,8 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     if (G_ == 1 && use_co_) {
         P.steal = steal_;
         P.refill = refill_;
+        if (order_morton_ && P.steal)
+            sort_chains(P);
         launch_step_co(P);
         return;
     }
@@ -987,11 +1018,36 @@ template <class R> void EngineT<R>::refine() {
     if (need > reg_cap_)
         grow_regions(std::max(need, reg_cap_ * 2));
     rd::RegionArrays ra = regions();
-    rd::k_refine<R><<<1, 1, 0, stream_>>>(nodes_.p, n_nodes_.p, static_cast<int>(reg_cap_ + 4), n_trees_,
-                                          scratch_cnt_.p, scratch_list_.p, ra, ktab_.p, visits_.p,
-                                          n_regions_.p, static_cast<int>(reg_cap_), d_.m_split, err_.p,
-                                          splits_.p);
-    ++launches_;
+    const int n0 = n_nodes_host_;
+    if (rf_key_[0].n < static_cast<size_t>(n0)) {
+        size_t cap = std::max<size_t>(static_cast<size_t>(n0) * 2, 1024);
+        for (int q = 0; q < 2; ++q) {
+            rf_key_[q].alloc(cap);
+            rf_val_[q].alloc(cap);
+        }
+        size_t tmp = 0;
+        RAMLT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, rf_key_[0].p, rf_key_[1].p, rf_val_[0].p,
+                                                   rf_val_[1].p, static_cast<int>(cap)));
+        rf_tmp_.alloc(tmp);
+        rf_count_.alloc(1);
+    }
+    RAMLT_CUDA(cudaMemsetAsync(rf_count_.p, 0, sizeof(int), stream_));
+    const unsigned nb = static_cast<unsigned>((n0 + 255) / 256);
+    rd::k_refine_keys<<<nb, 256, 0, stream_>>>(nodes_.p, n0, n_trees_, visits_.p, d_.m_split, rf_key_[0].p,
+                                                rf_val_[0].p, rf_count_.p);
+    RAMLT_CUDA(cudaGetLastError());
+    int end_bit = 1;
+    while ((1 << end_bit) <= n_trees_)
+        ++end_bit;
+    size_t tmp = rf_tmp_.n;
+    RAMLT_CUDA(cub::DeviceRadixSort::SortPairs(rf_tmp_.p, tmp, rf_key_[0].p, rf_key_[1].p, rf_val_[0].p,
+                                               rf_val_[1].p, n0, 0, end_bit, stream_));
+    rd::k_refine_apply<R><<<nb, 256, 0, stream_>>>(nodes_.p, n0, static_cast<int>(reg_cap_ + 4), rf_val_[1].p,
+                                                   rf_count_.p, ra, ktab_.p, visits_.p, n_regions_.p,
+                                                   static_cast<int>(reg_cap_), err_.p);
+    RAMLT_CUDA(cudaGetLastError());
+    rd::k_refine_finish<<<1, 1, 0, stream_>>>(n0, rf_count_.p, n_nodes_.p, n_regions_.p, splits_.p);
+    launches_ += 4;
     RAMLT_CUDA(cudaGetLastError());
     RAMLT_CUDA(cudaMemcpyAsync(&n_regions_host_, n_regions_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_));
     RAMLT_CUDA(cudaMemcpyAsync(&n_nodes_host_, n_nodes_.p, sizeof(int), cudaMemcpyDeviceToHost, stream_));

@@ -277,6 +277,85 @@ __device__ __forceinline__ double mix_step(const MixP<R> &P, R sigma, MixRegs<R,
     return a;
 }
 
+// Uniform from the two words of one next_double (hi first): Unit<R> without the generator.
+template <class R> __device__ __forceinline__ R mix_unit(uint32_t hi, uint32_t lo);
+template <> __device__ __forceinline__ double mix_unit<double>(uint32_t hi, uint32_t lo) {
+    return static_cast<double>(((static_cast<unsigned long long>(hi) << 32) | lo) >> 11) * 0x1.0p-53;
+}
+template <> __device__ __forceinline__ float mix_unit<float>(uint32_t hi, uint32_t) {
+    return static_cast<float>(hi >> 8) * 0x1.0p-24f;
+}
+
+// mix_step for Philox at D = 8 (configs[1]): a step consumes words
+// [c0, c0 + 16) for the 8 proposal draws and [c0 + 16, c0 + 18) for the accept
+// draw, i.e. at most Philox blocks c0/4 .. c0/4 + 4 (draws come in pairs, so
+// c0 % 4 is 0 or 2).  The five blocks are computed up front as five
+// independent Philox chains (instruction-level parallelism instead of five
+// serial out-of-line refills) and the words are picked from registers.  Same
+// words, same order, same arithmetic as mix_step.
+template <class R, int KT>
+__device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixRegs<R, 8> &cs, Rng<RNG_PHILOX> &rng,
+                                               bool &accepted) {
+    const unsigned long long c0 = rng.draw;
+    const unsigned off = static_cast<unsigned>(c0 & 3ull);
+    if (off & 1u)
+        return mix_step<R, RNG_PHILOX, 8, KT>(P, sigma, cs, rng, accepted);
+    const unsigned long long b = c0 >> 2;
+    const uint32_t k0 = static_cast<uint32_t>(rng.key), k1 = static_cast<uint32_t>(rng.key >> 32);
+    const uint32_t s0 = static_cast<uint32_t>(rng.stream), s1 = static_cast<uint32_t>(rng.stream >> 32);
+    uint32_t w[20];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        uint32_t x0 = static_cast<uint32_t>(b + q), x1 = static_cast<uint32_t>((b + q) >> 32), x2 = s0, x3 = s1;
+        philox10(x0, x1, x2, x3, k0, k1);
+        w[4 * q] = x0;
+        w[4 * q + 1] = x1;
+        w[4 * q + 2] = x2;
+        w[4 * q + 3] = x3;
+    }
+    uint32_t u[18];
+#pragma unroll
+    for (int i = 0; i < 18; ++i)
+        u[i] = off ? w[i + 2] : w[i];
+    R y[8];
+    bool in = true;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+        y[d] = cs.x[d] + sigma * nquantile<R>(mix_unit<R>(u[2 * d], u[2 * d + 1]));
+        in = in && (y[d] >= R(0) && y[d] <= R(1));
+    }
+    double a = 0.0;
+    R lpy = R(0);
+    if (in) {
+        lpy = log_target<R, 8, KT>(P.T, y);
+        R rr = M<R>::exp(lpy - cs.lp);
+        a = rr > R(0) ? (rr < R(1) ? static_cast<double>(rr) : 1.0) : 0.0;
+    }
+    accepted = false;
+    if (a > 0.0 && mix_unit<R>(u[16], u[17]) < static_cast<R>(a)) {
+        accepted = true;
+#pragma unroll
+        for (int d = 0; d < 8; ++d)
+            cs.x[d] = y[d];
+        cs.lp = lpy;
+    }
+    rng.draw = c0 + (a > 0.0 ? 18ull : 16ull);
+    rng.bid = ~0ULL;
+    cs.asum += a;
+    cs.nacc += accepted ? 1u : 0u;
+    return a;
+}
+
+// Dispatch: the batched-draw form where it applies.
+template <class R, int RK, int DT, int KT>
+__device__ __forceinline__ double mix_step_any(const MixP<R> &P, R sigma, MixRegs<R, DT> &cs, Rng<RK> &rng,
+                                               bool &accepted) {
+    if constexpr (RK == RNG_PHILOX && DT == 8)
+        return mix_step_px8<R, KT>(P, sigma, cs, rng, accepted);
+    else
+        return mix_step<R, RK, DT, KT>(P, sigma, cs, rng, accepted);
+}
+
 template <class R>
 __device__ __forceinline__ void mix_log(const MixP<R> &P, int c, unsigned long long j, double a, bool acc) {
     if (j < P.K_log) {
@@ -324,7 +403,7 @@ __global__ void __launch_bounds__(128) k_mix_fixed(MixP<R> P, unsigned long long
         load_chain<R, RK, DT>(P, c, cs, rng);
         for (unsigned long long j = j0; j < j1; ++j) {
             bool acc;
-            double a = mix_step<R, RK, DT, KT>(P, sigma, cs, rng, acc);
+            double a = mix_step_any<R, RK, DT, KT>(P, sigma, cs, rng, acc);
             mix_log(P, c, j, a, acc);
         }
         store_chain<R, RK, DT>(P, c, cs, rng);
@@ -420,7 +499,7 @@ __global__ void __launch_bounds__(128) k_mix_step(MixP<R> P, unsigned long long 
         load_chain<R, RK, DT>(P, c, cs, rng);
         r = mix_region(P, cs);
         bool acc;
-        a = mix_step<R, RK, DT, KT>(P, __ldcg(&P.sig[r]), cs, rng, acc);
+        a = mix_step_any<R, RK, DT, KT>(P, __ldcg(&P.sig[r]), cs, rng, acc);
         mix_log(P, c, j, a, acc);
         store_chain<R, RK, DT>(P, c, cs, rng);
         if (!pooled) {
@@ -474,7 +553,7 @@ __global__ void __launch_bounds__(128) k_mix_coop(MixP<R> P, unsigned long long 
         if (active) {
             r = mix_region(P, cs);
             bool acc;
-            a = mix_step<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
+            a = mix_step_any<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
             mix_log(P, c, j, a, acc);
         }
         const unsigned long long idx0 = j * static_cast<unsigned long long>(P.C_total) + P.off;

@@ -453,9 +453,14 @@ template <class R> struct BvhTrav {
         return sp < SSTACK ? ss[sp * 128] : sl[sp - SSTACK];
     }
 
-    __device__ __forceinline__ bool step(const SceneView<R> &s) {
+    // Node / triangle bases are passed from the kernel parameters (constant
+    // bank) rather than read through a SceneView the register allocator may
+    // have spilled: that reload sat on every node fetch's dependency chain.
+    __device__ __forceinline__ bool step(const SceneView<R> &s) { return step(s.bvh, s.trt, s.nsph); }
+    __device__ __forceinline__ bool step(const BvhNodeD<R> *__restrict__ nodes, const TriT<R> *__restrict__ trt,
+                                         int nsph) {
         while (node >= 0 && node != DONE) {
-            const BvhNodeD<R> n = ld_node(s.bvh + node);
+            const BvhNodeD<R> n = ld_node(nodes + node);
             R t0, t1;
             bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
             bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
@@ -483,11 +488,11 @@ template <class R> struct BvhTrav {
             int code = ~leaf;
             int first = code >> 4, cnt = code & 15;
             for (int k = first; k < first + cnt; ++k) {
-                const TriT<R> tr = ld_trit(s.trt + k);
+                const TriT<R> tr = ld_trit(trt + k);
                 R t;
                 if (!hit_tri_t(tr, o, d, t))
                     continue;
-                int kk = s.nsph + tr.orig;
+                int kk = nsph + tr.orig;
                 if (t < best || (t == best && kk < key)) {
                     best = t;
                     key = kk;

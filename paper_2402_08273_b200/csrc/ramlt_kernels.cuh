@@ -10,7 +10,7 @@
 //   k_bsub      estimate_b substream sums (core/driver.cpp:31-57).
 //   k_adapt_*   shared adaptation statistics (KernelController::record_acceptance,
 //               core/adaptation.cpp:60-92) after each lockstep step.
-//   k_refine    quadtree refinement at barriers (core/partition.cpp:68-100,
+//   k_refine_*  quadtree refinement at barriers (core/partition.cpp:68-100,
 //               217-227; core/adaptation.cpp:34-42).
 #pragma once
 
@@ -19,6 +19,7 @@
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
 
 namespace rd {
 
@@ -113,6 +114,7 @@ template <class R> struct StepParams {
     int ktab_l2;         // region kernel tables change inside this launch (cooperative): read via L2
     int pooled;          // fuse pooled accumulation into the step
     RegionArrays reg;
+    const unsigned *order;   // k_step_co: chain visiting order (nullptr: identity)
 };
 
 // Region kernel tables are rewritten between lockstep steps of one cooperative
@@ -1122,74 +1124,102 @@ __global__ void k_adapt_pool_apply(RegionArrays ra, KernTab<R> *ktab, AdaptCfg c
 
 __global__ void k_reset_touched(unsigned *n_touched) { *n_touched = 0; }
 
-// ---- quadtree refinement (single thread; core/partition.cpp:68-100, 217-227) ---------------------
+// ---- chain visiting order --------------------------------------------------------------------
+// Morton code of the current raster position (2 x 11 bits): sorting the chain
+// ids by it hands each warp chains whose primary rays are neighbours, so their
+// BVH walks share nodes.  Visiting order does not change any result.
+__device__ __forceinline__ unsigned spread11(unsigned v) {
+    v &= 0x7ffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
 template <class R>
-__global__ void k_refine(NodeD *nodes, int *n_nodes, int cap_nodes, int n_trees, int *scratch_cnt,
-                         int *scratch_list, RegionArrays ra, KernTab<R> *ktab,
-                         unsigned long long *visits, int *n_regions, int cap_regions,
-                         unsigned long long m_split, int *err, int *splits_out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0)
+__global__ void k_chain_keys(const R *cr, int C, unsigned *key, unsigned *val) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C)
         return;
-    const int n0 = *n_nodes;
-    for (int t = 0; t < n_trees; ++t)
-        scratch_cnt[t] = 0;
-    // snapshot of candidate leaves, grouped tree-major, node order inside a tree
-    for (int i = 0; i < n0; ++i) {
+    R u = cr[c], v = cr[C + c];
+    unsigned iu = static_cast<unsigned>(min(max(u, R(0)), R(0.99999)) * R(2048));
+    unsigned iv = static_cast<unsigned>(min(max(v, R(0)), R(0.99999)) * R(2048));
+    key[c] = spread11(iu) | (spread11(iv) << 1);
+    val[c] = static_cast<unsigned>(c);
+}
+
+// ---- quadtree refinement (core/partition.cpp:68-100, 217-227; core/adaptation.cpp:34-42) --------
+// Snapshot the leaves, split those with visits >= M_split; children get ids in
+// tree-then-leaf order.  Data-parallel with the exact id order preserved:
+//   k_refine_keys   candidate leaves of the snapshot [0, n0): key = tree, others
+//                   key = n_trees (sorted last); counts the candidates
+//   (host)          cub::DeviceRadixSort::SortPairs (stable LSD) -> candidates in
+//                   tree-major, node-index order = the reference's visiting order
+//   k_refine_apply  split s gets nodes n0 + 4s.. and regions nreg0 + 4s..,
+//                   children LL, LR, UL, UR, lambda copied, n = max(1, n / 4)
+//   k_refine_finish node / region counts
+__global__ void k_refine_keys(const NodeD *nodes, int n0, int n_trees, const unsigned long long *visits,
+                              unsigned long long m_split, int *key, int *val, int *count) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool cand = false;
+    if (i < n0) {
         NodeD nd = nodes[i];
-        if (nd.child < 0 && nd.level < 16 && visits[nd.region] >= m_split)
-            scratch_cnt[nd.tree]++;
+        cand = nd.child < 0 && nd.level < 16 && visits[nd.region] >= m_split;
+        key[i] = cand ? nd.tree : n_trees;
+        val[i] = i;
     }
-    int acc = 0;
-    for (int t = 0; t < n_trees; ++t) {
-        int c = scratch_cnt[t];
-        scratch_cnt[t] = acc;
-        acc += c;
+    unsigned b = __ballot_sync(0xffffffffu, cand);
+    if ((threadIdx.x & 31) == 0 && b)
+        atomicAdd(count, __popc(b));
+}
+
+template <class R>
+__global__ void k_refine_apply(NodeD *nodes, int n0, int cap_nodes, const int *order, const int *count,
+                               RegionArrays ra, KernTab<R> *ktab, unsigned long long *visits, const int *n_regions,
+                               int cap_regions, int *err) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= *count)
+        return;
+    const int nn = n0 + 4 * s, nr = *n_regions + 4 * s;
+    if (nn + 4 > cap_nodes || nr + 4 > cap_regions) {
+        *err = 2;
+        return;
     }
-    for (int i = 0; i < n0; ++i) {
-        NodeD nd = nodes[i];
-        if (nd.child < 0 && nd.level < 16 && visits[nd.region] >= m_split)
-            scratch_list[scratch_cnt[nd.tree]++] = i;
+    int idx = order[s];
+    NodeD nd = nodes[idx];
+    unsigned long long np = ra.n[nd.region];
+    double lam = ra.lambda[nd.region];
+    unsigned long long nc = np / 4 > 1 ? np / 4 : 1;
+    KernTab<R> kt = ktab[nd.region];
+    for (int q = 0; q < 4; ++q) {
+        NodeD ch;
+        ch.level = nd.level + 1;
+        ch.ix = nd.ix * 2 + (q & 1);
+        ch.iy = nd.iy * 2 + (q >> 1);
+        ch.child = -1;
+        ch.tree = nd.tree;
+        ch.region = nr + q;
+        ra.lambda[nr + q] = lam;
+        ra.n[nr + q] = nc;
+        ra.pend_n[nr + q] = 0;
+        ra.pend_sum[nr + q] = 0.0;
+        ra.pend_fx[nr + q] = 0;
+        ra.tot_vis[nr + q] = 0;
+        ra.tot_acc[nr + q] = 0.0;
+        ra.tot_fx[nr + q] = 0;
+        visits[nr + q] = 0;
+        ktab[nr + q] = kt;
+        nodes[nn + q] = ch;
     }
-    int nn = n0, nr = *n_regions, splits = 0;
-    for (int s = 0; s < acc; ++s) {
-        int idx = scratch_list[s];
-        NodeD nd = nodes[idx];
-        if (nn + 4 > cap_nodes || nr + 4 > cap_regions) {
-            *err = 2;
-            break;
-        }
-        unsigned long long np = ra.n[nd.region];
-        double lam = ra.lambda[nd.region];
-        unsigned long long nc = np / 4 > 1 ? np / 4 : 1;
-        for (int q = 0; q < 4; ++q) {
-            NodeD ch;
-            ch.level = nd.level + 1;
-            ch.ix = nd.ix * 2 + (q & 1);
-            ch.iy = nd.iy * 2 + (q >> 1);
-            ch.child = -1;
-            ch.tree = nd.tree;
-            ch.region = nr;
-            ra.lambda[nr] = lam;
-            ra.n[nr] = nc;
-            ra.pend_n[nr] = 0;
-            ra.pend_sum[nr] = 0.0;
-            ra.pend_fx[nr] = 0;
-            ra.tot_vis[nr] = 0;
-            ra.tot_acc[nr] = 0.0;
-            ra.tot_fx[nr] = 0;
-            visits[nr] = 0;
-            ktab[nr] = ktab[nd.region];
-            nodes[nn + q] = ch;
-            ++nr;
-        }
-        nodes[idx].child = nn;
-        visits[nd.region] = 0;
-        nn += 4;
-        ++splits;
-    }
-    *n_nodes = nn;
-    *n_regions = nr;
-    *splits_out = splits;
+    nodes[idx].child = nn;
+    visits[nd.region] = 0;
+}
+
+__global__ void k_refine_finish(int n0, const int *count, int *n_nodes, int *n_regions, int *splits_out) {
+    int m = *count;
+    *n_nodes = n0 + 4 * m;
+    *n_regions += 4 * m;
+    *splits_out = m;
 }
 
 // ---- reductions & film ---------------------------------------------------------------------

@@ -745,7 +745,7 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                     co.attempts = 0;
                     have = true;
                 } else if (mine < static_cast<unsigned>(P.C)) {
-                    co_load(co, P, static_cast<int>(mine));
+                    co_load(co, P, static_cast<int>(P.order ? __ldg(P.order + mine) : mine));
                     const unsigned long long my_steps =
                         P.per + (static_cast<unsigned long long>(co.gc) < P.rem ? 1ull : 0ull);
                     j = P.j0;
@@ -788,7 +788,7 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                 unsigned idle = __ballot_sync(0xffffffffu, !want && (have || !exhausted));
                 if (!busy || __popc(idle) >= P.refill)
                     break;
-                if (want && tv.step(S)) {
+                if (want && tv.step(P.scene.bvh, P.scene.trt, P.scene.nsph)) {
                     co.res_prim = tv.prim(S);
                     co.res_t = tv.best;
                     want = false;

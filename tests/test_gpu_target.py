@@ -23,7 +23,8 @@ pytestmark = pytest.mark.gpu
 
 def gpu_run(target, steps, log_steps=0, **kw):
     from paper_2402_08273_b200.mix import MixConfig, MixEngine
-    eng = MixEngine(target, MixConfig(log_steps=log_steps, trace_enabled=True, **kw))
+    kw.setdefault("trace_enabled", True)
+    eng = MixEngine(target, MixConfig(log_steps=log_steps, **kw))
     eng.init_chains()
     eng.run(steps)
     x, lp = eng.state()
