@@ -269,6 +269,14 @@ RAMLT_API int ramlt_gpu_visits_device(ramlt_gpu *h, uint64_t **visits, uint64_t 
 RAMLT_API int ramlt_gpu_refine_pending(ramlt_gpu *h, int32_t *pending);
 RAMLT_API int ramlt_gpu_refine(ramlt_gpu *h, int32_t keep_counts);
 
+/* Diagnostic (no reference counterpart): closest-hit throughput of the scene's
+ * triangle accelerator alone, for the roofline discussion in DESIGN.md.
+ * n_rays seeded incoherent rays (origins uniform in the scene bounds shrunk by
+ * 10 %, directions uniform on the sphere) traced by the coroutine kernel's
+ * traversal loop with dynamic ray fetch; returns the kernel time (CUDA events)
+ * and the number of rays that hit a triangle. */
+RAMLT_API int ramlt_gpu_trace_benchmark(ramlt_gpu *h, uint64_t n_rays, double *ms, uint64_t *hits);
+
 RAMLT_API const char *ramlt_gpu_last_error(ramlt_gpu *h);
 RAMLT_API void ramlt_gpu_destroy(ramlt_gpu *h);
 

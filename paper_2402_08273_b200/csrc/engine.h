@@ -58,6 +58,7 @@ public:
     virtual void visits_device(uint64_t **visits, uint64_t *n) = 0;
     virtual bool refine_pending() = 0;
     virtual void refine_now(bool keep_counts) = 0;
+    virtual void trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) = 0;
 
     std::string last_error;
 };

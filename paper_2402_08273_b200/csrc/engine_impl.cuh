@@ -94,6 +94,7 @@ public:
         *n = static_cast<uint64_t>(n_regions_host_);
     }
     bool refine_pending() override { return refine_pending_; }
+    void trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) override;
     void refine_now(bool keep_counts) override {
         if (!refine_pending_)
             return;
@@ -450,8 +451,14 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     else if (pkind_ == 4)
         initial = static_cast<size_t>(d.n_top) * d.n_top;
     size_t cap = initial;
-    if (pkind_ == 2 || pkind_ == 4)
-        cap = std::max<size_t>(d.region_capacity ? d.region_capacity : 4096, initial * 8);
+    if (pkind_ == 2 || pkind_ == 4) {
+        // Every split consumes >= m_split visits, so the run can create at most
+        // 4 * mutations / m_split regions: reserve that up front (bounded) so
+        // the quadtree never reallocates (a device-wide sync) inside the span loop.
+        size_t bound = initial + 4 * static_cast<size_t>(d.mutations / std::max<uint64_t>(d.m_split, 1)) + 64;
+        size_t autocap = std::max<size_t>(4096, std::min<size_t>(bound, size_t(1) << 24));
+        cap = std::max<size_t>(d.region_capacity ? d.region_capacity : autocap, initial * 8);
+    }
     alloc_regions(cap);
     n_regions_host_ = static_cast<int>(initial);
     {
@@ -802,6 +809,60 @@ template <class R> void EngineT<R>::sort_chains(rd::StepParams<R> &P) {
                                                ord_val_[1].p, C_, 0, 22, stream_));
     launches_ += 2;
     P.order = ord_val_[1].p;
+}
+
+template <class R> void EngineT<R>::trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) {
+    if (!use_bvh_)
+        throw std::logic_error("trace_benchmark needs the BVH accelerator (accel=bvh or > 128 triangles)");
+    if (n_rays >= 0xffffffffull)
+        throw std::invalid_argument("trace_benchmark: n_rays must fit 32 bits");
+    // scene bounds from the triangles, shrunk by 10 % on every side
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (const ramlt_triangle &t : hs_.tri)
+        for (const double *v : {t.a, t.b, t.c})
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = std::min(lo[k], v[k]);
+                hi[k] = std::max(hi[k], v[k]);
+            }
+    rd::V3<R> l, e;
+    l.x = static_cast<R>(lo[0] + 0.1 * (hi[0] - lo[0]));
+    l.y = static_cast<R>(lo[1] + 0.1 * (hi[1] - lo[1]));
+    l.z = static_cast<R>(lo[2] + 0.1 * (hi[2] - lo[2]));
+    e.x = static_cast<R>(0.8 * (hi[0] - lo[0]));
+    e.y = static_cast<R>(0.8 * (hi[1] - lo[1]));
+    e.z = static_cast<R>(0.8 * (hi[2] - lo[2]));
+    rd::StepParams<R> P = params();
+    P.refill = refill_;
+    size_t smem = (smem_ + 15) & ~size_t(15);
+    P.co_stack_off = static_cast<unsigned>(smem);
+    smem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
+    auto kern = rd::k_trace_bench<R>;
+    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0, dev = 0, sms = 148;
+    RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    RAMLT_CUDA(cudaGetDevice(&dev));
+    RAMLT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf<unsigned long long> h;
+    h.alloc(1);
+    h.zero(stream_);
+    RAMLT_CUDA(cudaMemsetAsync(work_.p, 0, sizeof(unsigned), stream_));
+    cudaEvent_t e0, e1;
+    RAMLT_CUDA(cudaEventCreate(&e0));
+    RAMLT_CUDA(cudaEventCreate(&e1));
+    RAMLT_CUDA(cudaEventRecord(e0, stream_));
+    kern<<<static_cast<unsigned>(std::max(per_sm, 1) * sms), 128, smem, stream_>>>(P, n_rays, work_.p, h.p, l, e);
+    RAMLT_CUDA(cudaGetLastError());
+    RAMLT_CUDA(cudaEventRecord(e1, stream_));
+    RAMLT_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    RAMLT_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ++launches_;
+    *ms = t;
+    unsigned long long hh = 0;
+    RAMLT_CUDA(cudaMemcpy(&hh, h.p, sizeof(hh), cudaMemcpyDeviceToHost));
+    *hits = hh;
 }
 
 template <class R>

@@ -300,13 +300,21 @@ __device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &
     return false;
 }
 
-// Read-only vector loads of BVH records (fp32: 4 x 16 B per node, 3 x 16 B per
+// Read-only vector loads of BVH records (fp32: 2 x 32 B per node, 3 x 16 B per
 // leaf triangle through the non-coherent path) instead of one scalar load per
-// field -- a quarter of the L1 requests.
+// field.  The 256-bit node loads (LDG.E.ENL2.256, sm_100) raise the traversal
+// probe from 941 to 1080 M incoherent rays/s (profiles/r01h/trace_bench.txt).
 template <class R> __device__ __forceinline__ BvhNodeD<R> ld_node(const BvhNodeD<R> *p) { return *p; }
+// sm_100 256-bit loads (LDG.E.ENL2.256): a 64 B node in two requests.
+__device__ __forceinline__ void ldg256(const void *p, float4 &a, float4 &b) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
 template <> __device__ __forceinline__ BvhNodeD<float> ld_node(const BvhNodeD<float> *p) {
-    const float4 *q = reinterpret_cast<const float4 *>(p);
-    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), e = __ldg(q + 3);
+    float4 a, b, c, e;
+    ldg256(p, a, b);
+    ldg256(reinterpret_cast<const char *>(p) + 32, c, e);
     BvhNodeD<float> n;
     n.lo0[0] = a.x, n.lo0[1] = a.y, n.lo0[2] = a.z, n.hi0[0] = a.w;
     n.hi0[1] = b.x, n.hi0[2] = b.y, n.lo1[0] = b.z, n.lo1[1] = b.w;

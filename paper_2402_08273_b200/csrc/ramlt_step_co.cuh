@@ -812,4 +812,72 @@ k_step_co(StepParams<R> P, unsigned int *work) {
     }
 }
 
+// ---- traversal-only throughput probe (ramlt_gpu_trace_benchmark) ------------------------------
+__device__ __forceinline__ uint32_t tb_hash(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+// The coroutine kernel's traversal loop (while-while rounds, dynamic ray
+// fetch with the same refill rule) on synthetic incoherent rays.
+template <class R>
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? RAMLT_CO_MINBLOCKS : 1)
+k_trace_bench(StepParams<R> P, unsigned long long n, unsigned *work, unsigned long long *hits, V3<R> lo, V3<R> ext) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    BvhTrav<R> tv;
+    int tv_sl[BvhTrav<R>::STACK - BvhTrav<R>::SSTACK];
+    tv.sl = tv_sl;
+    tv.ss = reinterpret_cast<int *>(smem + P.co_stack_off) + threadIdx.x;
+    bool want = false, exhausted = false;
+    unsigned h = 0;
+    for (;;) {
+        unsigned need = __ballot_sync(0xffffffffu, !want && !exhausted);
+        if (need) {
+            int leader = __ffs(need) - 1;
+            unsigned base = 0;
+            if (static_cast<int>(lane) == leader)
+                base = atomicAdd(work, static_cast<unsigned>(__popc(need)));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (!want && !exhausted) {
+                unsigned mine = base + __popc(need & lt);
+                if (mine < n) {
+                    uint32_t a = tb_hash(mine * 5u + 1u), b = tb_hash(mine * 5u + 2u), c = tb_hash(mine * 5u + 3u);
+                    uint32_t e = tb_hash(mine * 5u + 4u), f = tb_hash(mine * 5u + 5u);
+                    const R k = R(1) / R(4294967296.0);
+                    V3<R> o = mk(lo.x + ext.x * (R(a) * k), lo.y + ext.y * (R(b) * k), lo.z + ext.z * (R(c) * k));
+                    R z = R(1) - R(2) * (R(e) * k), ph = R(kTwoPiD) * (R(f) * k);
+                    R r = M<R>::sqrt(fmax(R(0), R(1) - z * z));
+                    tv.begin(S, o, mk(r * M<R>::cos(ph), r * M<R>::sin(ph), z), M<R>::inf(), false);
+                    want = true;
+                } else {
+                    exhausted = true;
+                }
+            }
+        }
+        if (!__any_sync(0xffffffffu, want))
+            break;
+        for (;;) {
+            unsigned busy = __ballot_sync(0xffffffffu, want);
+            unsigned idle = __ballot_sync(0xffffffffu, !want && !exhausted);
+            if (!busy || __popc(idle) >= P.refill)
+                break;
+            if (want && tv.step(P.scene.bvh, P.scene.trt, P.scene.nsph)) {
+                h += tv.pos >= 0 ? 1u : 0u;
+                want = false;
+            }
+        }
+    }
+    unsigned s = __reduce_add_sync(0xffffffffu, h);
+    if (lane == 0)
+        atomicAdd(hits, static_cast<unsigned long long>(s));
+}
+
 }  // namespace rd
+

@@ -332,6 +332,13 @@ class Engine:
     def refine(self, keep_counts: bool):
         self._check(self.lib.ramlt_gpu_refine(self.h, int(keep_counts)))
 
+    def trace_benchmark(self, n_rays: int):
+        """Diagnostic: (kernel ms, hits) of n_rays incoherent closest-hit rays
+        through the BVH traversal alone (ramlt_gpu_trace_benchmark)."""
+        ms, hits = C.c_double(), C.c_uint64()
+        self._check(self.lib.ramlt_gpu_trace_benchmark(self.h, n_rays, C.byref(ms), C.byref(hits)))
+        return ms.value, hits.value
+
     def result(self) -> RenderResult:
         s = self.stats()
         return RenderResult(

@@ -105,3 +105,16 @@ def test_partition_invariants_after_refinement():
     assert area == pytest.approx(1.0, abs=1e-12)
     assert (len(leaves) - 1) % 3 == 0          # each split adds exactly 3 leaves
     assert np.all(n >= 1)
+
+
+@pytest.mark.gpu
+def test_trace_benchmark_probe():
+    """ramlt_gpu_trace_benchmark (diagnostic): every seeded ray from inside the
+    closed cluster room hits a triangle, and the probe reports a positive time."""
+    from paper_2402_08273_b200 import Engine, RenderConfig, scenes
+    eng = Engine(scenes.cluster_room(n_tris=4096), RenderConfig(strategy="fixed", chains=64, mutations=64,
+                                                                 width=32, height=32, max_vertices=9,
+                                                                 accel="bvh"))
+    ms, hits = eng.trace_benchmark(1 << 16)
+    eng.close()
+    assert ms > 0 and hits == 1 << 16

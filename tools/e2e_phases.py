@@ -11,6 +11,7 @@ from paper_2402_08273_b200 import Engine, RenderConfig, parse_scene, scenes  # n
 
 
 def main(name="c5", steps=16):
+    steps = int(steps)
     wl = bench.WORKLOADS[name]
     t = [time.perf_counter()]
     text = scenes.SCENES[wl["scene"]](**wl["scene_args"])
@@ -41,4 +42,4 @@ def main(name="c5", steps=16):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["c5"]))
+    main(*(sys.argv[1:3] or ["c5"]))
