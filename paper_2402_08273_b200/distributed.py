@@ -182,3 +182,40 @@ class ShardedRender:
         self.engine.init_chains()
         self.run(self.cfg.mutations)
         return reduce_film(self.engine)
+
+
+class ShardedMix:
+    """The analytic-target harness (configs[1]) over torch.distributed ranks:
+    chains shard by global id (their Philox streams do not depend on the
+    partition); adaptive strategies advance one lockstep step at a time and
+    SUM/SUM/MAX-all-reduce the pooled (count, fixed-point sum, last index)
+    per region before every rank applies the identical update -- the same
+    exchange as ShardedRender, so lambda trajectories equal the single-GPU
+    pooled run bit for bit."""
+
+    def __init__(self, target, cfg):
+        import torch
+        import torch.distributed as dist
+        from .mix import MixEngine
+        self.world = dist.get_world_size()
+        self.rank = dist.get_rank()
+        self.plan = ShardPlan(cfg.chains, self.world, self.rank)
+        local = torch.cuda.current_device()
+        self.cfg = replace(cfg, chains=self.plan.count, chains_total=cfg.chains, chain_offset=self.plan.offset,
+                           device=local, adapt_mode="pooled" if cfg.strategy != "fixed" else cfg.adapt_mode)
+        self.engine = MixEngine(target, self.cfg)
+        self.engine.set_stream(torch.cuda.current_stream().cuda_stream)
+        self.adaptive = cfg.strategy != "fixed"
+        if self.adaptive and self.world > 1:
+            self.engine.set_external_adaptation(True)
+
+    def init_chains(self):
+        self.engine.init_chains()
+
+    def run(self, steps: int):
+        if not self.adaptive or self.world == 1:
+            self.engine.run(steps)
+            return
+        for _ in range(steps):
+            self.engine.run(1)
+            exchange_adaptation(self.engine)

@@ -66,7 +66,11 @@ def test_f64_pcg_matches_reference(name, coop):
                                                   ("global", 64, "literal"), ("ra-grid", 64, "literal"),
                                                   ("fixed", 500, "pooled")])
 @pytest.mark.parametrize("coop", [True, False])
-def test_f64_philox_matches_oracle(strategy, chains, mode, coop):
+@pytest.mark.parametrize("lanes", [2, 1])
+def test_f64_philox_matches_oracle(strategy, chains, mode, coop, lanes, monkeypatch):
+    """D = 8 / K = 4 with Philox takes the two-lanes-per-chain kernels by
+    default (RAMLT_MIX_LANES=1: one lane); both equal the oracle."""
+    monkeypatch.setenv("RAMLT_MIX_LANES", str(lanes))
     from oracle.abi import OracleMixConfig, mix_run
     from paper_2402_08273_b200.mix import MixTarget
     t = MixTarget.config2(5)
@@ -118,6 +122,21 @@ def test_external_exchange_equals_single_handle():
     np.testing.assert_array_equal(tr, a["trace"])
 
 
+@pytest.mark.parametrize("lanes", [2, 1])
+def test_f32_pair_equals_single_lane(lanes, monkeypatch):
+    """fp32 at the configs[1] chain count: the two-lane kernel is bit-identical
+    to the one-lane kernel (same words, same arithmetic)."""
+    from paper_2402_08273_b200.mix import MixTarget
+    t = MixTarget.config2(3)
+    monkeypatch.setenv("RAMLT_MIX_LANES", "1")
+    a = gpu_run(t, 64, strategy="global", chains=65536, seed=2, precision="f32", rng="philox")
+    monkeypatch.setenv("RAMLT_MIX_LANES", str(lanes))
+    b = gpu_run(t, 64, strategy="global", chains=65536, seed=2, precision="f32", rng="philox")
+    np.testing.assert_array_equal(a["x"], b["x"])
+    np.testing.assert_array_equal(a["lambda_"], b["lambda_"])
+    np.testing.assert_array_equal(a["trace"], b["trace"])
+
+
 def test_f32_config2_statistics():
     """configs[1] at full chain count (65,536 chains), fp32 production build,
     1,024 steps: acceptance targets 0.5, lambda agrees with the f64 oracle, and
@@ -154,3 +173,57 @@ def test_generic_dimension_path():
     o = mix_run(t, OracleMixConfig(steps=200, rng="philox", adapt_mode="pooled", **kw))
     gpu = gpu_run(t, 200, precision="f64", rng="philox", adapt_mode="pooled", **kw)
     assert_same(o, gpu)
+
+
+def _sharded_mix_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2402_08273_b200.distributed import ShardedMix
+        from paper_2402_08273_b200.mix import MixConfig, MixTarget
+        torch.cuda.set_device(0)
+        t = MixTarget.config2(2)
+        sm = ShardedMix(t, MixConfig(strategy="ra-grid", grid_n=3, chains=999, seed=8, precision="f64",
+                                     rng="philox", trace_enabled=True))
+        sm.init_chains()
+        sm.run(40)
+        x, _ = sm.engine.state()
+        lam, n, _, _ = sm.engine.regions()
+        q.put((rank, sm.plan.offset, x, lam, n))
+        sm.engine.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_mix_equals_single_handle():
+    """configs[1] over two ranks (gloo, both on cuda:0; host-mediated exchange
+    between steps, no kernel waits on another rank): chains and region lambdas
+    equal the single-handle pooled run."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2402_08273_b200.mix import MixTarget
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_mix_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=300) for _ in range(2)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    t = MixTarget.config2(2)
+    ref = gpu_run(t, 40, strategy="ra-grid", grid_n=3, chains=999, seed=8, precision="f64", rng="philox",
+                  adapt_mode="pooled")
+    x = np.concatenate([o[2] for o in out], axis=0)
+    np.testing.assert_array_equal(x, ref["x"])
+    for o in out:
+        np.testing.assert_array_equal(o[3], ref["lambda_"])
+        np.testing.assert_array_equal(o[4], ref["n"])
