@@ -237,7 +237,8 @@ RAMLT_API int ramlt_gpu_read_tallies(ramlt_gpu *h, double *accept_sum, uint64_t 
 /* Region lambda / update counts (KernelController::lambda_of / updates_of). */
 RAMLT_API int ramlt_gpu_read_regions(ramlt_gpu *h, double *lambda, uint64_t *n, uint64_t cap, uint64_t *count);
 RAMLT_API int ramlt_gpu_read_trace(ramlt_gpu *h, ramlt_trace_row *rows, uint64_t cap, uint64_t *n);
-/* MetricsRow (driver.hpp:52-57): cap rows of (time_s, mutations, rrmse=NaN, mean_acceptance). */
+/* MetricsRow (driver.hpp:52-57): cap rows of (time_s, mutations, rrmse, mean_acceptance);
+ * rrmse is NaN unless a reference image was set (driver.cpp:265-272). */
 RAMLT_API int ramlt_gpu_read_metrics(ramlt_gpu *h, double *rows, uint64_t cap, uint64_t *n);
 /* Per-chain decision log of the first K steps: a[K][chains] and flags
  * (bit0 accepted, bit1 perturbation, bit2 logged), chain-major copy out:
@@ -268,6 +269,12 @@ RAMLT_API int ramlt_gpu_set_exchange_interval(ramlt_gpu *h, uint32_t steps);
 RAMLT_API int ramlt_gpu_visits_device(ramlt_gpu *h, uint64_t **visits, uint64_t *n_regions);
 RAMLT_API int ramlt_gpu_refine_pending(ramlt_gpu *h, int32_t *pending);
 RAMLT_API int ramlt_gpu_refine(ramlt_gpu *h, int32_t keep_counts);
+
+/* RenderConfig::reference (driver.hpp:38): a W*H*3 fp32 image (rows top to
+ * bottom, as read_image) copied to the device; every metrics row then carries
+ * error_report(image, reference, 1e-2, luminance).rrmse (diagnostics.cpp:11-38).
+ * Dimensions must match the render (std::invalid_argument otherwise). */
+RAMLT_API int ramlt_gpu_set_reference(ramlt_gpu *h, const float *rgb, int32_t width, int32_t height);
 
 /* Diagnostic (no reference counterpart): closest-hit throughput of the scene's
  * triangle accelerator alone, for the roofline discussion in DESIGN.md.

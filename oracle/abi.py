@@ -268,9 +268,45 @@ class RefLib(_Lib):
                                  C.POINTER(C.c_double), C.POINTER(C.c_double),
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_parse.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ref_set_reference.restype = None
+        L.ref_set_reference.argtypes = [C.POINTER(C.c_float), C.c_int, C.c_int]
+        L.ref_error_report.restype = C.c_int
+        L.ref_error_report.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int, C.c_int,
+                                       C.c_double, C.c_int, C.POINTER(C.c_double)]
         L.ref_quadtree.restype = C.c_int
         L.ref_quadtree.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_uint64, C.c_int,
                                    C.c_char_p, C.c_int]
+
+
+def ref_set_reference(lib: "RefLib", image):
+    """RenderConfig::reference for the next ref_render calls (None clears)."""
+    if image is None:
+        lib.lib.ref_set_reference(None, 0, 0)
+        return
+    img = np.ascontiguousarray(image, np.float32)
+    lib._ref_keep = img
+    lib.lib.ref_set_reference(img.ctypes.data_as(C.POINTER(C.c_float)), img.shape[1], img.shape[0])
+
+
+def ref_error_report(lib: "RefLib", image, reference, eps: float = 1e-2, rgb: bool = False) -> float:
+    a = np.ascontiguousarray(image, np.float32)
+    b = np.ascontiguousarray(reference, np.float32)
+    out = C.c_double()
+    rc = lib.lib.ref_error_report(a.ctypes.data_as(C.POINTER(C.c_float)), b.ctypes.data_as(C.POINTER(C.c_float)),
+                                  a.shape[1], a.shape[0], eps, int(rgb), C.byref(out))
+    if rc:
+        raise RenderError(rc, "error_report: image dimensions differ")
+    return out.value
+
+
+def np_error_report(image, reference, eps: float = 1e-2) -> float:
+    """error_report(..., rgb=false).rrmse (core/diagnostics.cpp:11-38) in numpy (test checker)."""
+    a = np.asarray(image, np.float32).astype(np.float64).reshape(-1, 3)
+    b = np.asarray(reference, np.float32).astype(np.float64).reshape(-1, 3)
+    la = 0.2126 * a[:, 0] + 0.7152 * a[:, 1] + 0.0722 * a[:, 2]
+    lb = 0.2126 * b[:, 0] + 0.7152 * b[:, 1] + 0.0722 * b[:, 2]
+    e = np.abs(la - lb) / (lb + eps)
+    return float(np.sqrt(np.sum(e * e) / e.size))
 
 
 class OracleLib(_Lib):

@@ -28,6 +28,8 @@
 #include "camera.hpp"
 #include "adaptation.hpp"
 #include "partition.hpp"
+#include "diagnostics.hpp"
+#include "film.hpp"
 
 #include "oracle_abi.h"
 
@@ -233,6 +235,29 @@ int ref_has_log(void) {
 #endif
 }
 
+// RenderConfig::reference for the next ref_render calls (w = 0 clears it).
+ramlt::Image g_reference;
+void ref_set_reference(const float *rgb, int w, int h) {
+    g_reference = ramlt::Image();
+    if (w > 0 && h > 0) {
+        g_reference = ramlt::Image(w, h);
+        std::memcpy(g_reference.data.data(), rgb, sizeof(float) * 3 * static_cast<size_t>(w) * h);
+    }
+}
+
+// error_report (core/diagnostics.cpp:11-38) on two W x H RGB images.
+int ref_error_report(const float *img, const float *ref, int w, int h, double eps, int rgb, double *rrmse) {
+    try {
+        ramlt::Image a(w, h), b(w, h);
+        std::memcpy(a.data.data(), img, sizeof(float) * 3 * static_cast<size_t>(w) * h);
+        std::memcpy(b.data.data(), ref, sizeof(float) * 3 * static_cast<size_t>(w) * h);
+        *rrmse = ramlt::error_report(a, b, eps, rgb != 0).rrmse;
+        return 0;
+    } catch (...) {
+        return 3;
+    }
+}
+
 // run_render through the reference's public API (core/driver.hpp:80).
 // Returns 0 on success; 1 runtime_error, 2 logic_error, 3 invalid_argument,
 // 4 other exception.  err receives e.what().
@@ -242,6 +267,8 @@ int ref_render(const char *scene_text, const oracle_config *c, oracle_stats *st,
         ramlt::SceneModel scene = ramlt::parse_scene(scene_text, "<scene>");
         ramlt::RenderConfig cfg = to_config(c);
         cfg.dump_partition = out && out->dump && out->cap_dump > 0;
+        if (g_reference.width > 0)
+            cfg.reference = &g_reference;   // RenderConfig::reference (driver.hpp:38)
 #ifdef RAMLT_REF_LOG
         for (auto &kv : g_logs)
             delete kv.second;

@@ -143,6 +143,7 @@ SIGNATURES = {
     "ramlt_gpu_visits_device": (C.c_int, [H, P(P(C.c_uint64)), P(C.c_uint64)]),
     "ramlt_gpu_refine_pending": (C.c_int, [H, P(C.c_int32)]),
     "ramlt_gpu_refine": (C.c_int, [H, C.c_int32]),
+    "ramlt_gpu_set_reference": (C.c_int, [H, P(C.c_float), C.c_int32, C.c_int32]),
     "ramlt_gpu_trace_benchmark": (C.c_int, [H, C.c_uint64, P(C.c_double), P(C.c_uint64)]),
     "ramlt_gpu_last_error": (C.c_char_p, [H]),
     "ramlt_gpu_destroy": (None, [H]),

@@ -479,6 +479,9 @@ int ramlt_gpu_set_exchange_interval(ramlt_gpu *h, uint32_t s) { RAMLT_H(h->eng->
 int ramlt_gpu_visits_device(ramlt_gpu *h, uint64_t **v, uint64_t *n) { RAMLT_H(h->eng->visits_device(v, n)); }
 int ramlt_gpu_refine_pending(ramlt_gpu *h, int32_t *p) { RAMLT_H(*p = h->eng->refine_pending() ? 1 : 0); }
 int ramlt_gpu_refine(ramlt_gpu *h, int32_t keep) { RAMLT_H(h->eng->refine_now(keep != 0)); }
+int ramlt_gpu_set_reference(ramlt_gpu *h, const float *rgb, int32_t w, int32_t ht) {
+    RAMLT_H(h->eng->set_reference(rgb, w, ht));
+}
 int ramlt_gpu_trace_benchmark(ramlt_gpu *h, uint64_t n, double *ms, uint64_t *hits) {
     RAMLT_H(h->eng->trace_benchmark(n, ms, hits));
 }

@@ -59,6 +59,7 @@ public:
     virtual bool refine_pending() = 0;
     virtual void refine_now(bool keep_counts) = 0;
     virtual void trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) = 0;
+    virtual void set_reference(const float *rgb, int width, int height) = 0;
 
     std::string last_error;
 };

@@ -95,6 +95,10 @@ public:
     }
     bool refine_pending() override { return refine_pending_; }
     void trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) override;
+    void set_reference(const float *rgb, int width, int height) override;
+    double rrmse_now(uint64_t at);
+    DBuf<float> ref_img_;      // RenderConfig::reference (driver.hpp:38) for the metrics rRMSE
+    DBuf<double> rrmse_part_;
     void refine_now(bool keep_counts) override {
         if (!refine_pending_)
             return;
@@ -1145,8 +1149,38 @@ template <class R> void EngineT<R>::flush_metrics(uint64_t at) {
     double r[6];
     reduce_chains(true, r);
     double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
-    metrics_.push_back({t, static_cast<double>(at), std::numeric_limits<double>::quiet_NaN(),
-                        r[5] > 0 ? r[1] / r[5] : 0.0});
+    // row.rrmse (core/driver.cpp:265-272): NaN unless a reference image is set;
+    // a sharded handle holds a partial film, so its rows stay NaN
+    double rr = (ref_img_.p && Ctot_ == C_) ? rrmse_now(at) : std::numeric_limits<double>::quiet_NaN();
+    metrics_.push_back({t, static_cast<double>(at), rr, r[5] > 0 ? r[1] / r[5] : 0.0});
+}
+
+template <class R> void EngineT<R>::set_reference(const float *rgb, int width, int height) {
+    if (width != d_.width || height != d_.height)
+        throw std::invalid_argument("error_report: image dimensions differ");
+    size_t n = static_cast<size_t>(width) * height * 3;
+    ref_img_.alloc(n);
+    RAMLT_CUDA(cudaMemcpy(ref_img_.p, rgb, n * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+// error_report(to_image(b / at), reference, kDefaultRrmseEpsilon = 1e-2, luminance).rrmse
+template <class R> double EngineT<R>::rrmse_now(uint64_t at) {
+    fold();
+    const int npix = d_.width * d_.height;
+    const unsigned blocks = static_cast<unsigned>((npix + 255) / 256);
+    if (rrmse_part_.n < blocks)
+        rrmse_part_.alloc(blocks);
+    rd::k_rrmse_partial<<<blocks, 256, 0, stream_>>>(film64_.p, ref_img_.p, npix, b_ / static_cast<double>(at),
+                                                      1e-2, rrmse_part_.p);
+    ++launches_;
+    RAMLT_CUDA(cudaGetLastError());
+    std::vector<double> h(blocks);
+    RAMLT_CUDA(cudaMemcpyAsync(h.data(), rrmse_part_.p, blocks * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    RAMLT_CUDA(cudaStreamSynchronize(stream_));
+    double sum = 0.0;
+    for (double v : h)
+        sum += v;
+    return std::sqrt(sum / static_cast<double>(npix));
 }
 
 template <class R> void EngineT<R>::run(uint64_t mutations) {

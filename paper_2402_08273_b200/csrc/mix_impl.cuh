@@ -27,9 +27,6 @@
 //                or region-keyed warp aggregation + apply (RA-grid, literal)
 //   k_mix_step + k_mix_apply_*  the same step from HBM state, one launch per
 //                step (non-resident chain counts, sharded exchange)
-// On the configs[1] fast path (Philox, D = 8) the fixed and cooperative
-// kernels run two lanes per chain (mix_step_g2): each lane draws half of the
-// proposal, doubling the resident warps of the latency-bound 65,536-chain run.
 #pragma once
 
 #include "mix.h"
@@ -39,7 +36,6 @@
 
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -350,81 +346,6 @@ __device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixReg
     return a;
 }
 
-// Two lanes per chain (configs[1] fast path, Philox, D = 8): lane q draws the
-// proposal coordinates 4q .. 4q+3 -- Philox blocks c0/4 + 2q .. + 2q + 2,
-// three independent chains of work -- and the halves are swapped with one
-// shuffle per coordinate; both lanes then evaluate the (constant-bank) target
-// identically and take the accept draw (block c0/4 + 4, held by lane 1) by
-// shuffle.  Same words, order and arithmetic as mix_step: the pair's result is
-// bit-identical to one lane's.  Doubles the resident warps of the 65,536-chain
-// configuration (3.5 -> 7 per scheduler), which is latency-bound.
-template <class R, int KT>
-__device__ __forceinline__ double mix_step_g2(const MixP<R> &P, R sigma, MixRegs<R, 8> &cs, Rng<RNG_PHILOX> &rng,
-                                              int q, bool &accepted) {
-    const unsigned lane = threadIdx.x & 31u;
-    const unsigned pm = 3u << (lane & 30u);
-    const unsigned long long c0 = rng.draw;
-    const unsigned off = static_cast<unsigned>(c0 & 3ull);   // 0 or 2: draws come in pairs
-    const unsigned long long b = (c0 >> 2) + 2ull * static_cast<unsigned>(q);
-    const uint32_t k0 = static_cast<uint32_t>(rng.key), k1 = static_cast<uint32_t>(rng.key >> 32);
-    const uint32_t s0 = static_cast<uint32_t>(rng.stream), s1 = static_cast<uint32_t>(rng.stream >> 32);
-    uint32_t w[12];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        uint32_t x0 = static_cast<uint32_t>(b + t), x1 = static_cast<uint32_t>((b + t) >> 32), x2 = s0, x3 = s1;
-        philox10(x0, x1, x2, x3, k0, k1);
-        w[4 * t] = x0;
-        w[4 * t + 1] = x1;
-        w[4 * t + 2] = x2;
-        w[4 * t + 3] = x3;
-    }
-    R yo[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        uint32_t hi = off ? w[2 * i + 2] : w[2 * i], lo = off ? w[2 * i + 3] : w[2 * i + 1];
-        R xi = q ? cs.x[4 + i] : cs.x[i];
-        yo[i] = xi + sigma * nquantile<R>(mix_unit<R>(hi, lo));
-    }
-    R y[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        R o = __shfl_xor_sync(pm, yo[i], 1);
-        y[i] = q ? o : yo[i];
-        y[4 + i] = q ? yo[i] : o;
-    }
-    R ua = mix_unit<R>(off ? w[10] : w[8], off ? w[11] : w[9]);
-    ua = __shfl_sync(pm, ua, static_cast<int>(lane | 1u));
-    bool in = true;
-#pragma unroll
-    for (int d = 0; d < 8; ++d)
-        in = in && (y[d] >= R(0) && y[d] <= R(1));
-    double a = 0.0;
-    R lpy = R(0);
-    if (in) {
-        lpy = log_target<R, 8, KT>(P.T, y);
-        R rr = M<R>::exp(lpy - cs.lp);
-        a = rr > R(0) ? (rr < R(1) ? static_cast<double>(rr) : 1.0) : 0.0;
-    }
-    accepted = false;
-    if (a > 0.0 && ua < static_cast<R>(a)) {
-        accepted = true;
-#pragma unroll
-        for (int d = 0; d < 8; ++d)
-            cs.x[d] = y[d];
-        cs.lp = lpy;
-    }
-    rng.draw = c0 + (a > 0.0 ? 18ull : 16ull);
-    rng.bid = ~0ULL;
-    cs.asum += a;
-    cs.nacc += accepted ? 1u : 0u;
-    return a;
-}
-
-// G lanes per chain: G = 2 only on the configs[1] fast path.
-template <class R, int RK, int DT, int KT, int G>
-__device__ __forceinline__ double mix_step_lanes(const MixP<R> &P, R sigma, MixRegs<R, DT> &cs, Rng<RK> &rng, int q,
-                                                 bool &accepted);
-
 // Dispatch: the batched-draw form where it applies.
 template <class R, int RK, int DT, int KT>
 __device__ __forceinline__ double mix_step_any(const MixP<R> &P, R sigma, MixRegs<R, DT> &cs, Rng<RK> &rng,
@@ -433,18 +354,6 @@ __device__ __forceinline__ double mix_step_any(const MixP<R> &P, R sigma, MixReg
         return mix_step_px8<R, KT>(P, sigma, cs, rng, accepted);
     else
         return mix_step<R, RK, DT, KT>(P, sigma, cs, rng, accepted);
-}
-
-template <class R, int RK, int DT, int KT, int G>
-__device__ __forceinline__ double mix_step_lanes(const MixP<R> &P, R sigma, MixRegs<R, DT> &cs, Rng<RK> &rng, int q,
-                                                 bool &accepted) {
-    if constexpr (G == 2) {
-        static_assert(RK == RNG_PHILOX && DT == 8, "two lanes per chain: Philox, D = 8");
-        return mix_step_g2<R, KT>(P, sigma, cs, rng, q, accepted);
-    } else {
-        (void)q;
-        return mix_step_any<R, RK, DT, KT>(P, sigma, cs, rng, accepted);
-    }
 }
 
 template <class R>
@@ -485,23 +394,19 @@ __global__ void __launch_bounds__(128) k_mix_init(MixP<R> P) {
 }
 
 // ---- Fixed strategy: no shared state, every step in registers ----------------------------
-template <class R, int RK, int DT, int KT, int G = 1>
+template <class R, int RK, int DT, int KT>
 __global__ void __launch_bounds__(128) k_mix_fixed(MixP<R> P, unsigned long long j0, unsigned long long j1) {
     const R sigma = P.sig[0];
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int q = tid % G;
-    for (int c = tid / G; c < P.C; c += gridDim.x * blockDim.x / G) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < P.C; c += gridDim.x * blockDim.x) {
         MixRegs<R, DT> cs;
         Rng<RK> rng;
         load_chain<R, RK, DT>(P, c, cs, rng);
         for (unsigned long long j = j0; j < j1; ++j) {
             bool acc;
-            double a = mix_step_lanes<R, RK, DT, KT, G>(P, sigma, cs, rng, q, acc);
-            if (q == 0)
-                mix_log(P, c, j, a, acc);
+            double a = mix_step_any<R, RK, DT, KT>(P, sigma, cs, rng, acc);
+            mix_log(P, c, j, a, acc);
         }
-        if (q == 0)
-            store_chain<R, RK, DT>(P, c, cs, rng);
+        store_chain<R, RK, DT>(P, c, cs, rng);
     }
 }
 
@@ -618,22 +523,22 @@ template <class R> __global__ void k_mix_apply_literal(MixP<R> P, unsigned long 
 
 // ---- persistent cooperative kernel (adaptive strategies) -----------------------------------
 // mode 0: Global + pooled -- the region state is replicated in every thread's
-//         registers; per step one block-reduced atomic per block into a
-//         rotating 3-slot buffer and ONE grid barrier; every thread then
-//         applies the identical update (slot j+2 is cleared by thread 0: its
-//         last readers passed barrier j, its next writers wait for barrier j+1).
+//         registers; per step one block-reduced 64-bit atomic per block into a
+//         rotating 3-slot buffer that doubles as the grid barrier (arrival
+//         count in the high bits, no cooperative-groups barrier); every thread
+//         then applies the identical update (slot j+2 is cleared by thread 0:
+//         its last readers arrived at step j, its next writers wait for step j+1).
 // mode 1: pooled, any partition: region-keyed warp aggregation, barrier,
 //         grid-stride apply, barrier.
 // mode 2: literal: per-chain (region, a) to HBM, barrier, canonical-order
 //         sequential apply by one thread, barrier.
-// fp32 pairs: <= 72 registers so the 131,072 threads of configs[1] are co-resident (7 blocks / SM)
-template <class R, int RK, int DT, int KT, int G = 1>
-__global__ void __launch_bounds__(128, (G == 2 && sizeof(R) == 4) ? 7 : 1) k_mix_coop(MixP<R> P, unsigned long long j0, unsigned long long j1, int mode) {
+template <class R, int RK, int DT, int KT>
+__global__ void __launch_bounds__(128) k_mix_coop(MixP<R> P, unsigned long long j0, unsigned long long j1, int mode) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long wsum[4];
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int c = tid / G, q = tid % G;   // G lanes per chain; lane q == 0 owns the chain's outputs
+    __shared__ unsigned long long wtot;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = c < P.C;
     MixRegs<R, DT> cs;
     Rng<RK> rng;
@@ -650,25 +555,34 @@ __global__ void __launch_bounds__(128, (G == 2 && sizeof(R) == 4) ? 7 : 1) k_mix
         if (active) {
             r = mix_region(P, cs);
             bool acc;
-            a = mix_step_lanes<R, RK, DT, KT, G>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, q, acc);
-            if (q == 0)
-                mix_log(P, c, j, a, acc);
+            a = mix_step_any<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
+            mix_log(P, c, j, a, acc);
         }
         const unsigned long long idx0 = j * static_cast<unsigned long long>(P.C_total) + P.off;
         if (mode == 0) {
-            unsigned fx = active && q == 0 ? static_cast<unsigned>(mix_fx(a)) : 0u;
+            // One 64-bit atomic per block is both the data and the barrier
+            // arrival: bits 48.. count arrived blocks, bits 0..47 carry the
+            // fixed-point sum (<= 65,536 chains x 2^24 < 2^41).  Thread 0 spins
+            // until every block arrived, then the block reads the total.
+            unsigned fx = active ? static_cast<unsigned>(mix_fx(a)) : 0u;
             unsigned ws = __reduce_add_sync(0xffffffffu, fx);
             if ((threadIdx.x & 31) == 0)
                 wsum[threadIdx.x >> 5] = ws;
             __syncthreads();
             if (threadIdx.x == 0) {
-                unsigned long long b = 0;
+                unsigned long long b = 1ull << 48;
                 for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
                     b += wsum[w];
-                atomicAdd(&P.gbuf[j % 3], b);
+                unsigned long long v = atomicAdd(&P.gbuf[j % 3], b) + b;
+                const unsigned long long want = static_cast<unsigned long long>(gridDim.x);
+                while ((v >> 48) < want) {
+                    __nanosleep(32);
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&P.gbuf[j % 3]) : "memory");
+                }
+                wtot = v & ((1ull << 48) - 1);
             }
-            grid.sync();
-            unsigned long long fxs = __ldcg(&P.gbuf[j % 3]);
+            __syncthreads();
+            unsigned long long fxs = wtot;
             unsigned long long cnt = static_cast<unsigned long long>(P.C);
             tfx += fxs;
             tvis += cnt;
@@ -683,31 +597,33 @@ __global__ void __launch_bounds__(128, (G == 2 && sizeof(R) == 4) ? 7 : 1) k_mix
                 pn = 0;
                 pf = 0;
                 sigma = static_cast<R>(::exp(0.5 * lam));
-                if (tid == 0 && P.trace)
+                if (c == 0 && P.trace)
                     mix_trace(P, idx0 + P.C - 1, 0, n0, lam, ah);
             }
-            if (tid == 0)
-                P.gbuf[(j + 2) % 3] = 0;
+            if (c == 0) {
+                P.gbuf[(j + 2) % 3] = 0;   // its readers all arrived at step j; next written after step j+1
+                __threadfence();
+            }
         } else if (mode == 1) {
-            mix_accum_pooled(P, q == 0 ? r : -1, a, idx0 + c);
+            mix_accum_pooled(P, r, a, idx0 + c);
             grid.sync();
-            for (int rr = tid; rr < P.nreg; rr += gridDim.x * blockDim.x)
+            for (int rr = c; rr < P.nreg; rr += gridDim.x * blockDim.x)
                 mix_apply_pooled_region(P, rr);
             grid.sync();
         } else {
-            if (active && q == 0) {
+            if (active) {
                 P.vreg[c] = r;
                 P.va[c] = a;
             }
             grid.sync();
-            if (tid == 0)
+            if (c == 0)
                 mix_apply_literal(P, j);
             grid.sync();
         }
     }
-    if (active && q == 0)
+    if (active)
         store_chain<R, RK, DT>(P, c, cs, rng);
-    if (mode == 0 && tid == 0) {
+    if (mode == 0 && c == 0) {
         P.lambda[0] = lam;
         P.n[0] = n;
         P.pend_n[0] = pn;
@@ -807,8 +723,6 @@ private:
     cudaStream_t stream_ = nullptr;
     bool own_stream_ = true;
     int coop_blocks_ = -1;   // resident capacity of k_mix_coop in blocks (-1 unknown)
-    int coop_blocks2_ = 0;   // ... of the two-lanes-per-chain instantiation
-    int lanes_ = 0;          // RAMLT_MIX_LANES: 1 forces one lane per chain
     uint64_t steps_ = 0, launches_ = 0;
     MBuf<R> x_, lp_, sig_;
     MBuf<unsigned long long> rng0_, rng1_;
@@ -842,8 +756,6 @@ MixEngineT<R>::MixEngineT(const MixHostTarget &t, const ramlt_mix_desc &d) : d_(
     if (d.device >= 0)
         RAMLT_MCUDA(cudaSetDevice(d.device));
     RAMLT_MCUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    if (const char *v = std::getenv("RAMLT_MIX_LANES"))
-        lanes_ = std::atoi(v);
     C_ = d.chains;
     D_ = t.D;
     K_ = t.K;
@@ -1040,42 +952,24 @@ void MixEngineT<R>::launch_run(uint64_t steps) {
         }
     };
     unsigned long long j0 = steps_, j1 = steps_ + steps;
-    // two lanes per chain on the configs[1] fast path (RAMLT_MIX_LANES=1 forces one)
-    constexpr bool kPair = RK == rd::RNG_PHILOX && DT == 8;
-    const bool pair = kPair && lanes_ != 1;
-    const int blocks2 = (2 * C_ + threads - 1) / threads;
     if (ctl_ == 0) {
         // Fixed: one launch, grid sized to the chains (no shared state)
         auto e = ev_begin();
-        if constexpr (kPair) {
-            if (pair)
-                rdm::k_mix_fixed<R, RK, DT, KT, 2><<<blocks2, threads, 0, stream_>>>(P, j0, j1);
-            else
-                rdm::k_mix_fixed<R, RK, DT, KT, 1><<<blocks, threads, 0, stream_>>>(P, j0, j1);
-        } else {
-            rdm::k_mix_fixed<R, RK, DT, KT, 1><<<blocks, threads, 0, stream_>>>(P, j0, j1);
-        }
+        rdm::k_mix_fixed<R, RK, DT, KT><<<blocks, threads, 0, stream_>>>(P, j0, j1);
         RAMLT_MCUDA(cudaGetLastError());
         ev_end(e);
         ++launches_;
         return;
     }
-    void *k1 = reinterpret_cast<void *>(rdm::k_mix_coop<R, RK, DT, KT, 1>);
-    void *k2 = k1;
-    if constexpr (kPair)
-        k2 = reinterpret_cast<void *>(rdm::k_mix_coop<R, RK, DT, KT, 2>);
     if (coop_blocks_ < 0) {
-        int dev = 0, nsm = 0, per = 0, per2 = 0, coop = 0;
+        int dev = 0, nsm = 0, per = 0, coop = 0;
         RAMLT_MCUDA(cudaGetDevice(&dev));
         RAMLT_MCUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
         RAMLT_MCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        RAMLT_MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1, threads, 0));
-        RAMLT_MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k2, threads, 0));
+        RAMLT_MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rdm::k_mix_coop<R, RK, DT, KT>, threads, 0));
         coop_blocks_ = coop ? per * nsm : 0;
-        coop_blocks2_ = coop ? per2 * nsm : 0;
     }
-    const bool coop2 = pair && !external_ && d_.cooperative && blocks2 <= coop_blocks2_;
-    const bool coop = coop2 || (!external_ && d_.cooperative && blocks <= coop_blocks_);
+    const bool coop = !external_ && d_.cooperative && blocks <= coop_blocks_;
     if (coop) {
         int mode = adapt_ == 0 ? 2 : (ctl_ == 1 ? 0 : 1);
         const uint64_t chunk = 1024;   // bound one launch's duration
@@ -1083,8 +977,8 @@ void MixEngineT<R>::launch_run(uint64_t steps) {
             unsigned long long b = std::min<unsigned long long>(j1, a + chunk);
             void *args[] = {&P, &a, &b, &mode};
             auto e = ev_begin();
-            RAMLT_MCUDA(cudaLaunchCooperativeKernel(coop2 ? k2 : k1, dim3(coop2 ? blocks2 : blocks), dim3(threads),
-                                                    args, 0, stream_));
+            RAMLT_MCUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(rdm::k_mix_coop<R, RK, DT, KT>),
+                                                    dim3(blocks), dim3(threads), args, 0, stream_));
             ev_end(e);
             ++launches_;
         }

@@ -1270,6 +1270,35 @@ __global__ void k_to_image(const double *film, float *img, int n, double scale) 
         img[i] = static_cast<float>(film[i] * scale);
 }
 
+// error_report(image, reference, eps, rgb = false) (core/diagnostics.cpp:11-38)
+// on the image to_image(scale) would produce: per pixel e = |lum(a) - lum(b)| /
+// (lum(b) + eps) with lum in fp64 of the fp32 pixels; per-block sums of e^2 in
+// a fixed-order tree, finished on the host in block order.
+__global__ void k_rrmse_partial(const double *film, const float *ref, int npix, double scale, double eps,
+                                double *out) {
+    __shared__ double s[256];
+    int i = blockIdx.x * 256 + threadIdx.x;
+    double e2 = 0.0;
+    if (i < npix) {
+        double a0 = static_cast<float>(film[3 * i] * scale), a1 = static_cast<float>(film[3 * i + 1] * scale),
+               a2 = static_cast<float>(film[3 * i + 2] * scale);
+        double b0 = ref[3 * i], b1 = ref[3 * i + 1], b2 = ref[3 * i + 2];
+        double la = 0.2126 * a0 + 0.7152 * a1 + 0.0722 * a2;
+        double lb = 0.2126 * b0 + 0.7152 * b1 + 0.0722 * b2;
+        double e = ::fabs(la - lb) / (lb + eps);
+        e2 = e * e;
+    }
+    s[threadIdx.x] = e2;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (static_cast<int>(threadIdx.x) < w)
+            s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        out[blockIdx.x] = s[0];
+}
+
 }  // namespace rd
 
 // ---- cooperative persistent step kernel (adaptive strategies, small chain counts) ----------

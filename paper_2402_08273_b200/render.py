@@ -332,6 +332,14 @@ class Engine:
     def refine(self, keep_counts: bool):
         self._check(self.lib.ramlt_gpu_refine(self.h, int(keep_counts)))
 
+    def set_reference(self, image: np.ndarray):
+        """RenderConfig::reference (core/driver.hpp:38): metrics rows carry the
+        rRMSE of the running image against it (core/driver.cpp:265-272)."""
+        img = np.ascontiguousarray(image, np.float32)
+        h, w = img.shape[:2]
+        self._ref = img
+        self._check(self.lib.ramlt_gpu_set_reference(self.h, img.ctypes.data_as(C.POINTER(C.c_float)), w, h))
+
     def trace_benchmark(self, n_rays: int):
         """Diagnostic: (kernel ms, hits) of n_rays incoherent closest-hit rays
         through the BVH traversal alone (ramlt_gpu_trace_benchmark)."""
@@ -353,12 +361,16 @@ class Engine:
             kernel_launches=s.kernel_launches)
 
 
-def run_render(scene, cfg: RenderConfig, b: Optional[float] = None) -> RenderResult:
-    """run_render (core/driver.hpp:80): estimate_b, chain init, span loop, reduce."""
+def run_render(scene, cfg: RenderConfig, b: Optional[float] = None,
+               reference: Optional[np.ndarray] = None) -> RenderResult:
+    """run_render (core/driver.hpp:80): estimate_b, chain init, span loop, reduce.
+    ``reference`` is RenderConfig::reference (an (H, W, 3) float32 image)."""
     eng = Engine(scene, cfg)
     try:
         if b is not None:
             eng.set_b(b)
+        if reference is not None:
+            eng.set_reference(reference)
         eng.render()
         return eng.result()
     finally:

@@ -66,11 +66,8 @@ def test_f64_pcg_matches_reference(name, coop):
                                                   ("global", 64, "literal"), ("ra-grid", 64, "literal"),
                                                   ("fixed", 500, "pooled")])
 @pytest.mark.parametrize("coop", [True, False])
-@pytest.mark.parametrize("lanes", [2, 1])
-def test_f64_philox_matches_oracle(strategy, chains, mode, coop, lanes, monkeypatch):
-    """D = 8 / K = 4 with Philox takes the two-lanes-per-chain kernels by
-    default (RAMLT_MIX_LANES=1: one lane); both equal the oracle."""
-    monkeypatch.setenv("RAMLT_MIX_LANES", str(lanes))
+def test_f64_philox_matches_oracle(strategy, chains, mode, coop):
+    """D = 8 / K = 4 with Philox takes the batched-draw step (mix_step_px8)."""
     from oracle.abi import OracleMixConfig, mix_run
     from paper_2402_08273_b200.mix import MixTarget
     t = MixTarget.config2(5)
@@ -120,21 +117,6 @@ def test_external_exchange_equals_single_handle():
     np.testing.assert_array_equal(lam, a["lambda_"])
     np.testing.assert_array_equal(n, a["n"])
     np.testing.assert_array_equal(tr, a["trace"])
-
-
-@pytest.mark.parametrize("lanes", [2, 1])
-def test_f32_pair_equals_single_lane(lanes, monkeypatch):
-    """fp32 at the configs[1] chain count: the two-lane kernel is bit-identical
-    to the one-lane kernel (same words, same arithmetic)."""
-    from paper_2402_08273_b200.mix import MixTarget
-    t = MixTarget.config2(3)
-    monkeypatch.setenv("RAMLT_MIX_LANES", "1")
-    a = gpu_run(t, 64, strategy="global", chains=65536, seed=2, precision="f32", rng="philox")
-    monkeypatch.setenv("RAMLT_MIX_LANES", str(lanes))
-    b = gpu_run(t, 64, strategy="global", chains=65536, seed=2, precision="f32", rng="philox")
-    np.testing.assert_array_equal(a["x"], b["x"])
-    np.testing.assert_array_equal(a["lambda_"], b["lambda_"])
-    np.testing.assert_array_equal(a["trace"], b["trace"])
 
 
 def test_f32_config2_statistics():

@@ -180,3 +180,26 @@ def test_truncated_normal_properties(oracle_lib):
         integral = np.trapezoid(vals, sel[::50])
         assert integral == pytest.approx(1.0, abs=2e-5), sigma
         del pdf
+
+
+def test_rrmse_formula_matches_reference(ref_lib):
+    """The metrics rRMSE (error_report, core/diagnostics.cpp:11-38, luminance,
+    eps 1e-2): numpy checker == the reference's function; and the reference's
+    last metrics row with RenderConfig::reference set equals error_report of
+    its final image."""
+    from oracle.abi import OracleConfig, np_error_report, ref_error_report, ref_set_reference
+    from paper_2402_08273_b200 import scenes
+    rng = np.random.default_rng(3)
+    a = rng.random((16, 24, 3), dtype=np.float32) * 2
+    b = rng.random((16, 24, 3), dtype=np.float32)
+    assert abs(np_error_report(a, b) - ref_error_report(ref_lib, a, b)) <= 1e-14 * ref_error_report(ref_lib, a, b)
+    cfg = OracleConfig(strategy="fixed", perturbation="lens", chains=8, mutations=8 * 40, width=24, height=16,
+                       max_vertices=9, b_samples=4096, seed=5, metrics_interval=8 * 10)
+    ref_set_reference(ref_lib, b)
+    try:
+        o = ref_lib.render(scenes.cornell_box(), cfg)
+    finally:
+        ref_set_reference(ref_lib, None)
+    rr = o.metrics[:, 2]
+    assert len(rr) == 4 and np.all(np.isfinite(rr))
+    assert rr[-1] == ref_error_report(ref_lib, o.image, b)
