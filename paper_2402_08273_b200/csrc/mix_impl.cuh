@@ -36,6 +36,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -533,10 +534,10 @@ template <class R> __global__ void k_mix_apply_literal(MixP<R> P, unsigned long 
 // mode 2: literal: per-chain (region, a) to HBM, barrier, canonical-order
 //         sequential apply by one thread, barrier.
 template <class R, int RK, int DT, int KT>
-__global__ void __launch_bounds__(128) k_mix_coop(MixP<R> P, unsigned long long j0, unsigned long long j1, int mode) {
+__global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long j0, unsigned long long j1, int mode) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
-    __shared__ unsigned long long wsum[4];
+    __shared__ unsigned long long wsum[8];
     __shared__ unsigned long long wtot;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = c < P.C;
@@ -723,6 +724,7 @@ private:
     cudaStream_t stream_ = nullptr;
     bool own_stream_ = true;
     int coop_blocks_ = -1;   // resident capacity of k_mix_coop in blocks (-1 unknown)
+    int coop_threads_ = 256; // RAMLT_MIX_COOP_THREADS: 128 / 256
     uint64_t steps_ = 0, launches_ = 0;
     MBuf<R> x_, lp_, sig_;
     MBuf<unsigned long long> rng0_, rng1_;
@@ -756,6 +758,8 @@ MixEngineT<R>::MixEngineT(const MixHostTarget &t, const ramlt_mix_desc &d) : d_(
     if (d.device >= 0)
         RAMLT_MCUDA(cudaSetDevice(d.device));
     RAMLT_MCUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    if (const char *v = std::getenv("RAMLT_MIX_COOP_THREADS"))
+        coop_threads_ = std::atoi(v) == 128 ? 128 : 256;
     C_ = d.chains;
     D_ = t.D;
     K_ = t.K;
@@ -936,6 +940,10 @@ void MixEngineT<R>::launch_run(uint64_t steps) {
     rdm::MixP<R> P = params();
     const int threads = 128;
     const int blocks = (C_ + threads - 1) / threads;
+    // cooperative kernel: 256-thread blocks halve the barrier arrivals; the
+    // busiest SM holds the same number of chains as with 128-thread blocks
+    const int cthreads = coop_threads_;
+    const int cblocks = (C_ + cthreads - 1) / cthreads;
     auto ev_begin = [&]() -> std::pair<cudaEvent_t, cudaEvent_t> {
         std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
         if (d_.profile_kernels) {
@@ -966,10 +974,10 @@ void MixEngineT<R>::launch_run(uint64_t steps) {
         RAMLT_MCUDA(cudaGetDevice(&dev));
         RAMLT_MCUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
         RAMLT_MCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        RAMLT_MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rdm::k_mix_coop<R, RK, DT, KT>, threads, 0));
+        RAMLT_MCUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rdm::k_mix_coop<R, RK, DT, KT>, cthreads, 0));
         coop_blocks_ = coop ? per * nsm : 0;
     }
-    const bool coop = !external_ && d_.cooperative && blocks <= coop_blocks_;
+    const bool coop = !external_ && d_.cooperative && cblocks <= coop_blocks_;
     if (coop) {
         int mode = adapt_ == 0 ? 2 : (ctl_ == 1 ? 0 : 1);
         const uint64_t chunk = 1024;   // bound one launch's duration
@@ -978,7 +986,7 @@ void MixEngineT<R>::launch_run(uint64_t steps) {
             void *args[] = {&P, &a, &b, &mode};
             auto e = ev_begin();
             RAMLT_MCUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(rdm::k_mix_coop<R, RK, DT, KT>),
-                                                    dim3(blocks), dim3(threads), args, 0, stream_));
+                                                    dim3(cblocks), dim3(cthreads), args, 0, stream_));
             ev_end(e);
             ++launches_;
         }
