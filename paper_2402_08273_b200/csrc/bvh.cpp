@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -59,11 +60,18 @@ struct Builder {
     std::vector<int32_t> &idx;
     std::vector<BvhBuildNode> nodes;
     int leaf_max;
+    int bins = 16;          // RAMLT_BVH_BINS: binned-SAH bins per axis (<= 64)
+    double sah_ct = 0.0;    // RAMLT_BVH_CT > 0: SAH leaf termination, node cost / triangle cost
     int depth = 0;
     int par_depth = -1;                 // >= 0: defer subtrees starting at this depth
     std::vector<Task> *tasks = nullptr;
 
-    Builder(Shared *s, int lm) : sh(s), tb(s->tb), cen(s->cen), idx(s->idx), leaf_max(lm) {}
+    Builder(Shared *s, int lm) : sh(s), tb(s->tb), cen(s->cen), idx(s->idx), leaf_max(lm) {
+        if (const char *v = std::getenv("RAMLT_BVH_BINS"))
+            bins = std::max(4, std::min(64, std::atoi(v)));
+        if (const char *v = std::getenv("RAMLT_BVH_CT"))
+            sah_ct = std::atof(v);
+    }
 
     // Outward padding: a few ulps of the coordinate magnitude plus an absolute
     // floor, so fp32/fp64 slab tests (with their own slack) never cull a hit.
@@ -96,25 +104,26 @@ struct Builder {
         cb.reset();
         for (int i = s; i < e; ++i)
             cb.grow(&cen[3 * idx[i]]);
-        constexpr int B = 16;
+        constexpr int BMAX = 64;
+        const int B = bins;
         double best_cost = std::numeric_limits<double>::infinity();
         int best_axis = -1, best_bin = -1;
         for (int ax = 0; ax < 3; ++ax) {
             double ext = cb.hi[ax] - cb.lo[ax];
             if (!(ext > 0.0))
                 continue;
-            Box bb[B];
-            int cnt[B] = {0};
-            for (auto &b : bb)
-                b.reset();
+            Box bb[BMAX];
+            int cnt[BMAX] = {0};
+            for (int i = 0; i < B; ++i)
+                bb[i].reset();
             for (int i = s; i < e; ++i) {
                 int t = idx[i];
                 int bi = std::min(B - 1, static_cast<int>((cen[3 * t + ax] - cb.lo[ax]) / ext * B));
                 bb[bi].grow(tb[t]);
                 ++cnt[bi];
             }
-            double la[B], ra[B];
-            int lc[B], rc[B];
+            double la[BMAX], ra[BMAX];
+            int lc[BMAX], rc[BMAX];
             Box acc;
             acc.reset();
             int c = 0;
@@ -145,6 +154,13 @@ struct Builder {
         }
         if (best_axis < 0)
             return n <= 15 ? leaf(s, e) : split_median(s, e, d);
+        if (sah_ct > 0.0 && n <= 15) {
+            // SAH termination: a leaf costs n triangle tests, a split
+            // Ct + (A_l n_l + A_r n_r) / A
+            double area = range_box(s, e).area();
+            if (area > 0.0 && static_cast<double>(n) <= sah_ct + best_cost / area)
+                return leaf(s, e);
+        }
         double ext = cb.hi[best_axis] - cb.lo[best_axis];
         auto mid = std::partition(idx.begin() + s, idx.begin() + e, [&](int t) {
             int bi = std::min(B - 1, static_cast<int>((cen[3 * t + best_axis] - cb.lo[best_axis]) / ext * B));

@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long wsum[8];
-    __shared__ unsigned long long wtot;
+    __shared__ R wsig;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = c < P.C;
     MixRegs<R, DT> cs;
@@ -580,31 +580,33 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
                     __nanosleep(32);
                     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&P.gbuf[j % 3]) : "memory");
                 }
-                wtot = v & ((1ull << 48) - 1);
+                // the region update once per block (thread 0 holds the replica)
+                unsigned long long fxs = v & ((1ull << 48) - 1);
+                unsigned long long cnt = static_cast<unsigned long long>(P.C);
+                tfx += fxs;
+                tvis += cnt;
+                pn += cnt;
+                pf += fxs;
+                if (pn >= static_cast<unsigned long long>(P.L)) {
+                    double ah = static_cast<double>(pf) / 16777216.0 / static_cast<double>(pn);
+                    ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
+                    unsigned long long n0 = n;
+                    lam = mix_lambda_next(lam, ah, n0, P.gmax, P.gscale, P.target, P.lmin);
+                    n = n0 + 1;
+                    pn = 0;
+                    pf = 0;
+                    sigma = static_cast<R>(::exp(0.5 * lam));
+                    if (c == 0 && P.trace)
+                        mix_trace(P, idx0 + P.C - 1, 0, n0, lam, ah);
+                }
+                wsig = sigma;
+                if (c == 0) {
+                    P.gbuf[(j + 2) % 3] = 0;   // its readers all arrived at step j; next written after step j+1
+                    __threadfence();
+                }
             }
             __syncthreads();
-            unsigned long long fxs = wtot;
-            unsigned long long cnt = static_cast<unsigned long long>(P.C);
-            tfx += fxs;
-            tvis += cnt;
-            pn += cnt;
-            pf += fxs;
-            if (pn >= static_cast<unsigned long long>(P.L)) {
-                double ah = static_cast<double>(pf) / 16777216.0 / static_cast<double>(pn);
-                ah = ah < 0.0 ? 0.0 : (ah > 1.0 ? 1.0 : ah);
-                unsigned long long n0 = n;
-                lam = mix_lambda_next(lam, ah, n0, P.gmax, P.gscale, P.target, P.lmin);
-                n = n0 + 1;
-                pn = 0;
-                pf = 0;
-                sigma = static_cast<R>(::exp(0.5 * lam));
-                if (c == 0 && P.trace)
-                    mix_trace(P, idx0 + P.C - 1, 0, n0, lam, ah);
-            }
-            if (c == 0) {
-                P.gbuf[(j + 2) % 3] = 0;   // its readers all arrived at step j; next written after step j+1
-                __threadfence();
-            }
+            sigma = wsig;
         } else if (mode == 1) {
             mix_accum_pooled(P, r, a, idx0 + c);
             grid.sync();
