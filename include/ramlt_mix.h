@@ -67,6 +67,8 @@ typedef struct ramlt_mix_desc {
     uint64_t trace_capacity;   /* update-event rows kept on the device */
     int32_t profile_kernels;   /* CUDA events around every step launch */
     int32_t cooperative;       /* 1 (default): persistent cooperative kernel when resident */
+    uint32_t series_steps;     /* record one scalar per chain for the first T steps (0 = off) */
+    int32_t series_dim;        /* -1: log pi(x); d >= 0: coordinate x_d */
 } ramlt_mix_desc;
 
 typedef struct ramlt_mix_stats {
@@ -110,6 +112,16 @@ RAMLT_API int ramlt_mix_read_regions(ramlt_mix *h, double *lambda, uint64_t *n, 
 RAMLT_API int ramlt_mix_read_trace(ramlt_mix *h, ramlt_trace_row *rows, uint64_t cap, uint64_t *n);
 /* First K steps per chain: a[chain*K + step], flags bit0 accepted, bit1 proposal, bit2 logged. */
 RAMLT_API int ramlt_mix_read_decisions(ramlt_mix *h, uint32_t K, double *a, uint8_t *flags);
+
+/* The recorded series, chain-major (chains x series_steps; steps not yet run are 0). */
+RAMLT_API int ramlt_mix_read_series(ramlt_mix *h, double *out);
+/* autocorrelation_time (core/diagnostics.cpp:87-127: Geyer initial positive
+ * sequence, tau >= 1e-3, n_eff = n / tau, sigma2 = tau / n * var) of the
+ * recorded series of chains [first, first + count), on the device.  status[i]
+ * = RAMLT_E_INVALID where the reference throws (fewer than 1000 steps or no
+ * variance), else 0. */
+RAMLT_API int ramlt_mix_autocorrelation(ramlt_mix *h, int32_t first, int32_t count, double *tau,
+                                        double *n_eff, double *sigma2, int32_t *status);
 
 /* Sharded pooled adaptation (as ramlt_gpu_adapt_exchange / _apply): after a
  * run() step the handle holds per-region (count, fixed-point sum, last index)

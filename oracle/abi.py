@@ -273,6 +273,9 @@ class RefLib(_Lib):
         L.ref_error_report.restype = C.c_int
         L.ref_error_report.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int, C.c_int,
                                        C.c_double, C.c_int, C.POINTER(C.c_double)]
+        L.ref_autocorrelation_time.restype = C.c_int
+        L.ref_autocorrelation_time.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.POINTER(C.c_double),
+                                               C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_quadtree.restype = C.c_int
         L.ref_quadtree.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_uint64, C.c_int,
                                    C.c_char_p, C.c_int]
@@ -297,6 +300,40 @@ def ref_error_report(lib: "RefLib", image, reference, eps: float = 1e-2, rgb: bo
     if rc:
         raise RenderError(rc, "error_report: image dimensions differ")
     return out.value
+
+
+def ref_autocorrelation_time(lib: "RefLib", series):
+    """The reference's autocorrelation_time: (tau, n_eff, sigma2), or None where it throws."""
+    x = np.ascontiguousarray(series, np.float64)
+    t, e, s2 = C.c_double(), C.c_double(), C.c_double()
+    rc = lib.lib.ref_autocorrelation_time(x.ctypes.data_as(C.POINTER(C.c_double)), x.size, C.byref(t),
+                                          C.byref(e), C.byref(s2))
+    return None if rc else (t.value, e.value, s2.value)
+
+
+def np_autocorrelation_time(series):
+    """autocorrelation_time (core/diagnostics.cpp:87-127) in numpy (test checker):
+    Geyer's initial positive sequence over rho(k) = sum (x_i - m)(x_{i+k} - m) / (n var)."""
+    x = np.asarray(series, np.float64)
+    n = x.size
+    if n < 1000:
+        return None
+    m = x.mean()
+    var = np.mean((x - m) ** 2)
+    if not var > 0:
+        return None
+    y = x - m
+    tau = -1.0
+    mm = 0
+    while 2 * mm + 1 <= n // 2:
+        k0, k1 = 2 * mm, 2 * mm + 1
+        g = (np.dot(y[: n - k0], y[k0:]) + np.dot(y[: n - k1], y[k1:])) / (n * var)
+        if g <= 0:
+            break
+        tau += 2 * g
+        mm += 1
+    tau = max(tau, 1e-3)
+    return tau, n / tau, tau / n * var
 
 
 def np_error_report(image, reference, eps: float = 1e-2) -> float:

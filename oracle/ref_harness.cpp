@@ -30,6 +30,7 @@
 #include "partition.hpp"
 #include "diagnostics.hpp"
 #include "film.hpp"
+#include "image_io.hpp"
 
 #include "oracle_abi.h"
 
@@ -41,6 +42,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <span>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -242,6 +244,44 @@ void ref_set_reference(const float *rgb, int w, int h) {
     if (w > 0 && h > 0) {
         g_reference = ramlt::Image(w, h);
         std::memcpy(g_reference.data.data(), rgb, sizeof(float) * 3 * static_cast<size_t>(w) * h);
+    }
+}
+
+// autocorrelation_time (core/diagnostics.cpp:87-127) on one series.
+int ref_autocorrelation_time(const double *series, uint64_t n, double *tau, double *n_eff, double *sigma2) {
+    try {
+        ramlt::ChainDiagnostics d = ramlt::autocorrelation_time(std::span<const double>(series, n));
+        *tau = d.tau;
+        *n_eff = d.n_eff;
+        *sigma2 = d.sigma2;
+        return 0;
+    } catch (const std::invalid_argument &) {
+        return 3;
+    }
+}
+
+// write_pfm / read_pfm (core/image_io.cpp:15-56).
+int ref_write_pfm(const float *rgb, int w, int h, const char *path) {
+    try {
+        ramlt::Image img(w, h);
+        std::memcpy(img.data.data(), rgb, sizeof(float) * 3 * static_cast<size_t>(w) * h);
+        ramlt::write_pfm(img, path);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+int ref_read_pfm(const char *path, float *rgb, int cap_pixels, int *w, int *h, char *err, int errlen) {
+    try {
+        ramlt::Image img = ramlt::read_pfm(path);
+        *w = img.width;
+        *h = img.height;
+        if (static_cast<long long>(img.width) * img.height <= cap_pixels)
+            std::memcpy(rgb, img.data.data(), img.data.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception &e) {
+        copy_err(err, errlen, e.what());
+        return 1;
     }
 }
 

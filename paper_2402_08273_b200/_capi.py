@@ -91,6 +91,7 @@ class ramlt_mix_desc(C.Structure):
         ("chains_total", C.c_int64), ("chain_offset", C.c_int64), ("log_steps", C.c_uint32),
         ("trace_enabled", C.c_int32), ("trace_capacity", C.c_uint64),
         ("profile_kernels", C.c_int32), ("cooperative", C.c_int32),
+        ("series_steps", C.c_uint32), ("series_dim", C.c_int32),
     ]
 
 
@@ -164,6 +165,9 @@ SIGNATURES = {
                                          P(C.c_uint64), C.c_uint64, P(C.c_uint64)]),
     "ramlt_mix_read_trace": (C.c_int, [H, P(ramlt_trace_row), C.c_uint64, P(C.c_uint64)]),
     "ramlt_mix_read_decisions": (C.c_int, [H, C.c_uint32, P(C.c_double), P(C.c_uint8)]),
+    "ramlt_mix_read_series": (C.c_int, [H, P(C.c_double)]),
+    "ramlt_mix_autocorrelation": (C.c_int, [H, C.c_int32, C.c_int32, P(C.c_double), P(C.c_double),
+                                            P(C.c_double), P(C.c_int32)]),
     "ramlt_mix_adapt_exchange": (C.c_int, [H, P(P(C.c_uint64)), P(P(C.c_uint64)),
                                            P(P(C.c_uint64)), P(C.c_uint64)]),
     "ramlt_mix_adapt_apply": (C.c_int, [H]),

@@ -60,7 +60,7 @@ struct Builder {
     std::vector<int32_t> &idx;
     std::vector<BvhBuildNode> nodes;
     int leaf_max;
-    int bins = 16;          // RAMLT_BVH_BINS: binned-SAH bins per axis (<= 64)
+    int bins = 32;          // RAMLT_BVH_BINS: binned-SAH bins per axis (<= 64); 32: traversal +4 % over 16
     double sah_ct = 0.0;    // RAMLT_BVH_CT > 0: SAH leaf termination, node cost / triangle cost
     int depth = 0;
     int par_depth = -1;                 // >= 0: defer subtrees starting at this depth

@@ -36,6 +36,9 @@ public:
     virtual uint64_t read_regions(double *lambda, uint64_t *n, double *acc, uint64_t *vis, uint64_t cap) = 0;
     virtual uint64_t read_trace(ramlt_trace_row *rows, uint64_t cap) = 0;
     virtual void read_decisions(uint32_t K, double *a, uint8_t *flags) = 0;
+    virtual void read_series(double *out) = 0;
+    virtual void autocorrelation(int first, int count, double *tau, double *n_eff, double *sigma2,
+                                 int32_t *status) = 0;
     virtual void adapt_exchange(uint64_t **cnt, uint64_t **fx, uint64_t **last, uint64_t *n) = 0;
     virtual void adapt_apply() = 0;
     virtual void set_external(bool on) = 0;

@@ -124,6 +124,8 @@ void ramlt_mix_default_desc(ramlt_mix_desc *d) {
     d->adapt_mode = RAMLT_ADAPT_AUTO;
     d->device = -1;
     d->cooperative = 1;
+    d->series_steps = 0;
+    d->series_dim = -1;
 }
 
 int ramlt_mix_create(const ramlt_mix_target *target, const ramlt_mix_desc *desc, ramlt_mix **out) {
@@ -171,6 +173,11 @@ int ramlt_mix_read_trace(ramlt_mix *h, ramlt_trace_row *rows, uint64_t cap, uint
 }
 int ramlt_mix_read_decisions(ramlt_mix *h, uint32_t K, double *a, uint8_t *f) {
     RAMLT_MH(h->eng->read_decisions(K, a, f));
+}
+int ramlt_mix_read_series(ramlt_mix *h, double *out) { RAMLT_MH(h->eng->read_series(out)); }
+int ramlt_mix_autocorrelation(ramlt_mix *h, int32_t first, int32_t count, double *tau, double *n_eff,
+                              double *sigma2, int32_t *status) {
+    RAMLT_MH(h->eng->autocorrelation(first, count, tau, n_eff, sigma2, status));
 }
 int ramlt_mix_adapt_exchange(ramlt_mix *h, uint64_t **cnt, uint64_t **fx, uint64_t **last, uint64_t *n) {
     RAMLT_MH(h->eng->adapt_exchange(cnt, fx, last, n));

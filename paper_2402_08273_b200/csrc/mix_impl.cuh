@@ -67,6 +67,9 @@ template <class R> struct MixP {
     unsigned long long seed;
     int trace;
     unsigned K_log;
+    unsigned T_series;      // record a scalar per chain for the first T_series steps
+    int series_dim;         // -1: log pi(x), else coordinate x_d
+    double *series;         // [T_series][C], fp64
     // chain SoA
     R *x;                   // [D][C]
     R *lp;                  // [C]
@@ -365,6 +368,20 @@ __device__ __forceinline__ void mix_log(const MixP<R> &P, int c, unsigned long l
     }
 }
 
+// The chain's scalar series for autocorrelation_time (core/diagnostics.cpp:87-127):
+// the state after step j.
+template <class R, int DT>
+__device__ __forceinline__ void mix_record(const MixP<R> &P, int c, unsigned long long j, const MixRegs<R, DT> &cs) {
+    if (j < P.T_series) {
+        R v = cs.lp;
+#pragma unroll
+        for (int d = 0; d < MixRegs<R, DT>::DN; ++d)
+            if (d == P.series_dim)
+                v = cs.x[d];
+        P.series[j * P.C + c] = static_cast<double>(v);
+    }
+}
+
 // ---- initialisation --------------------------------------------------------------------
 template <class R, int RK, int DT, int KT>
 __global__ void __launch_bounds__(128) k_mix_init(MixP<R> P) {
@@ -406,6 +423,7 @@ __global__ void __launch_bounds__(128) k_mix_fixed(MixP<R> P, unsigned long long
             bool acc;
             double a = mix_step_any<R, RK, DT, KT>(P, sigma, cs, rng, acc);
             mix_log(P, c, j, a, acc);
+            mix_record(P, c, j, cs);
         }
         store_chain<R, RK, DT>(P, c, cs, rng);
     }
@@ -502,6 +520,7 @@ __global__ void __launch_bounds__(128) k_mix_step(MixP<R> P, unsigned long long 
         bool acc;
         a = mix_step_any<R, RK, DT, KT>(P, __ldcg(&P.sig[r]), cs, rng, acc);
         mix_log(P, c, j, a, acc);
+        mix_record(P, c, j, cs);
         store_chain<R, RK, DT>(P, c, cs, rng);
         if (!pooled) {
             P.vreg[c] = r;
@@ -558,6 +577,7 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
             bool acc;
             a = mix_step_any<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
             mix_log(P, c, j, a, acc);
+            mix_record(P, c, j, cs);
         }
         const unsigned long long idx0 = j * static_cast<unsigned long long>(P.C_total) + P.off;
         if (mode == 0) {
@@ -637,6 +657,80 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
     }
 }
 
+// ---- autocorrelation_time (core/diagnostics.cpp:87-127) on device -------------------------
+// One block per selected chain: the series (stride C in the [T][C] record) is
+// staged in shared memory, mean / variance / rho(k) are block reductions in a
+// fixed order, and thread 0 runs Geyer's initial positive sequence exactly as
+// the reference (pairs rho(2m) + rho(2m+1) while positive, up to lag n/2).
+// status: 0 ok, 3 series shorter than 1000 or without variance (the reference
+// throws std::invalid_argument).
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (static_cast<int>(threadIdx.x) < w)
+            red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_autocorr(const double *series, int C, int n, int first, double *tau,
+                                                  double *n_eff, double *sigma2, int *status) {
+    extern __shared__ double sm[];   // n series values + 256 reduction slots
+    double *sv = sm, *red = sm + n;
+    const int c = first + blockIdx.x;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        sv[i] = series[static_cast<size_t>(i) * C + c];
+    __syncthreads();
+    double part = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        part += sv[i];
+    const double mean = block_sum(part, red) / static_cast<double>(n);
+    part = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        part += (sv[i] - mean) * (sv[i] - mean);
+    const double var = block_sum(part, red) / static_cast<double>(n);
+    if (n < 1000 || !(var > 0.0)) {
+        if (threadIdx.x == 0) {
+            status[blockIdx.x] = 3;
+            tau[blockIdx.x] = n_eff[blockIdx.x] = sigma2[blockIdx.x] = 0.0;
+        }
+        return;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        sv[i] -= mean;
+    __syncthreads();
+    double t = -1.0;
+    const int max_lag = n / 2;
+    for (int m = 0;; ++m) {
+        const int k0 = 2 * m, k1 = 2 * m + 1;
+        if (k1 > max_lag)
+            break;
+        double p0 = 0.0, p1 = 0.0;
+        for (int i = threadIdx.x; i + k0 < n; i += blockDim.x) {
+            p0 += sv[i] * sv[i + k0];
+            if (i + k1 < n)
+                p1 += sv[i] * sv[i + k1];
+        }
+        const double r0 = block_sum(p0, red) / (static_cast<double>(n) * var);
+        const double r1 = block_sum(p1, red) / (static_cast<double>(n) * var);
+        const double gamma = r0 + r1;
+        if (gamma <= 0.0)
+            break;
+        t += 2.0 * gamma;
+    }
+    t = t > 1e-3 ? t : 1e-3;
+    if (threadIdx.x == 0) {
+        status[blockIdx.x] = 0;
+        tau[blockIdx.x] = t;
+        n_eff[blockIdx.x] = static_cast<double>(n) / t;
+        sigma2[blockIdx.x] = t / static_cast<double>(n) * var;
+    }
+}
+
 }  // namespace rdm
 
 namespace ramlt_b200 {
@@ -695,6 +789,8 @@ public:
     uint64_t read_regions(double *lambda, uint64_t *n, double *acc, uint64_t *vis, uint64_t cap) override;
     uint64_t read_trace(ramlt_trace_row *rows, uint64_t cap) override;
     void read_decisions(uint32_t K, double *a, uint8_t *flags) override;
+    void read_series(double *out) override;
+    void autocorrelation(int first, int count, double *tau, double *n_eff, double *sigma2, int32_t *status) override;
     void adapt_exchange(uint64_t **cnt, uint64_t **fx, uint64_t **last, uint64_t *n) override {
         *cnt = reinterpret_cast<uint64_t *>(x_cnt_.p);
         *fx = reinterpret_cast<uint64_t *>(x_fx_.p);
@@ -734,6 +830,7 @@ private:
     MBuf<unsigned> nacc_;
     MBuf<double> log_a_;
     MBuf<unsigned char> log_f_;
+    MBuf<double> series_;
     MBuf<int> vreg_, err_;
     MBuf<double> va_, lambda_, pend_sum_, tot_acc_;
     MBuf<unsigned long long> n_, pend_n_, pend_fx_, tot_fx_, tot_vis_, x_cnt_, x_fx_, x_last_, gbuf_;
@@ -797,6 +894,10 @@ MixEngineT<R>::MixEngineT(const MixHostTarget &t, const ramlt_mix_desc &d) : d_(
     vreg_.alloc(C_);
     va_.alloc(C_);
     err_.alloc(1);
+    if (d.series_dim < -1 || d.series_dim >= t.D)
+        throw std::invalid_argument("mix: series_dim must be -1 (log pi) or a coordinate index");
+    if (d.series_steps)
+        series_.alloc(static_cast<size_t>(d.series_steps) * C_);
     if (d.log_steps) {
         log_a_.alloc(static_cast<size_t>(d.log_steps) * C_);
         log_f_.alloc(static_cast<size_t>(d.log_steps) * C_);
@@ -861,6 +962,9 @@ template <class R> rdm::MixP<R> MixEngineT<R>::params() const {
     P.seed = d_.seed;
     P.trace = d_.trace_enabled;
     P.K_log = d_.log_steps;
+    P.T_series = d_.series_steps;
+    P.series_dim = d_.series_dim;
+    P.series = series_.p;
     P.x = x_.p;
     P.lp = lp_.p;
     P.rng0 = rng0_.p;
@@ -1162,6 +1266,45 @@ template <class R> void MixEngineT<R>::read_decisions(uint32_t K, double *a, uin
             a[static_cast<size_t>(c) * K + j] = have ? la[static_cast<size_t>(j) * C_ + c] : 0.0;
             flags[static_cast<size_t>(c) * K + j] = have ? lf[static_cast<size_t>(j) * C_ + c] : 0;
         }
+}
+
+template <class R> void MixEngineT<R>::read_series(double *out) {
+    synchronize();
+    const uint64_t T = std::min<uint64_t>(steps_, d_.series_steps);
+    std::vector<double> h(static_cast<size_t>(d_.series_steps) * C_);
+    if (!h.empty())
+        series_.down(h.data(), h.size());
+    for (int c = 0; c < C_; ++c)
+        for (uint64_t j = 0; j < d_.series_steps; ++j)
+            out[static_cast<size_t>(c) * d_.series_steps + j] = j < T ? h[j * C_ + c] : 0.0;
+}
+
+template <class R>
+void MixEngineT<R>::autocorrelation(int first, int count, double *tau, double *n_eff, double *sigma2,
+                                    int32_t *status) {
+    if (first < 0 || count < 0 || first + count > C_)
+        throw std::logic_error("mix: autocorrelation chain range outside the handle");
+    const uint64_t n = std::min<uint64_t>(steps_, d_.series_steps);
+    if (count == 0)
+        return;
+    size_t smem = (static_cast<size_t>(n) + 256) * sizeof(double);
+    if (smem > 227 * 1024)
+        throw std::invalid_argument("mix: series too long for the on-chip autocorrelation (<= 28,800 steps)");
+    MBuf<double> t, e, s2;
+    MBuf<int> st;
+    t.alloc(count);
+    e.alloc(count);
+    s2.alloc(count);
+    st.alloc(count);
+    RAMLT_MCUDA(cudaFuncSetAttribute(rdm::k_autocorr, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    rdm::k_autocorr<<<count, 256, smem, stream_>>>(series_.p, C_, static_cast<int>(n), first, t.p, e.p, s2.p, st.p);
+    RAMLT_MCUDA(cudaGetLastError());
+    ++launches_;
+    synchronize();
+    t.down(tau, count);
+    e.down(n_eff, count);
+    s2.down(sigma2, count);
+    st.down(status, count);
 }
 
 }  // namespace ramlt_b200

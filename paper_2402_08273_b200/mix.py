@@ -110,6 +110,8 @@ class MixConfig:
     trace_capacity: int = 0
     profile_kernels: bool = False
     cooperative: bool = True
+    series_steps: int = 0         # record a scalar per chain for autocorrelation_time
+    series_dim: int = -1          # -1: log pi(x), d: coordinate x_d
 
     def to_c(self) -> _capi.ramlt_mix_desc:
         d = _capi.ramlt_mix_desc()
@@ -215,6 +217,23 @@ class MixEngine:
         self._check(self.lib.ramlt_mix_read_decisions(
             self.h, K, a.ctypes.data_as(C.POINTER(C.c_double)), f.ctypes.data_as(C.POINTER(C.c_uint8))))
         return a, f
+
+    def series(self) -> np.ndarray:
+        out = np.zeros((self.cfg.chains, self.cfg.series_steps), np.float64)
+        self._check(self.lib.ramlt_mix_read_series(self.h, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def autocorrelation(self, first: int = 0, count: int | None = None):
+        """autocorrelation_time (core/diagnostics.cpp:87-127) of the recorded
+        series of chains [first, first + count): (tau, n_eff, sigma2, status)."""
+        count = self.cfg.chains - first if count is None else count
+        tau, neff, s2 = np.zeros(count), np.zeros(count), np.zeros(count)
+        st = np.zeros(count, np.int32)
+        dp = C.POINTER(C.c_double)
+        self._check(self.lib.ramlt_mix_autocorrelation(self.h, first, count, tau.ctypes.data_as(dp),
+                                                       neff.ctypes.data_as(dp), s2.ctypes.data_as(dp),
+                                                       st.ctypes.data_as(C.POINTER(C.c_int32))))
+        return tau, neff, s2, st
 
     # --- sharded pooled adaptation ---------------------------------------------------
     def set_external_adaptation(self, on: bool):

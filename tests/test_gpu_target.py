@@ -209,3 +209,30 @@ def test_sharded_mix_equals_single_handle():
     for o in out:
         np.testing.assert_array_equal(o[3], ref["lambda_"])
         np.testing.assert_array_equal(o[4], ref["n"])
+
+
+def test_autocorrelation_on_device():
+    """Device autocorrelation_time of recorded chain series equals the checker
+    (pinned to the reference's function) on the same series; series shorter
+    than 1,000 steps report the reference's invalid_argument status."""
+    from oracle.abi import np_autocorrelation_time
+    from paper_2402_08273_b200.mix import MixConfig, MixEngine, MixTarget
+    t = MixTarget.config2(0)
+    for dim in (-1, 0):
+        eng = MixEngine(t, MixConfig(strategy="global", chains=4096, seed=3, precision="f32", rng="philox",
+                                     series_steps=3000, series_dim=dim))
+        eng.init_chains()
+        eng.run(500)
+        _, _, _, st = eng.autocorrelation(0, 8)
+        assert np.all(st == 3)
+        eng.run(2500)
+        tau, neff, s2, st = eng.autocorrelation(100, 64)
+        ser = eng.series()
+        eng.close()
+        for i in range(64):
+            r = np_autocorrelation_time(ser[100 + i])
+            if r is None:
+                assert st[i] == 3
+                continue
+            assert st[i] == 0
+            np.testing.assert_allclose([tau[i], neff[i], s2[i]], r, rtol=1e-9)

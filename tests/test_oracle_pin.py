@@ -203,3 +203,38 @@ def test_rrmse_formula_matches_reference(ref_lib):
     rr = o.metrics[:, 2]
     assert len(rr) == 4 and np.all(np.isfinite(rr))
     assert rr[-1] == ref_error_report(ref_lib, o.image, b)
+
+
+def test_pfm_io_matches_reference(ref_lib, tmp_path):
+    """paper_2402_08273_b200.image_io mirrors write_pfm / read_pfm
+    (core/image_io.cpp:15-56): byte-identical files, each reads the other's,
+    big-endian input, and the reference's error messages."""
+    import ctypes as C
+    from paper_2402_08273_b200.image_io import read_pfm, write_pfm
+    L = ref_lib.lib
+    L.ref_write_pfm.argtypes = [C.POINTER(C.c_float), C.c_int, C.c_int, C.c_char_p]
+    L.ref_read_pfm.argtypes = [C.c_char_p, C.POINTER(C.c_float), C.c_int, C.POINTER(C.c_int),
+                               C.POINTER(C.c_int), C.c_char_p, C.c_int]
+    img = np.random.default_rng(1).random((7, 5, 3), dtype=np.float32)
+    a, b = str(tmp_path / "a.pfm"), str(tmp_path / "b.pfm")
+    write_pfm(img, a)
+    assert L.ref_write_pfm(np.ascontiguousarray(img).ctypes.data_as(C.POINTER(C.c_float)), 5, 7, b.encode()) == 0
+    assert open(a, "rb").read() == open(b, "rb").read()
+    out = np.zeros_like(img)
+    w, h = C.c_int(), C.c_int()
+    err = C.create_string_buffer(256)
+    assert L.ref_read_pfm(a.encode(), out.ctypes.data_as(C.POINTER(C.c_float)), 35, C.byref(w), C.byref(h), err,
+                          256) == 0
+    assert np.array_equal(out, img) and np.array_equal(read_pfm(b), img)
+    big = str(tmp_path / "big.pfm")
+    with open(big, "wb") as f:
+        f.write(b"PF\n5 7\n1.0\n" + img[::-1].astype(">f4").tobytes())
+    assert np.array_equal(read_pfm(big), img)
+    for content, msg in ((b"P6\n1 1\n-1\n", "is not a color PFM file"), (b"PF\n0 1\n-1\n", "malformed PFM header"),
+                         (b"PF\n2 2\n-1\n" + b"\0" * 8, "truncated PFM data")):
+        bad = str(tmp_path / "bad.pfm")
+        open(bad, "wb").write(content)
+        with pytest.raises(RuntimeError, match=msg):
+            read_pfm(bad)
+        assert L.ref_read_pfm(bad.encode(), out.ctypes.data_as(C.POINTER(C.c_float)), 35, C.byref(w), C.byref(h),
+                              err, 256) == 1 and msg in err.value.decode()

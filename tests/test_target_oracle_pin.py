@@ -110,3 +110,23 @@ def test_error_contracts(oracle_built):
     with pytest.raises(RenderError) as e:
         mix_run(t, OracleMixConfig(chains=0))
     assert e.value.code == 2
+
+
+def test_autocorrelation_checker_matches_reference(ref_lib):
+    """autocorrelation_time (core/diagnostics.cpp:87-127): the numpy checker
+    equals the reference's function (AR(1) series with a known tau of
+    (1 + phi) / (1 - phi)), including its error contract."""
+    from oracle.abi import np_autocorrelation_time, ref_autocorrelation_time
+    rng = np.random.default_rng(4)
+    for phi in (0.0, 0.5, 0.9):
+        e = rng.standard_normal(20000)
+        x = np.empty_like(e)
+        x[0] = e[0]
+        for i in range(1, x.size):
+            x[i] = phi * x[i - 1] + e[i]
+        r = ref_autocorrelation_time(ref_lib, x)
+        p = np_autocorrelation_time(x)
+        np.testing.assert_allclose(p, r, rtol=1e-9)
+        assert abs(r[0] - (1 + phi) / (1 - phi)) < 0.25 * (1 + phi) / (1 - phi) + 0.2
+    assert ref_autocorrelation_time(ref_lib, np.ones(2000)) is None and np_autocorrelation_time(np.ones(2000)) is None
+    assert ref_autocorrelation_time(ref_lib, np.arange(999.0)) is None and np_autocorrelation_time(np.arange(999.0)) is None
