@@ -192,10 +192,6 @@ private:
     DBuf<int> roots_, n_nodes_, n_regions_, scratch_cnt_, scratch_list_, splits_;
     DBuf<int> rf_key_[2], rf_val_[2], rf_count_;   // parallel refine: sort keys / node ids
     DBuf<unsigned char> rf_tmp_;
-    bool order_morton_ = false;   // RAMLT_CHAIN_ORDER=morton: visit chains in raster Morton order
-    DBuf<unsigned> ord_key_[2], ord_val_[2];
-    DBuf<unsigned char> ord_tmp_;
-    void sort_chains(rd::StepParams<R> &P);
     DBuf<unsigned long long> trace_count_, trace_index_, trace_n_;
     DBuf<long long> trace_region_;
     DBuf<double> trace_lambda_, trace_alpha_;
@@ -431,8 +427,6 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         use_co_ = std::string(v) == "co" || std::string(v) == "co_static";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
     }
-    if (const char *v = std::getenv("RAMLT_CHAIN_ORDER"))
-        order_morton_ = std::string(v) == "morton";
     if (const char *v = std::getenv("RAMLT_CO_PV"))
         co_pv_global_ = std::string(v) != "smem";
     if (const char *v = std::getenv("RAMLT_CO_REFILL"))
@@ -794,27 +788,6 @@ template <class R> void EngineT<R>::init_chains() {
     chains_ready_ = true;
 }
 
-template <class R> void EngineT<R>::sort_chains(rd::StepParams<R> &P) {
-    if (ord_key_[0].n < static_cast<size_t>(C_)) {
-        for (int q = 0; q < 2; ++q) {
-            ord_key_[q].alloc(C_);
-            ord_val_[q].alloc(C_);
-        }
-        size_t tmp = 0;
-        RAMLT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ord_key_[0].p, ord_key_[1].p, ord_val_[0].p,
-                                                   ord_val_[1].p, C_));
-        ord_tmp_.alloc(tmp);
-    }
-    rd::k_chain_keys<R><<<static_cast<unsigned>((C_ + 255) / 256), 256, 0, stream_>>>(cr_.p, C_, ord_key_[0].p,
-                                                                                       ord_val_[0].p);
-    RAMLT_CUDA(cudaGetLastError());
-    size_t tmp = ord_tmp_.n;
-    RAMLT_CUDA(cub::DeviceRadixSort::SortPairs(ord_tmp_.p, tmp, ord_key_[0].p, ord_key_[1].p, ord_val_[0].p,
-                                               ord_val_[1].p, C_, 0, 22, stream_));
-    launches_ += 2;
-    P.order = ord_val_[1].p;
-}
-
 template <class R> void EngineT<R>::trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) {
     if (!use_bvh_)
         throw std::logic_error("trace_benchmark needs the BVH accelerator (accel=bvh or > 128 triangles)");
@@ -882,8 +855,6 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     if (G_ == 1 && use_co_) {
         P.steal = steal_;
         P.refill = refill_;
-        if (order_morton_ && P.steal)
-            sort_chains(P);
         launch_step_co(P);
         return;
     }

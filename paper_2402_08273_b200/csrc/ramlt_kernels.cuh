@@ -114,7 +114,6 @@ template <class R> struct StepParams {
     int ktab_l2;         // region kernel tables change inside this launch (cooperative): read via L2
     int pooled;          // fuse pooled accumulation into the step
     RegionArrays reg;
-    const unsigned *order;   // k_step_co: chain visiting order (nullptr: identity)
 };
 
 // Region kernel tables are rewritten between lockstep steps of one cooperative
@@ -1123,30 +1122,6 @@ __global__ void k_adapt_pool_apply(RegionArrays ra, KernTab<R> *ktab, AdaptCfg c
 }
 
 __global__ void k_reset_touched(unsigned *n_touched) { *n_touched = 0; }
-
-// ---- chain visiting order --------------------------------------------------------------------
-// Morton code of the current raster position (2 x 11 bits): sorting the chain
-// ids by it hands each warp chains whose primary rays are neighbours, so their
-// BVH walks share nodes.  Visiting order does not change any result.
-__device__ __forceinline__ unsigned spread11(unsigned v) {
-    v &= 0x7ffu;
-    v = (v | (v << 8)) & 0x00ff00ffu;
-    v = (v | (v << 4)) & 0x0f0f0f0fu;
-    v = (v | (v << 2)) & 0x33333333u;
-    v = (v | (v << 1)) & 0x55555555u;
-    return v;
-}
-template <class R>
-__global__ void k_chain_keys(const R *cr, int C, unsigned *key, unsigned *val) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C)
-        return;
-    R u = cr[c], v = cr[C + c];
-    unsigned iu = static_cast<unsigned>(min(max(u, R(0)), R(0.99999)) * R(2048));
-    unsigned iv = static_cast<unsigned>(min(max(v, R(0)), R(0.99999)) * R(2048));
-    key[c] = spread11(iu) | (spread11(iv) << 1);
-    val[c] = static_cast<unsigned>(c);
-}
 
 // ---- quadtree refinement (core/partition.cpp:68-100, 217-227; core/adaptation.cpp:34-42) --------
 // Snapshot the leaves, split those with visits >= M_split; children get ids in

@@ -745,7 +745,7 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                     co.attempts = 0;
                     have = true;
                 } else if (mine < static_cast<unsigned>(P.C)) {
-                    co_load(co, P, static_cast<int>(P.order ? __ldg(P.order + mine) : mine));
+                    co_load(co, P, static_cast<int>(mine));
                     const unsigned long long my_steps =
                         P.per + (static_cast<unsigned long long>(co.gc) < P.rem ? 1ull : 0ull);
                     j = P.j0;

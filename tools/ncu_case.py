@@ -8,7 +8,8 @@ res = int(sys.argv[7]) if len(sys.argv) > 7 else 512
 cfg = RenderConfig(strategy=strat, perturbation=pert, chains=C, mutations=C * steps, width=res, height=res,
                    max_vertices=maxv, b_samples=65536, precision="f32", rng="philox",
                    metrics_interval=C * steps, steps_per_launch=int(os.environ.get("SPL", "0")))
-eng = Engine(scenes.SCENES[scene](), cfg)
+kw = {"n_tris": int(os.environ["NTRIS"])} if os.environ.get("NTRIS") else {}
+eng = Engine(scenes.SCENES[scene](**kw), cfg)
 eng.estimate_b(); eng.init_chains(); eng.run(C * steps); eng.synchronize()
 s = eng.stats()
 print("ok", s.total_mutations, s.kernel_launches)
