@@ -175,6 +175,14 @@ template <> struct Unit<float> {
         (void)g.next_u32();
         return static_cast<float>(hi >> 8) * 0x1.0p-24f;
     }
+#ifdef RAMLT_NOINLINE_RNG
+    // one out-of-line copy instead of the draw inlined at every call site
+    static __device__ __noinline__ float draw(Rng<RNG_PHILOX> &g) {
+        uint32_t hi = g.next_u32();
+        (void)g.next_u32();
+        return static_cast<float>(hi >> 8) * 0x1.0p-24f;
+    }
+#endif
 };
 
 // ---- scene --------------------------------------------------------------------------
