@@ -129,6 +129,13 @@ __device__ __forceinline__ void philox10(uint32_t &c0, uint32_t &c1, uint32_t &c
     }
 }
 
+__device__ __noinline__ uint4 philox_block(uint64_t b, uint64_t stream, uint64_t key) {
+    uint32_t c0 = static_cast<uint32_t>(b), c1 = static_cast<uint32_t>(b >> 32);
+    uint32_t c2 = static_cast<uint32_t>(stream), c3 = static_cast<uint32_t>(stream >> 32);
+    philox10(c0, c1, c2, c3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
+    return make_uint4(c0, c1, c2, c3);
+}
+
 template <> struct Rng<RNG_PHILOX> {
     uint64_t key, stream, draw;
     uint32_t b0, b1, b2, b3;
@@ -139,14 +146,17 @@ template <> struct Rng<RNG_PHILOX> {
         draw = 0;
         bid = ~0ULL;
     }
-    // The 10-round block computation is out of line: next_u32 is inlined at
-    // every draw site, the refill runs once per four words.
-    __device__ __noinline__ void refill(uint64_t b) {
-        b0 = static_cast<uint32_t>(b);
-        b1 = static_cast<uint32_t>(b >> 32);
-        b2 = static_cast<uint32_t>(stream);
-        b3 = static_cast<uint32_t>(stream >> 32);
-        philox10(b0, b1, b2, b3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
+    // The 10-round block computation is out of line (philox_block): next_u32
+    // is inlined at every draw site, the refill runs once per four words.  The
+    // call takes and returns values only -- a member call would take the
+    // generator's address and pin it, and every struct holding it (the
+    // coroutine state), to local memory.
+    __device__ __forceinline__ void refill(uint64_t b) {
+        uint4 r = philox_block(b, stream, key);
+        b0 = r.x;
+        b1 = r.y;
+        b2 = r.z;
+        b3 = r.w;
         bid = b;
     }
     __device__ __forceinline__ uint32_t next_u32() {
@@ -175,14 +185,6 @@ template <> struct Unit<float> {
         (void)g.next_u32();
         return static_cast<float>(hi >> 8) * 0x1.0p-24f;
     }
-#ifdef RAMLT_NOINLINE_RNG
-    // one out-of-line copy instead of the draw inlined at every call site
-    static __device__ __noinline__ float draw(Rng<RNG_PHILOX> &g) {
-        uint32_t hi = g.next_u32();
-        (void)g.next_u32();
-        return static_cast<float>(hi >> 8) * 0x1.0p-24f;
-    }
-#endif
 };
 
 // ---- scene --------------------------------------------------------------------------

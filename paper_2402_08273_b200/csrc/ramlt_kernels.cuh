@@ -137,11 +137,7 @@ template <class R> struct CurPath {
     const GV<R> *verts;
     int C, c;
     const CamD<R> *cam;
-#ifdef RAMLT_NOINLINE_PATH
-    __device__ __noinline__ Vx<R> get(int i) const {
-#else
     __device__ __forceinline__ Vx<R> get(int i) const {
-#endif
         if (i == 0) {
             Vx<R> v;
             v.p = cam->pos;
