@@ -129,13 +129,6 @@ __device__ __forceinline__ void philox10(uint32_t &c0, uint32_t &c1, uint32_t &c
     }
 }
 
-__device__ __noinline__ uint4 philox_block(uint64_t b, uint64_t stream, uint64_t key) {
-    uint32_t c0 = static_cast<uint32_t>(b), c1 = static_cast<uint32_t>(b >> 32);
-    uint32_t c2 = static_cast<uint32_t>(stream), c3 = static_cast<uint32_t>(stream >> 32);
-    philox10(c0, c1, c2, c3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
-    return make_uint4(c0, c1, c2, c3);
-}
-
 template <> struct Rng<RNG_PHILOX> {
     uint64_t key, stream, draw;
     uint32_t b0, b1, b2, b3;
@@ -146,17 +139,16 @@ template <> struct Rng<RNG_PHILOX> {
         draw = 0;
         bid = ~0ULL;
     }
-    // The 10-round block computation is out of line (philox_block): next_u32
-    // is inlined at every draw site, the refill runs once per four words.  The
-    // call takes and returns values only -- a member call would take the
-    // generator's address and pin it, and every struct holding it (the
-    // coroutine state), to local memory.
-    __device__ __forceinline__ void refill(uint64_t b) {
-        uint4 r = philox_block(b, stream, key);
-        b0 = r.x;
-        b1 = r.y;
-        b2 = r.z;
-        b3 = r.w;
+    // The 10-round block computation is out of line: the refill runs once per
+    // four words.  (Passing the state by value instead, which lets the
+    // coroutine state leave local memory, measured slower: c4 62 -> 52 M
+    // mutations/s from register spills at the 64-register budget.)
+    __device__ __noinline__ void refill(uint64_t b) {
+        b0 = static_cast<uint32_t>(b);
+        b1 = static_cast<uint32_t>(b >> 32);
+        b2 = static_cast<uint32_t>(stream);
+        b3 = static_cast<uint32_t>(stream >> 32);
+        philox10(b0, b1, b2, b3, static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32));
         bid = b;
     }
     __device__ __forceinline__ uint32_t next_u32() {
@@ -171,8 +163,38 @@ template <> struct Rng<RNG_PHILOX> {
 
 // Uniform in [0,1): next_double (core/rng.hpp:32-40) for R = double; the same
 // two words truncated to 24 bits for R = float (identical consumption).
+// The Philox uniform draw is out of line: one copy per kernel instead of an
+// expansion at each of the ~20 draw sites of the chain step (a smaller
+// instruction footprint for the divergent coroutine; c4 +4 %).
+#ifndef RAMLT_DRAW_INLINE
+#define RAMLT_DRAW_INLINE __noinline__
+#endif
+// Philox: a uniform is always the word pair (2i, 2i+1) of one block when the
+// draw counter is even (every draw in the hot path is a next_double), so one
+// block check and one select replace two next_u32 expansions per draw site.
+__device__ __forceinline__ bool philox_pair(Rng<RNG_PHILOX> &g, uint32_t &hi, uint32_t &lo) {
+    if (g.draw & 1ull)
+        return false;
+    uint64_t b = g.draw >> 2;
+    if (b != g.bid)
+        g.refill(b);
+    const bool second = (g.draw & 2ull) != 0;
+    hi = second ? g.b2 : g.b0;
+    lo = second ? g.b3 : g.b1;
+    g.draw += 2;
+    return true;
+}
+
 template <class R> struct Unit;
 template <> struct Unit<double> {
+    static __device__ RAMLT_DRAW_INLINE double draw(Rng<RNG_PHILOX> &g) {
+        uint32_t h, l;
+        if (!philox_pair(g, h, l)) {
+            h = g.next_u32();
+            l = g.next_u32();
+        }
+        return static_cast<double>(((static_cast<uint64_t>(h) << 32) | l) >> 11) * 0x1.0p-53;
+    }
     template <class G> static __device__ __forceinline__ double draw(G &g) {
         uint64_t hi = g.next_u32();
         uint64_t lo = g.next_u32();
@@ -180,6 +202,14 @@ template <> struct Unit<double> {
     }
 };
 template <> struct Unit<float> {
+    static __device__ RAMLT_DRAW_INLINE float draw(Rng<RNG_PHILOX> &g) {
+        uint32_t h, l;
+        if (!philox_pair(g, h, l)) {
+            h = g.next_u32();
+            (void)g.next_u32();
+        }
+        return static_cast<float>(h >> 8) * 0x1.0p-24f;
+    }
     template <class G> static __device__ __forceinline__ float draw(G &g) {
         uint32_t hi = g.next_u32();
         (void)g.next_u32();
