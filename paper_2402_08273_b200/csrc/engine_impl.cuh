@@ -176,6 +176,7 @@ private:
     bool use_co_init_ = false;  // chain initialisation with the coroutine kernel (default with a BVH)
     int steal_ = 1;           // RAMLT_STEP_KERNEL=co_static: one chain per lane, no stealing
     int refill_ = 8;          // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round
+    int co_carveout_ = -1;    // k_step_co: RAMLT_CO_CARVEOUT percent (-1: driver default)
     // film
     DBuf<double> film64_;
     DBuf<float4> film32_;
@@ -429,6 +430,8 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     }
     if (const char *v = std::getenv("RAMLT_CO_PV"))
         co_pv_global_ = std::string(v) != "smem";
+    if (const char *v = std::getenv("RAMLT_CO_CARVEOUT"))
+        co_carveout_ = std::min(100, std::max(0, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_CO_REFILL"))
         refill_ = std::min(32, std::max(1, std::atoi(v)));
     size_t npix = static_cast<size_t>(d.width) * d.height;
@@ -909,6 +912,8 @@ void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
     if (use_bvh_)
         smem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (co_carveout_ >= 0)   // RAMLT_CO_CARVEOUT: shared-memory share of the L1/smem pool (percent)
+        RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, co_carveout_));
     int per_sm = 0;
     RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     int dev = 0, sms = 148;
