@@ -236,3 +236,35 @@ def test_autocorrelation_on_device():
                 continue
             assert st[i] == 0
             np.testing.assert_allclose([tau[i], neff[i], s2[i]], r, rtol=1e-9)
+
+
+@pytest.mark.parametrize("case", ["d1k1", "batch1", "lambda_floor", "ragged_block", "fixed_pcg_many"])
+def test_edge_cases_match_oracle(case):
+    """Edge cases of the controller / accept boundary, f64 vs the oracle
+    (PCG32 + literal where the reference composition applies, else Philox +
+    pooled): a 1-D single-component target (generic kernel path), L = 1
+    (an update after every visit), a target acceptance the walk cannot reach
+    (lambda pinned at lambda_min), a chain count that is not a multiple of the
+    block size, and Fixed with many chains on the reference's own streams."""
+    from oracle.abi import OracleMixConfig, mix_run
+    from paper_2402_08273_b200.mix import MixTarget
+    t = MixTarget.config2(6)
+    kw = dict(strategy="global", chains=37, seed=13, log_steps=16)
+    rng, mode, steps = "pcg32", "literal", 300
+    if case == "d1k1":
+        t = MixTarget(np.array([1.0]), np.array([[0.5]]), np.array([[[0.01]]]))
+    elif case == "batch1":
+        kw.update(batch_size=1)
+    elif case == "lambda_floor":
+        kw.update(target_acceptance=0.999, lambda_min=-12.0)
+        steps = 600
+    elif case == "ragged_block":
+        kw.update(chains=1000 + 37, strategy="ra-grid", grid_n=5)
+        rng, mode = "philox", "pooled"
+    elif case == "fixed_pcg_many":
+        kw.update(strategy="fixed", chains=3000, lambda_init=-7.5)
+    o = mix_run(t, OracleMixConfig(steps=steps, rng=rng, adapt_mode=mode, **kw))
+    g = gpu_run(t, steps, precision="f64", rng=rng, adapt_mode=mode, **kw)
+    assert_same(o, g)
+    if case == "lambda_floor":
+        assert g["lambda_"][0] == -12.0
