@@ -355,8 +355,13 @@ def bench_c2(args):
     sm_max = clk.summary().get("sm_max_mhz") or 1965.0
     peak = 148 * 128 * 2 * float(sm_max) * 1e6 / 1e12
     achieved = (muts / kl) * w / ((kms / kl) / 1e3) / 1e12
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic_c2.json"))).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        traffic = None
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic,
                 "peak_source": "nominal FP32 issue: 148 SM x 128 lanes x 2 x sm_max_mhz",
                 "work_per_unit": f"{w:.0f} FLOP per chain step (K(D^2+3D+2) + 2K+1 + 26D + 2, D={D}, K={K})",
                 "kernel": "k_mix_coop (persistent cooperative chain-step kernel)",
@@ -497,7 +502,10 @@ def main():
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("dram_bytes_per_launch")
+            if "dram_bytes_per_mutation" in tj:   # launches of this workload vary in size
+                traffic = tj["dram_bytes_per_mutation"] * per_launch_muts
         except Exception:
             traffic = None
     if wl["bound"] == "fp32":

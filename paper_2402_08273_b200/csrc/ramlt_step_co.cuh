@@ -205,7 +205,7 @@ template <class R, int RK, bool INIT>
 __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> &P, const SceneView<R> &S,
                                                       const PvSmem<R> &pv, RayCount &rc,
                                                       unsigned long long index) {
-    CurPath<R> cur{P.ch.verts, P.C, c, &S.cam};
+    CurPath<R> cur{P.ch.verts, P.C, c, S.cam.pos, S.cam.fwd};
     switch (pc) {
     case 0: {
         if constexpr (INIT) {
