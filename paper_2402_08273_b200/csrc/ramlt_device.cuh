@@ -458,7 +458,10 @@ template <class R> struct BvhTrav {
     // 128 (one bank per lane: conflict-free whatever each lane's depth), the
     // rest in local memory.  Scattered per-lane depths made a local-only stack
     // the top L1 miss / long-scoreboard stall.
-    static constexpr int SSTACK = 16;
+#ifndef RAMLT_SSTACK
+#define RAMLT_SSTACK 16
+#endif
+    static constexpr int SSTACK = RAMLT_SSTACK;
     int *ss;    // shared: entry i at ss[i * 128]
     int *sl;    // local: entry i >= SSTACK at sl[i - SSTACK]
 
