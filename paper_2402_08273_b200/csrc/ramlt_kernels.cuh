@@ -136,8 +136,29 @@ template <class R> __device__ __forceinline__ KernTab<R> ld_ktab(const KernTab<R
 template <class R> struct CurPath {
     const GV<R> *verts;
     int C, c;
-    // the camera vertex by value: a pointer into the (block-staged) SceneView
-    // would take its address and pin the whole view to local memory
+    const CamD<R> *cam;
+    __device__ __forceinline__ Vx<R> get(int i) const {
+        if (i == 0) {
+            Vx<R> v;
+            v.p = cam->pos;
+            v.n = cam->fwd;
+            v.mat = -1;
+            v.emi = -1;
+            v.spec = false;
+            v.ev = EV_NONE;
+            return v;
+        }
+        return load_gv(&verts[static_cast<size_t>(i - 1) * C + c]);
+    }
+};
+
+// The coroutine kernel's form: the camera vertex by value.  A pointer into
+// its block-staged SceneView would take the view's address and pin it -- every
+// scene pointer the step reads -- to local memory (c4 -3 %); the megakernel's
+// view is in local memory anyway and keeps the pointer (c3 -4 % by value).
+template <class R> struct CurPathV {
+    const GV<R> *verts;
+    int C, c;
     V3<R> cam_pos, cam_fwd;
     __device__ __forceinline__ Vx<R> get(int i) const {
         if (i == 0) {
@@ -610,7 +631,7 @@ template <class R, int RK, int G>
 __device__ void mutate(const StepParams<R> &P, const SceneView<R> &S, int c, long long gc,
                        unsigned long long index, ChainRegs<R> &cs, Rng<RK> &rng, const Group<G> &g,
                        RayCount &rc) {
-    CurPath<R> cur{P.ch.verts, P.C, c, S.cam.pos, S.cam.fwd};
+    CurPath<R> cur{P.ch.verts, P.C, c, &S.cam};
     Vx<R> pv[kMaxV];
     int head_end = 0;
     int kp = cs.k;
@@ -845,7 +866,7 @@ __device__ void init_chain(const StepParams<R> &P, const SceneView<R> &S, int c,
         double tf;
         if (!trace_eye(S, init, P.maxv, pv, k, sm, tf, g, rc))
             continue;
-        CurPath<R> dummy{P.ch.verts, P.C, c, S.cam.pos, S.cam.fwd};
+        CurPath<R> dummy{P.ch.verts, P.C, c, &S.cam};
         PropPath<R> path{pv, k - 1, &dummy};
         Contrib<R> con = evaluate(S, path, k, g, rc);
         if (con.pi > R(0)) {
@@ -917,7 +938,7 @@ __global__ void __launch_bounds__(128) k_bsub(StepParams<R> P, unsigned long lon
         double tf;
         double v = 0.0;
         if (trace_eye(S, rng, P.maxv, pv, k, sm, tf, g, rc)) {
-            CurPath<R> dummy{P.ch.verts, P.C, 0, S.cam.pos, S.cam.fwd};
+            CurPath<R> dummy{P.ch.verts, P.C, 0, &S.cam};
             PropPath<R> path{pv, k - 1, &dummy};
             Contrib<R> con = evaluate(S, path, k, g, rc);
             if (con.pi > R(0)) {

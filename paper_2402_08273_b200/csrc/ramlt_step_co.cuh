@@ -124,7 +124,7 @@ template <> __device__ __forceinline__ void PvSmem<double>::set(int i, const Vx<
 template <class R> struct PropS {
     PvSmem<R> pv;
     int head_end;
-    const CurPath<R> *cur;
+    const CurPathV<R> *cur;
     __device__ __forceinline__ Vx<R> get(int i) const { return i <= head_end ? pv.get(i) : cur->get(i); }
 };
 
@@ -205,7 +205,7 @@ template <class R, int RK, bool INIT>
 __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> &P, const SceneView<R> &S,
                                                       const PvSmem<R> &pv, RayCount &rc,
                                                       unsigned long long index) {
-    CurPath<R> cur{P.ch.verts, P.C, c, S.cam.pos, S.cam.fwd};
+    CurPathV<R> cur{P.ch.verts, P.C, c, S.cam.pos, S.cam.fwd};
     switch (pc) {
     case 0: {
         if constexpr (INIT) {
