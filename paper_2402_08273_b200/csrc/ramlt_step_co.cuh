@@ -143,11 +143,22 @@ enum { CO_RAY_PENDING = 1, CO_STEP_DONE = 2 };
 // INIT: the same coroutine runs chain initialisation (core/driver.cpp:219-242):
 // large-step eye paths from the chain's init stream until one has a nonzero
 // contribution, then the chain's state is written (as init_chain does).
+// The chain's persistent state the coroutine carries (ChainRegs without the
+// per-chain tallies: those are read-modify-written in HBM at the step's end,
+// which keeps the local-memory coroutine state 56 B smaller).
+template <class R> struct ChainCo {
+    int k;
+    unsigned sm;
+    V3<R> f;
+    R pi, ru, rv;
+    double eyeden;
+};
+
 template <class R, int RK, bool INIT = false> struct StepCo {
     // ---- chain (persists over the chain's steps) ----
     int c;
     long long gc;
-    ChainRegs<R> cs;
+    ChainCo<R> cs;
     Rng<RK> rng;
     // ---- coroutine ----
     int pc;
@@ -155,7 +166,7 @@ template <class R, int RK, bool INIT = false> struct StepCo {
     int res_prim;   // -1 miss / visible
     R res_t;
     // ---- per-step state ----
-    bool choose, ok, accepted;
+    bool choose, ok, accepted, pert_rec;
     R s_pert, dpdf;
     double tf, tr, a;   // transition densities and acceptance: fp64 in every build
     int endpoint, first, idx, next, i, region, kp, head_end;
@@ -234,6 +245,7 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
         pcb.pi = R(0);
         region = -1;
         ok = false;
+        pert_rec = false;
         kp = cs.k;
         smp = cs.sm;
         head_end = 0;
@@ -313,7 +325,6 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
         goto eval_start;
 
     large_step:
-        ++cs.nlarge;
     init_attempt:
         pcb.pi = R(0);
         // trace_eye_subpath (path.cpp:84-142) -- large_step (mutations.cpp:58-71)
@@ -585,10 +596,7 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
     pert_record:
         if (P.ctl == 2)
             atomicAdd(&P.part.visits[region], 1ull);
-        cs.acc += a;
-        cs.iacc += a;
-        ++cs.npert;
-        ++cs.ipert;
+        pert_rec = true;
 
     finish:
         if constexpr (INIT) {   // failed attempt: the next one continues the init stream
@@ -600,10 +608,23 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
             return CO_STEP_DONE;
         }
         // splat (driver.cpp:59-64)
-        if (a < 1.0 && cs.pi > R(0))
-            film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - static_cast<R>(a)) / cs.pi), cs.lum);
-        if (pcb.pi > R(0) && a > 0.0)
-            film_add(P, pcb.u, pcb.v, scl(pcb.f, static_cast<R>(a) / pcb.pi), cs.lum);
+        {
+            // per-chain tallies read-modify-written in HBM, in the reference's order
+            double lum = P.ch.lum[c];
+            if (a < 1.0 && cs.pi > R(0))
+                film_add(P, cs.ru, cs.rv, scl(cs.f, (R(1) - static_cast<R>(a)) / cs.pi), lum);
+            if (pcb.pi > R(0) && a > 0.0)
+                film_add(P, pcb.u, pcb.v, scl(pcb.f, static_cast<R>(a) / pcb.pi), lum);
+            P.ch.lum[c] = lum;
+            if (pert_rec) {
+                P.ch.acc[c] += a;
+                P.ch.iacc[c] += a;
+                P.ch.npert[c] += 1;
+                P.ch.ipert[c] += 1;
+            } else {
+                P.ch.nlarge[c] += 1;
+            }
+        }
         // accept / commit (driver.cpp:168-171)
         accepted = false;
         if (a > 0.0 && static_cast<double>(Unit<R>::draw(rng)) < a) {
@@ -618,8 +639,9 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
             cs.rv = pcb.v;
             cs.eyeden = __longlong_as_double(0x7ff8000000000000LL);
         }
-        if (cs.nsteps < P.ch.log_K) {
-            size_t ofs = static_cast<size_t>(cs.nsteps) * P.C + c;
+        const unsigned long long nst = P.ch.nsteps[c];
+        if (nst < P.ch.log_K) {
+            size_t ofs = static_cast<size_t>(nst) * P.C + c;
             P.ch.log_a[ofs] = a;
             P.ch.log_f[ofs] = static_cast<unsigned char>((accepted ? 1 : 0) | (choose ? 2 : 0) | 4);
         }
@@ -627,7 +649,7 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
             P.ch.vreg[c] = (choose && P.ctl != 0) ? region : -1;
             P.ch.va[c] = a;
         }
-        ++cs.nsteps;
+        P.ch.nsteps[c] = nst + 1;
         (void)index;
         pc = 0;
         return CO_STEP_DONE;
@@ -645,7 +667,7 @@ template <class R, int RK, bool I>
 __device__ __forceinline__ void co_load(StepCo<R, RK, I> &co, const StepParams<R> &P, int c) {
     co.c = c;
     co.gc = P.chain_off + c;
-    ChainRegs<R> &cs = co.cs;
+    ChainCo<R> &cs = co.cs;
     cs.k = P.ch.klen[c];
     cs.sm = P.ch.smask[c];
     cs.f = mk(P.ch.cf[c], P.ch.cf[P.C + c], P.ch.cf[2 * P.C + c]);
@@ -653,13 +675,6 @@ __device__ __forceinline__ void co_load(StepCo<R, RK, I> &co, const StepParams<R
     cs.ru = P.ch.cr[c];
     cs.rv = P.ch.cr[P.C + c];
     cs.eyeden = P.ch.eyeden[c];
-    cs.acc = P.ch.acc[c];
-    cs.iacc = P.ch.iacc[c];
-    cs.lum = P.ch.lum[c];
-    cs.npert = P.ch.npert[c];
-    cs.nlarge = P.ch.nlarge[c];
-    cs.ipert = P.ch.ipert[c];
-    cs.nsteps = P.ch.nsteps[c];
     RngIO<RK>::load(co.rng, P.ch.rng0, P.ch.rng1, c, P.seed, static_cast<unsigned long long>(co.gc));
     co.pc = 0;
 }
@@ -667,7 +682,7 @@ __device__ __forceinline__ void co_load(StepCo<R, RK, I> &co, const StepParams<R
 template <class R, int RK, bool I>
 __device__ __forceinline__ void co_store(const StepCo<R, RK, I> &co, const StepParams<R> &P) {
     const int c = co.c;
-    const ChainRegs<R> &cs = co.cs;
+    const ChainCo<R> &cs = co.cs;
     P.ch.klen[c] = cs.k;
     P.ch.smask[c] = cs.sm;
     P.ch.cf[c] = cs.f.x;
@@ -677,13 +692,6 @@ __device__ __forceinline__ void co_store(const StepCo<R, RK, I> &co, const StepP
     P.ch.cr[c] = cs.ru;
     P.ch.cr[P.C + c] = cs.rv;
     P.ch.eyeden[c] = cs.eyeden;
-    P.ch.acc[c] = cs.acc;
-    P.ch.iacc[c] = cs.iacc;
-    P.ch.lum[c] = cs.lum;
-    P.ch.npert[c] = cs.npert;
-    P.ch.nlarge[c] = cs.nlarge;
-    P.ch.ipert[c] = cs.ipert;
-    P.ch.nsteps[c] = cs.nsteps;
     RngIO<RK>::store(co.rng, P.ch.rng0, P.ch.rng1, c);
 }
 
