@@ -157,7 +157,6 @@ template <class R> struct ChainCo {
 template <class R, int RK, bool INIT = false> struct StepCo {
     // ---- chain (persists over the chain's steps) ----
     int c;
-    long long gc;
     ChainCo<R> cs;
     Rng<RK> rng;
     // ---- coroutine ----
@@ -178,7 +177,7 @@ template <class R, int RK, bool INIT = false> struct StepCo {
     double ep;
     R eseg;
     int ek, ei;
-    unsigned long long attempts;   // INIT
+    unsigned attempts;             // INIT (init_attempts < 2^32)
 
     __device__ __forceinline__ int advance(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
                                            RayCount &rc, unsigned long long index);
@@ -207,7 +206,7 @@ template <class R, int RK, bool INIT = false> struct StepCo {
         P.ch.ipert[c] = 0;
         P.ch.nsteps[c] = 0;
         Rng<RK> fresh;
-        fresh.reseed(P.seed, static_cast<unsigned long long>(gc));
+        fresh.reseed(P.seed, static_cast<unsigned long long>(P.chain_off + c));
         RngIO<RK>::store(fresh, P.ch.rng0, P.ch.rng1, c);
     }
 };
@@ -666,7 +665,6 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
 template <class R, int RK, bool I>
 __device__ __forceinline__ void co_load(StepCo<R, RK, I> &co, const StepParams<R> &P, int c) {
     co.c = c;
-    co.gc = P.chain_off + c;
     ChainCo<R> &cs = co.cs;
     cs.k = P.ch.klen[c];
     cs.sm = P.ch.smask[c];
@@ -675,7 +673,7 @@ __device__ __forceinline__ void co_load(StepCo<R, RK, I> &co, const StepParams<R
     cs.ru = P.ch.cr[c];
     cs.rv = P.ch.cr[P.C + c];
     cs.eyeden = P.ch.eyeden[c];
-    RngIO<RK>::load(co.rng, P.ch.rng0, P.ch.rng1, c, P.seed, static_cast<unsigned long long>(co.gc));
+    RngIO<RK>::load(co.rng, P.ch.rng0, P.ch.rng1, c, P.seed, static_cast<unsigned long long>(P.chain_off + c));
     co.pc = 0;
 }
 
@@ -747,15 +745,14 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                 }
                 if (INIT && mine < static_cast<unsigned>(P.C)) {
                     co.c = static_cast<int>(mine);
-                    co.gc = P.chain_off + co.c;
-                    co.rng.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(co.gc) * 2ull);
+                    co.rng.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(P.chain_off + co.c) * 2ull);
                     co.pc = 0;
                     co.attempts = 0;
                     have = true;
                 } else if (mine < static_cast<unsigned>(P.C)) {
                     co_load(co, P, static_cast<int>(mine));
                     const unsigned long long my_steps =
-                        P.per + (static_cast<unsigned long long>(co.gc) < P.rem ? 1ull : 0ull);
+                        P.per + (static_cast<unsigned long long>(P.chain_off + co.c) < P.rem ? 1ull : 0ull);
                     j = P.j0;
                     jend = static_cast<int>(min(static_cast<unsigned long long>(P.j1), my_steps));
                     have = true;
@@ -771,7 +768,7 @@ k_step_co(StepParams<R> P, unsigned int *work) {
         }
         // (2) divergent: advance to the next ray cast
         while (have && !want) {
-            unsigned long long index = P.span_start + static_cast<unsigned long long>(j) * P.C_total + co.gc;
+            unsigned long long index = P.span_start + static_cast<unsigned long long>(j) * P.C_total + P.chain_off + co.c;
             int st = co.advance(P, S, pv, rc, index);
             if (st == CO_RAY_PENDING) {
                 want = true;
