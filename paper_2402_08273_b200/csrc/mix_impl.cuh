@@ -42,6 +42,11 @@
 #include <string>
 #include <vector>
 
+// back-off of the configs[1] grid barrier's spin (ns; 0 = busy spin)
+#ifndef RAMLT_MIX_SPIN_NS
+#define RAMLT_MIX_SPIN_NS 32
+#endif
+
 namespace rdm {
 using namespace rd;
 
@@ -597,7 +602,8 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
                 unsigned long long v = atomicAdd(&P.gbuf[j % 3], b) + b;
                 const unsigned long long want = static_cast<unsigned long long>(gridDim.x);
                 while ((v >> 48) < want) {
-                    __nanosleep(32);
+                    if (RAMLT_MIX_SPIN_NS > 0)
+                        __nanosleep(RAMLT_MIX_SPIN_NS);
                     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&P.gbuf[j % 3]) : "memory");
                 }
                 // the region update once per block (thread 0 holds the replica)
