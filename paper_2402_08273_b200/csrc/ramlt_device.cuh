@@ -826,21 +826,21 @@ template <class R> __device__ __forceinline__ R nquantile(R p) {
             c4 = R(4.374664141464968e+00), c5 = R(2.938163982698783e+00);
     const R d0 = R(7.784695709041462e-03), d1 = R(3.224671290700398e-01),
             d2 = R(2.445134137142996e+00), d3 = R(3.754408661907416e+00);
-    R x;
-    if (p < R(0.02425)) {
-        R q = M<R>::sqrt(R(-2) * M<R>::log(p));
-        x = (((((c0 * q + c1) * q + c2) * q + c3) * q + c4) * q + c5) /
-            ((((d0 * q + d1) * q + d2) * q + d3) * q + R(1));
-    } else if (p > R(1) - R(0.02425)) {
-        R q = M<R>::sqrt(R(-2) * M<R>::log(R(1) - p));
-        x = -(((((c0 * q + c1) * q + c2) * q + c3) * q + c4) * q + c5) /
-            ((((d0 * q + d1) * q + d2) * q + d3) * q + R(1));
-    } else {
-        R q = p - R(0.5);
-        R r = q * q;
-        x = (((((a0 * r + a1) * r + a2) * r + a3) * r + a4) * r + a5) * q /
-            (((((b0 * r + b1) * r + b2) * r + b3) * r + b4) * r + R(1));
-    }
+    // Branch-free over the three regions (warps almost always hold lanes of
+    // more than one): select the region's coefficients and evaluate one
+    // rational function.  Same operations in the same order as the branchy
+    // form (the tail denominator's missing leading term enters as 0 * t + d0
+    // = d0, the tail numerator's sign as an exact +-1 factor), so fp64 results
+    // are bit-identical to it.
+    const bool lo = p < R(0.02425), hi = p > R(1) - R(0.02425), mid = !lo && !hi;
+    const R qc = p - R(0.5);
+    const R qt = M<R>::sqrt(R(-2) * M<R>::log(hi ? R(1) - p : p));
+    const R t = mid ? qc * qc : qt;
+    const R n = (((((mid ? a0 : c0) * t + (mid ? a1 : c1)) * t + (mid ? a2 : c2)) * t + (mid ? a3 : c3)) * t +
+                 (mid ? a4 : c4)) * t + (mid ? a5 : c5);
+    const R d = (((((mid ? b0 : R(0)) * t + (mid ? b1 : d0)) * t + (mid ? b2 : d1)) * t + (mid ? b3 : d2)) * t +
+                 (mid ? b4 : d3)) * t + R(1);
+    R x = n * (mid ? qc : (hi ? R(-1) : R(1))) / d;
     if (sizeof(R) == 8) {   // the Halley refinement only pays at fp64 precision
         R e = ncdf(x) - p;
         R u = e * M<R>::sqrt(R(kTwoPiD)) * M<R>::exp(R(0.5) * x * x);
