@@ -175,7 +175,7 @@ private:
     bool use_co_ = false;     // G == 1: the coroutine kernel (default with a BVH)
     bool use_co_init_ = false;  // chain initialisation with the coroutine kernel (default with a BVH)
     int steal_ = 1;           // RAMLT_STEP_KERNEL=co_static: one chain per lane, no stealing
-    int refill_ = 8;          // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round
+    int refill_ = 24;         // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round (c4: 4/8/16/24/28/32 -> 62.3/65.8/70.0/71.8/72.2/71.3 M)
     int co_carveout_ = -1;    // k_step_co: RAMLT_CO_CARVEOUT percent (-1: driver default)
     // film
     DBuf<double> film64_;
