@@ -175,6 +175,7 @@ private:
     bool use_co_ = false;     // G == 1: the coroutine kernel (default with a BVH)
     bool use_co_init_ = false;  // chain initialisation with the coroutine kernel (default with a BVH)
     int steal_ = 1;           // RAMLT_STEP_KERNEL=co_static: one chain per lane, no stealing
+    int init_refill_ = 8;     // the same for chain initialisation (RAMLT_CO_INIT_REFILL; c4 init 8/16/24/32: 0.81/0.84/0.85/0.95 s)
     int refill_ = 24;         // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round (c4: 4/8/16/24/28/32 -> 62.3/65.8/70.0/71.8/72.2/71.3 M)
     int co_carveout_ = -1;    // k_step_co: RAMLT_CO_CARVEOUT percent (-1: driver default)
     // film
@@ -434,6 +435,8 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         co_carveout_ = std::min(100, std::max(0, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_CO_REFILL"))
         refill_ = std::min(32, std::max(1, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_CO_INIT_REFILL"))
+        init_refill_ = std::min(32, std::max(1, std::atoi(v)));
     size_t npix = static_cast<size_t>(d.width) * d.height;
     film64_.alloc(npix * 3);
     film64_.zero(stream_);
@@ -766,7 +769,7 @@ template <class R> void EngineT<R>::init_chains() {
     rd::StepParams<R> P = params();
     if (use_co_init_) {   // BVH scenes: the coroutine kernel with dynamic ray fetch
         P.steal = 1;
-        P.refill = refill_;
+        P.refill = init_refill_;
         P.init_attempts = 50000000ull;
         launch_step_co<true>(P);
         check_err("init");
