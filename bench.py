@@ -459,7 +459,8 @@ def main():
             return
         sample = args.cpu_sample or wl["cpu_sample"]
         vals, times = [], []
-        for _ in range(args.warmup if args.warmup < 3 else 1):
+        n_warm = args.warmup if args.warmup < 3 else 1
+        for _ in range(n_warm):
             cpu_reference_run(wl, wl["scene_text"], max(sample // 8, threads), threads)
         for _ in range(min(args.steps, 8 if wl["bound"] == "fp32" else 2)):
             v, kind, cores, t, chains = cpu_reference_run(wl, wl["scene_text"], sample, threads)
@@ -467,7 +468,7 @@ def main():
             times.append(t)
         v = sum(vals) / len(vals)
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": len(vals),
-                "warmup": 1, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+                "warmup": n_warm, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
                 "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "impl": "reference", "config": dict(config, chains_cpu=chains),
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
