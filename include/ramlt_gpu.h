@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RAMLT_GPU_ABI_VERSION 1
+#define RAMLT_GPU_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define RAMLT_API __attribute__((visibility("default")))
@@ -196,6 +196,26 @@ RAMLT_API int ramlt_gpu_create_from_text(const char *scene_text, const char *ori
                                const ramlt_render_desc *desc, ramlt_gpu **out);
 RAMLT_API const char *ramlt_gpu_last_create_error(void);
 
+/* create() over several devices of this process (n_dev, devs):
+ * one handle, chains sharded by global id in contiguous blocks (device i owns
+ * [i*C/n, (i+1)*C/n)), so it is a drop-in for run_render's thread-per-chain
+ * loop (core/driver.cpp:282-297) at 1..8 GPUs.  Exchanges are device to device
+ * over peer memory (NVLink/NVSwitch), stream-ordered: pooled adaptation after
+ * every lockstep step, quadtree visits at every m_refine barrier, b partials
+ * once, and the film every film_sync_steps lockstep steps (configs[4]: 4096;
+ * 0 = only at metrics rows and reads) -- film merge of core/film.cpp:22-27.
+ * Fixed runs are identical to the single-device handle; adaptive runs use the
+ * pooled rule (RAMLT_ADAPT_POOLED), also identical to one device.  Devices may
+ * repeat (two shards on one GPU: a functional test of the same path).
+ * n_dev == 1 returns a plain single-device handle on devs[0].  The per-shard
+ * plumbing calls (set_stream, film_device, adapt_*, visits_device, refine)
+ * return RAMLT_E_LOGIC on a multi-device handle. */
+RAMLT_API int ramlt_gpu_create_multi(const ramlt_scene_desc *scene, const ramlt_render_desc *desc, int32_t n_dev,
+                                     const int32_t *devs, uint32_t film_sync_steps, ramlt_gpu **out);
+RAMLT_API int ramlt_gpu_create_multi_from_text(const char *scene_text, const char *origin,
+                                               const ramlt_render_desc *desc, int32_t n_dev, const int32_t *devs,
+                                               uint32_t film_sync_steps, ramlt_gpu **out);
+
 /* estimate_b (driver.hpp:49, driver.cpp:31-57) over desc.b_samples samples
  * split into b_substreams independent substreams. */
 RAMLT_API int ramlt_gpu_estimate_b(ramlt_gpu *h, double *b, double *stderr_);
@@ -275,6 +295,11 @@ RAMLT_API int ramlt_gpu_refine(ramlt_gpu *h, int32_t keep_counts);
  * error_report(image, reference, 1e-2, luminance).rrmse (diagnostics.cpp:11-38).
  * Dimensions must match the render (std::invalid_argument otherwise). */
 RAMLT_API int ramlt_gpu_set_reference(ramlt_gpu *h, const float *rgb, int32_t width, int32_t height);
+/* error_report(to_image(b / at), reference, 1e-2, luminance).rrmse
+ * (core/diagnostics.cpp:11-38, the MetricsRow.rrmse of core/driver.cpp:265-272)
+ * of the handle's current film; NaN without a reference.  On a sharded handle
+ * (chains_total > chains) call it after the film all-reduce. */
+RAMLT_API int ramlt_gpu_rrmse(ramlt_gpu *h, uint64_t at, double *out);
 
 /* Diagnostic (no reference counterpart): closest-hit throughput of the scene's
  * triangle accelerator alone, for the roofline discussion in DESIGN.md.

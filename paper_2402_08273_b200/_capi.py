@@ -117,6 +117,10 @@ SIGNATURES = {
     "ramlt_scene_free": (None, [vp]),
     "ramlt_gpu_create": (C.c_int, [P(ramlt_scene_desc), P(ramlt_render_desc), P(H)]),
     "ramlt_gpu_create_from_text": (C.c_int, [C.c_char_p, C.c_char_p, P(ramlt_render_desc), P(H)]),
+    "ramlt_gpu_create_multi": (C.c_int, [P(ramlt_scene_desc), P(ramlt_render_desc), C.c_int32, P(C.c_int32),
+                                         C.c_uint32, P(H)]),
+    "ramlt_gpu_create_multi_from_text": (C.c_int, [C.c_char_p, C.c_char_p, P(ramlt_render_desc), C.c_int32,
+                                                   P(C.c_int32), C.c_uint32, P(H)]),
     "ramlt_gpu_last_create_error": (C.c_char_p, []),
     "ramlt_gpu_estimate_b": (C.c_int, [H, P(C.c_double), P(C.c_double)]),
     "ramlt_gpu_estimate_b_partials": (C.c_int, [H, C.c_uint64, C.c_uint64, P(C.c_double)]),
@@ -145,6 +149,7 @@ SIGNATURES = {
     "ramlt_gpu_refine_pending": (C.c_int, [H, P(C.c_int32)]),
     "ramlt_gpu_refine": (C.c_int, [H, C.c_int32]),
     "ramlt_gpu_set_reference": (C.c_int, [H, P(C.c_float), C.c_int32, C.c_int32]),
+    "ramlt_gpu_rrmse": (C.c_int, [H, C.c_uint64, P(C.c_double)]),
     "ramlt_gpu_trace_benchmark": (C.c_int, [H, C.c_uint64, P(C.c_double), P(C.c_uint64)]),
     "ramlt_gpu_last_error": (C.c_char_p, [H]),
     "ramlt_gpu_destroy": (None, [H]),

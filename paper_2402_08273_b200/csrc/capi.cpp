@@ -424,6 +424,30 @@ int ramlt_gpu_create_from_text(const char *text, const char *origin, const ramlt
     });
 }
 
+int ramlt_gpu_create_multi(const ramlt_scene_desc *scene, const ramlt_render_desc *desc, int32_t n_dev,
+                           const int32_t *devs, uint32_t film_sync_steps, ramlt_gpu **out) {
+    return guard(g_create_err, [&] {
+        if (!scene || !desc)
+            throw std::logic_error("null scene or render descriptor");
+        HostScene hs = ramlt_b200::from_desc(scene);
+        auto h = std::make_unique<ramlt_gpu>();
+        h->eng.reset(ramlt_b200::make_engine_multi(hs, *desc, n_dev, devs, film_sync_steps));
+        *out = h.release();
+    });
+}
+
+int ramlt_gpu_create_multi_from_text(const char *text, const char *origin, const ramlt_render_desc *desc,
+                                     int32_t n_dev, const int32_t *devs, uint32_t film_sync_steps, ramlt_gpu **out) {
+    return guard(g_create_err, [&] {
+        if (!desc)
+            throw std::logic_error("null render descriptor");
+        HostScene hs = ramlt_b200::parse_scene(text ? text : "", origin ? origin : "<string>");
+        auto h = std::make_unique<ramlt_gpu>();
+        h->eng.reset(ramlt_b200::make_engine_multi(hs, *desc, n_dev, devs, film_sync_steps));
+        *out = h.release();
+    });
+}
+
 const char *ramlt_gpu_last_create_error(void) { return g_create_err.c_str(); }
 
 #define RAMLT_H(body)                                                                              \
@@ -482,6 +506,7 @@ int ramlt_gpu_refine(ramlt_gpu *h, int32_t keep) { RAMLT_H(h->eng->refine_now(ke
 int ramlt_gpu_set_reference(ramlt_gpu *h, const float *rgb, int32_t w, int32_t ht) {
     RAMLT_H(h->eng->set_reference(rgb, w, ht));
 }
+int ramlt_gpu_rrmse(ramlt_gpu *h, uint64_t at, double *out) { RAMLT_H(*out = h->eng->rrmse(at)); }
 int ramlt_gpu_trace_benchmark(ramlt_gpu *h, uint64_t n, double *ms, uint64_t *hits) {
     RAMLT_H(h->eng->trace_benchmark(n, ms, hits));
 }

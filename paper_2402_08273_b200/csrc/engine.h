@@ -60,11 +60,20 @@ public:
     virtual void refine_now(bool keep_counts) = 0;
     virtual void trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) = 0;
     virtual void set_reference(const float *rgb, int width, int height) = 0;
+    // multi-device handle (multi.cu) plumbing
+    virtual void *stream_handle() = 0;
+    virtual double rrmse(uint64_t at) = 0;   // error_report rRMSE of this handle's film; NaN without a reference
+    // interval acceptance sums (accepted, proposals) of the metrics row flushed at `at`
+    virtual bool metrics_sums(uint64_t at, double *num, double *den) = 0;
 
     std::string last_error;
 };
 
 EngineBase *make_engine_f32(const HostScene &scene, const ramlt_render_desc &desc);
 EngineBase *make_engine_f64(const HostScene &scene, const ramlt_render_desc &desc);
+// One handle over several devices (chains sharded by global id, pooled adaptation
+// and quadtree visits exchanged every lockstep step, film every film_sync steps).
+EngineBase *make_engine_multi(const HostScene &scene, const ramlt_render_desc &desc, int n_dev, const int *devs,
+                              uint32_t film_sync_steps);
 
 }  // namespace ramlt_b200

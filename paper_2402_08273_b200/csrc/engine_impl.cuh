@@ -97,6 +97,19 @@ public:
     void trace_benchmark(uint64_t n_rays, double *ms, uint64_t *hits) override;
     void set_reference(const float *rgb, int width, int height) override;
     double rrmse_now(uint64_t at);
+    void *stream_handle() override { return stream_; }
+    double rrmse(uint64_t at) override {
+        return ref_img_.p && at > 0 ? rrmse_now(at) : std::numeric_limits<double>::quiet_NaN();
+    }
+    bool metrics_sums(uint64_t at, double *num, double *den) override {
+        for (auto it = metrics_.rbegin(); it != metrics_.rend(); ++it)
+            if (static_cast<uint64_t>((*it)[1]) == at) {
+                *num = (*it)[4];
+                *den = (*it)[5];
+                return true;
+            }
+        return false;
+    }
     DBuf<float> ref_img_;      // RenderConfig::reference (driver.hpp:38) for the metrics rRMSE
     DBuf<double> rrmse_part_;
     void refine_now(bool keep_counts) override {
@@ -203,7 +216,7 @@ private:
     uint64_t b_n_ = 0;
     bool b_set_ = false, chains_ready_ = false;
     uint64_t done_ = 0, next_refine_, next_metrics_;
-    std::vector<std::array<double, 4>> metrics_;
+    std::vector<std::array<double, 6>> metrics_;   // time, at, rrmse, acceptance, accepted sum, proposals
     std::chrono::steady_clock::time_point t0_;
     bool t0_set_ = false;
     uint64_t launches_ = 0;
@@ -1048,7 +1061,8 @@ template <class R> void EngineT<R>::adapt_apply() {
     if (ctl_ == 0 || adapt_ != 1)
         return;
     rd::RegionArrays ra = regions();
-    rd::k_adapt_pool_apply<R><<<148, 256, 0, stream_>>>(ra, ktab_.p, adaptcfg(), tracebuf());
+    rd::k_adapt_pool_apply<R><<<148, 256, 0, stream_>>>(ra, ktab_.p, adaptcfg(), tracebuf(),
+                                                        exchange_interval_ ? n_regions_host_ : 0);
     rd::k_reset_touched<<<1, 1, 0, stream_>>>(n_touched_.p);
     launches_ += 2;
     RAMLT_CUDA(cudaGetLastError());
@@ -1131,7 +1145,7 @@ template <class R> void EngineT<R>::flush_metrics(uint64_t at) {
     // row.rrmse (core/driver.cpp:265-272): NaN unless a reference image is set;
     // a sharded handle holds a partial film, so its rows stay NaN
     double rr = (ref_img_.p && Ctot_ == C_) ? rrmse_now(at) : std::numeric_limits<double>::quiet_NaN();
-    metrics_.push_back({t, static_cast<double>(at), rr, r[5] > 0 ? r[1] / r[5] : 0.0});
+    metrics_.push_back({t, static_cast<double>(at), rr, r[5] > 0 ? r[1] / r[5] : 0.0, r[1], r[5]});
 }
 
 template <class R> void EngineT<R>::set_reference(const float *rgb, int width, int height) {
@@ -1172,6 +1186,15 @@ template <class R> void EngineT<R>::run(uint64_t mutations) {
     }
     finalized_ = false;
     const uint64_t target = done_ + mutations;
+    // Sharded quadtree runs defer the refine to the caller (visit all-reduce,
+    // then ramlt_gpu_refine): a run must end at the refine boundary, never step
+    // past it on the old partition (distributed.py chunks its runs this way).
+    if (exchange_interval_ && (pkind_ == 2 || pkind_ == 4)) {
+        if (refine_pending_ && mutations > 0)
+            throw std::logic_error("sharded run: refine pending (all-reduce visits and call ramlt_gpu_refine first)");
+        if (target > next_refine_)
+            throw std::logic_error("sharded run crosses a refine boundary: end run() at multiples of m_refine");
+    }
     const uint32_t fuse = d_.steps_per_launch ? d_.steps_per_launch : 256;
     while (done_ < target) {
         uint64_t boundary = std::min({target, next_refine_, next_metrics_});

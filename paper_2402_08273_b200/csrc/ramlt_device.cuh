@@ -479,7 +479,7 @@ template <class R> struct BvhTrav {
         d = d_;
         any = any_hit;
         best = lim;
-        key = 0x7fffffff;
+        key = -1;   // no winner yet: a hit at exactly t == lim loses the tie (reference: visible iff t >= dist - eps)
         spos = -1;
         pos = -1;
         for (int i = 0; i < s.nsph; ++i) {
@@ -656,7 +656,7 @@ __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> 
     if constexpr (G == 0) {
         // every lane of a group traverses the same ray: identical results, no reduction
         R best = M<R>::inf();
-        int key = 0x7fffffff, spos = -1;
+        int key = -1, spos = -1;
         for (int i = 0; i < s.nsph; ++i) {
             R t;
             if (hit_sphere(s.sph[i], o, d, t) && t < best) {
@@ -748,7 +748,7 @@ __device__ __forceinline__ bool visible(const SceneView<R> &s, V3<R> a, V3<R> b,
         }
         if (!occ) {
             R best = lim;
-            int key = 0x7fffffff;
+            int key = -1;   // strict t < lim occludes, as the brute-force scan
             occ = bvh_trace(s, a, d, lim, best, key, true) >= 0;
         }
         return !occ;

@@ -1111,12 +1111,18 @@ __global__ void k_adapt_pool_accum(const int *vreg, const double *va, int C, lon
 }
 
 // Pooled rule, phase 2: one update per touched region.
+// n_scan > 0 (sharded runs, after the SUM/SUM/MAX all-reduce of x_cnt/x_fx/x_last):
+// every region in [0, n_scan) with pooled visits is updated, not only the ones
+// this rank's chains touched -- a region visited only on another rank must take
+// the same lambda step here, and its exchanged counts must be consumed.
 template <class R>
-__global__ void k_adapt_pool_apply(RegionArrays ra, KernTab<R> *ktab, AdaptCfg cfg, TraceBuf tb) {
-    unsigned nt = *ra.n_touched;
+__global__ void k_adapt_pool_apply(RegionArrays ra, KernTab<R> *ktab, AdaptCfg cfg, TraceBuf tb, int n_scan) {
+    unsigned nt = n_scan > 0 ? static_cast<unsigned>(n_scan) : *ra.n_touched;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nt; i += gridDim.x * blockDim.x) {
-        int r = static_cast<int>(ra.touched_list[i]);
+        int r = n_scan > 0 ? static_cast<int>(i) : static_cast<int>(ra.touched_list[i]);
         unsigned long long cnt = ra.x_cnt[r], fx = ra.x_fx[r], last = ra.x_last[r];
+        if (n_scan > 0 && cnt == 0)
+            continue;
         ra.x_cnt[r] = 0;
         ra.x_fx[r] = 0;
         ra.x_last[r] = 0;

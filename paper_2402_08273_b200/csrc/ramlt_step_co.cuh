@@ -31,7 +31,7 @@ template <class R, bool BVH>
 __device__ __forceinline__ int trace_ray(const SceneView<R> &s, const RayReq<R> &r, R &t_out) {
     if constexpr (BVH) {
         R best = r.lim;
-        int key = 0x7fffffff, spos = -1;
+        int key = -1, spos = -1;   // a hit at exactly t == lim is not below lim
         for (int i = 0; i < s.nsph; ++i) {
             R t;
             if (hit_sphere(s.sph[i], r.o, r.d, t) && t < best) {

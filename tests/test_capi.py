@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     out = os.popen(f"nm -D --defined-only {_capi.LIB_PATH}").read()
     exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
     assert {s for s in exported if s.startswith("ramlt_")} == set(names)
-    assert lib.ramlt_gpu_abi_version() == 1
+    assert lib.ramlt_gpu_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
