@@ -110,18 +110,71 @@ def dist_env():
     return world, rank, local
 
 
-def oracle_rays_per_mutation(wl: dict, scene_text: str) -> float:
-    """R_m: reference-equivalent ray casts (closest-hit + visibility) per mutation,
-    counted by the CPU oracle on a small sample of the same variant and scene
-    (SURVEY.md §8(d))."""
-    from oracle.abi import OracleConfig, OracleLib
-    per = 60 if wl["scene"] == "clusters" else 300
-    cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=64,
-                       mutations=64 * per, width=wl["width"], height=wl["height"],
-                       max_vertices=wl["max_vertices"], b_samples=20000, seed=3, rng="philox",
-                       adapt_mode="pooled", m_refine=64 * 100, m_split=500)
-    o = OracleLib().render(scene_text, cfg)
-    return (o.stats.rays_closest + o.stats.rays_visibility) / max(o.stats.total_mutations, 1)
+def reference_rays_per_mutation(wl: dict, scene_text: str, threads: int):
+    """R_m: reference ray casts (closest-hit + visibility) per mutation, counted
+    by the UNMODIFIED reference on the benched scene itself (oracle/_ref
+    libramlt_ref_log.so: link-time --wrap counters on SceneModel::intersect /
+    visible, counted inside the mutation loop only), with
+    chains = host threads.  Falls back to the restatement oracle when the
+    reference was not built."""
+    from oracle.abi import OracleConfig, OracleLib, RefLib, REF_LOG_SO
+    big = wl["scene"] == "clusters"
+    per = 16 if big else 256
+    cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=threads,
+                       mutations=threads * per, width=wl["width"], height=wl["height"],
+                       max_vertices=wl["max_vertices"], b_samples=16 if big else 4096, seed=3,
+                       metrics_interval=threads * per)
+    if os.path.exists(REF_LOG_SO):
+        o = RefLib(log=True).render(scene_text, cfg, log_steps=1)
+        src = (f"counted by the unmodified reference on the benched scene ({threads} threads x {per} "
+               f"mutations, loop-only --wrap counters)")
+    else:
+        cfg.chains, cfg.mutations = 8, 8 * per
+        o = OracleLib().render(scene_text, cfg, log_steps=1)
+        src = f"counted by the restatement oracle on the benched scene (8 chains x {per} mutations)"
+    return (o.stats.rays_closest + o.stats.rays_visibility) / max(o.stats.total_mutations, 1), src
+
+
+def relmse_vs_reference(args):
+    """relMSE vs CPU (BASELINE.json metric): the f32 engine against the
+    unmodified reference at EQUAL mutation counts on a configuration the
+    reference can run as specified -- C1 (Cornell box, 1,024 chains, 256^2,
+    path length 8, RA-quadtree lens).  error_report rRMSE (core/diagnostics.cpp:
+    11-38, eps 1e-2, luminance) of the GPU image against reference seed 1,
+    next to the reference's own seed-to-seed rRMSE (seed 2 vs seed 1) measured
+    in the same run; tolerance 1.5x that noise."""
+    import numpy as np
+    from oracle.abi import OracleConfig, RefLib, REF_SO, ref_error_report
+    from paper_2402_08273_b200 import Engine, RenderConfig, scenes
+    if not os.path.exists(REF_SO):
+        return {"unavailable": "oracle/_ref not built"}
+    text = scenes.cornell_box()
+    wl = WORKLOADS["c1"]
+    M = args.relmse_mutations
+    common = dict(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=wl["chains"], mutations=M,
+                  width=wl["width"], height=wl["height"], max_vertices=wl["max_vertices"], b_samples=1_000_000,
+                  metrics_interval=M)
+    lib = RefLib(log=False)
+    t0 = time.perf_counter()
+    r1 = lib.render(text, OracleConfig(**common, seed=1))
+    r2 = lib.render(text, OracleConfig(**common, seed=2))
+    t_ref = time.perf_counter() - t0
+    eng = Engine(text, RenderConfig(**common, seed=3, precision="f32", rng="philox"))
+    eng.set_reference(r1.image)
+    eng.render()
+    err = eng.rrmse(M)            # the engine's own error_report (k_rrmse_partial) against the reference image
+    s = eng.stats()
+    eng.close()
+    noise = ref_error_report(lib, r2.image, r1.image)
+    return {"value": err, "noise": noise, "tolerance": 1.5 * noise, "ratio": err / noise,
+            "pass": bool(err <= 1.5 * noise),
+            "acceptance": {"gpu": s.mean_acceptance, "reference_seed1": r1.stats.mean_acceptance,
+                           "reference_seed2": r2.stats.mean_acceptance},
+            "b": {"gpu": s.b, "reference": r1.stats.b},
+            "config": (f"C1 Cornell box, {wl['chains']} chains, {wl['width']}^2, max_vertices {wl['max_vertices']}, "
+                       f"{wl['strategy']} {wl['perturbation']}, {M} mutations each; GPU f32/Philox vs the "
+                       f"unmodified reference (seeds 1, 2; {wl['chains']} threads, {t_ref:.1f} s)"),
+            "metric": "error_report rRMSE (luminance, eps 1e-2) vs reference seed 1"}
 
 
 def cpu_reference_run(wl: dict, scene_text: str, mutations: int, threads: int):
@@ -145,12 +198,18 @@ def cpu_reference_run(wl: dict, scene_text: str, mutations: int, threads: int):
     return out.stats.total_mutations / t, kind, cores, t, cfg.chains
 
 
+def _acc_sums(eng):
+    """(accepted-probability sum, perturbation proposals) of this rank so far."""
+    s = eng.stats()
+    return s.mean_acceptance * s.perturbation_proposals, float(s.perturbation_proposals)
+
+
 def run_ours(args, wl, scene_text):
     import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2402_08273_b200 import Engine, RenderConfig
-    from paper_2402_08273_b200.distributed import ShardPlan, sharded_sync, all_gather_b
+    from paper_2402_08273_b200.distributed import ShardPlan, ShardedRender
 
     world, rank, local = dist_env()
     local = local % max(torch.cuda.device_count(), 1)
@@ -165,33 +224,50 @@ def run_ours(args, wl, scene_text):
             dist.init_process_group(backend)
     C = wl["chains"]
     plan = ShardPlan(C, world, rank)
-    total_steps = args.warmup + args.steps
     stream = torch.cuda.current_stream()
-    cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=plan.count,
-                       chains_total=C, chain_offset=plan.offset,
+    cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=C,
                        mutations=C * wl["steps_per_chain"], width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=1,
                        precision="f32", rng="philox", device=local, profile_kernels=True,
                        metrics_interval=C * wl["steps_per_chain"])
-    eng = Engine(wl["scene_text"], cfg)
-    eng.set_stream(stream.cuda_stream)
-    # prologue: b over substreams (sharded, gathered in substream order), chain init
-    if world > 1:
-        all_gather_b(eng, cfg, plan)
-        eng.set_exchange_interval(1)
-    else:
-        eng.estimate_b()
-    eng.init_chains()
+    # one process per GPU: chains shard by global id; pooled adaptation exchanged
+    # every lockstep step, quadtree visits at every refine barrier, the film every
+    # 2^12 lockstep steps (configs[4]) -- distributed.ShardedRender
+    sr = ShardedRender(wl["scene_text"], cfg, exchange_every=1, film_sync_steps=4096)
+    eng = sr.engine
+    sr.estimate_b()
+    sr.init_chains()
 
     def step():
-        eng.run(C)
-        if world > 1:
-            sharded_sync(eng)
+        sr.run(C)
 
+    def window_acceptance(a0, n0):
+        a1, n1 = _acc_sums(eng)
+        t = torch.tensor([a1 - a0, n1 - n0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t[0] / t[1]) if t[1] > 0 else 0.0, (a1, n1)
+
+    # burn-in (outside the timed region): the adaptive controller starts at
+    # lambda_init = 1 (sigma = e^0.5 rad) far from alpha* = 0.5; step until the
+    # pooled window acceptance is within 0.1 of the target (steady state), at
+    # most burnin_max steps.  Fixed strategies need none.
+    burn, burn_acc = 0, None
+    sums = _acc_sums(eng)
+    if cfg.strategy != "fixed":
+        target = cfg.target_acceptance
+        while burn < args.burnin_max:
+            step()
+            burn += 1
+            burn_acc, sums = window_acceptance(*sums)
+            if burn >= 4 and abs(burn_acc - target) <= 0.1:
+                break
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    sums = _acc_sums(eng)
     s0 = eng.stats()
+    d0 = sr.done
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -204,27 +280,35 @@ def run_ours(args, wl, scene_text):
         else:
             # one call: the engine batches the lockstep steps of a span itself
             # (cooperative launches for adaptive runs with few chains)
-            eng.run(C * args.steps)
+            sr.run(C * args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
         dist.barrier()
     s1 = eng.stats()
+    acc_window, _ = window_acceptance(*sums)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    muts = args.steps * C
+    muts = sr.done - d0   # = steps x C (N > 1: whole lockstep steps of the canonical spans)
     value = muts / (ms_max / 1e3)
     launches = s1.kernel_launches - s0.kernel_launches
     step_ms = (s1.step_kernel_ms - s0.step_kernel_ms)
     step_launches = s1.step_kernel_launches - s0.step_kernel_launches
     rays_dev = (s1.rays_closest + s1.rays_visibility) - (s0.rays_closest + s0.rays_visibility)
+    rays_t = torch.tensor([float(rays_dev)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(rays_t, op=dist.ReduceOp.SUM)
+    k = eng.chain_lengths()
+    k_bar = float(k.mean()) if k.size else float("nan")
     eng.close()
     return dict(value=value, ms=ms_max, launches=launches, step_ms=step_ms,
-                step_launches=step_launches, rays_dev=rays_dev, muts=muts, clocks=clk.summary(),
-                world=world, rank=rank, local=local, mutations_per_rank=args.steps * plan.count)
+                step_launches=step_launches, rays_dev=float(rays_t.item()), muts=muts, clocks=clk.summary(),
+                world=world, rank=rank, local=local, mutations_per_rank=muts * plan.count / C,
+                acceptance=acc_window, burnin=dict(steps=burn, acceptance=burn_acc, max=args.burnin_max),
+                k_bar=k_bar)
 
 
 def run_e2e(args, wl):
@@ -433,6 +517,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=0, help="mutations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-relmse", action="store_true", help="skip the relMSE-vs-reference leg (C1)")
+    ap.add_argument("--relmse-mutations", type=int, default=1 << 24)
+    ap.add_argument("--burnin-max", type=int, default=64,
+                    help="max untimed burn-in steps until the window acceptance is within 0.1 of the target")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
@@ -484,11 +572,8 @@ def main():
     if res["rank"] != 0:
         return
     peaks = load_peaks()
-    rm_text = wl["scene_text"]
-    if wl["scene"] == "clusters":
-        from paper_2402_08273_b200 import scenes as _sc
-        rm_text = _sc.cluster_room(n_tris=4096)
-    r_m = oracle_rays_per_mutation(wl, rm_text)
+    threads = os.cpu_count() or 1
+    r_m, r_m_src = reference_rays_per_mutation(wl, wl["scene_text"], threads)
     from paper_2402_08273_b200 import parse_scene
     n_mat, n_sph, n_tri, n_emi = parse_scene(wl["scene_text"]).counts
     flop_per_mut = r_m * (45.0 * n_tri + 20.0 * n_sph)
@@ -515,14 +600,14 @@ def main():
                     "peak_source": "nominal FP32 issue: 148 SM x 128 lanes x 2 x sm_max_mhz "
                                    "(MEASURED_PEAKS.json has no FP32 figure)",
                     "work_per_unit": f"R_m x (45 N_tri + 20 N_sph) = {r_m:.3f} x (45x{n_tri} + 20x{n_sph}) "
-                                     f"= {flop_per_mut:.0f} FLOP/mutation (R_m oracle-counted)"}
+                                     f"= {flop_per_mut:.0f} FLOP/mutation (R_m: {r_m_src})"}
     else:
         # B = R_m x B_ray + B_state per mutation, B_ray = one
         # BVH root-to-leaf descent (64 B per level) + 4 triangles x 48 B
         import math
         levels = max(1, math.ceil(math.log2(max(n_tri / 4.0, 2.0))))
         b_ray = 64.0 * levels + 4 * 48.0
-        k_bar = 6.0
+        k_bar = res["k_bar"]   # measured: mean current path length over all chains after the timed steps
         b_state = 2.0 * (16.0 * k_bar + 48.0) + 32.0
         bytes_per_mut = r_m * b_ray + b_state
         ach = per_launch_muts * bytes_per_mut / mean_launch_s / 1e9
@@ -532,7 +617,7 @@ def main():
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s",
                     "work_per_unit": f"R_m x B_ray + B_state = {r_m:.3f} x {b_ray:.0f} B + {b_state:.0f} B "
                                      f"= {bytes_per_mut:.0f} B/mutation (B_ray: {levels} BVH levels x 64 B + "
-                                     f"4 x 48 B; R_m oracle-counted on a 4096-triangle sample of the scene)"}
+                                     f"4 x 48 B; k_bar = {k_bar:.2f} measured; R_m: {r_m_src})"}
     kname = ("k_step_co (coroutine chain-step kernel, BVH traversal with dynamic ray fetch)"
              if wl["scene"] == "clusters" else "k_step (chain-step megakernel)")
     roofline.update({"kernel": kname,
@@ -544,6 +629,9 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{sample} mutations, chains = {chains} host threads, loop-only time "
                          f"{t:.2f} s (core/driver.cpp:246,262)"}
+    rel = None
+    if not args.no_relmse and res["world"] == 1:
+        rel = relmse_vs_reference(args)
     e2e_v, h2d, d2h, _ = run_e2e(args, wl) if res["world"] == 1 else res["e2e"]
     e2e_steps = max(args.steps, wl["e2e_steps"])
     steps = args.steps
@@ -552,8 +640,13 @@ def main():
         "steps": steps, "warmup": args.warmup, "ms_per_step": res["ms"] / steps,
         "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded stand-in scene, BASELINE.json config)", "config": config,
-        "rays_per_s": {"device": res["rays_dev"] / (res["ms"] / 1e3) * res["world"],
-                       "reference_equivalent": res["value"] * r_m, "r_m": r_m},
+        "rays_per_s": {"device": res["rays_dev"] / (res["ms"] / 1e3),
+                       "device_per_mutation": res["rays_dev"] / res["muts"],
+                       "reference_equivalent": res["value"] * r_m, "r_m": r_m, "r_m_source": r_m_src},
+        "acceptance": {"value": res["acceptance"], "target": 0.5,
+                       "window": "mean perturbation acceptance over the timed steps, all ranks",
+                       "burnin": res["burnin"]},
+        "relmse": rel,
         "roofline": roofline, "cpu_baseline": cpu,
         "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                 "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,

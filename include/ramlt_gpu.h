@@ -237,6 +237,16 @@ RAMLT_API int ramlt_gpu_init_chains(ramlt_gpu *h);
  * the reference does (per-chain steps = span / chains, +1 for the first
  * span % chains chains), refining and flushing metrics at the barriers. */
 RAMLT_API int ramlt_gpu_run(ramlt_gpu *h, uint64_t mutations);
+/* The span loop of run_render (core/driver.cpp:282-312) one piece at a time,
+ * for sharded callers that exchange state between lockstep steps: runs up to
+ * n lockstep steps of the CANONICAL spans (boundaries at the configured total
+ * and the m_refine / metrics_interval barriers -- exactly the spans of
+ * ramlt_gpu_run(desc.mutations), so every chain's step count and decisions
+ * are independent of n), returning early at the end of a span.  *done = the
+ * global mutation count reached, *executed = lockstep steps run (0 while a
+ * sharded quadtree refine is pending).  Do not mix with ramlt_gpu_run inside
+ * an open span (RAMLT_E_LOGIC). */
+RAMLT_API int ramlt_gpu_run_steps(ramlt_gpu *h, uint32_t n, uint64_t *done, uint32_t *executed);
 
 /* run_render in one call: estimate_b (unless set), init, run(desc.mutations)
  * or the wall-clock budget, finalise.  Synchronous. */
@@ -266,6 +276,15 @@ RAMLT_API int ramlt_gpu_read_metrics(ramlt_gpu *h, double *rows, uint64_t cap, u
 RAMLT_API int ramlt_gpu_read_decisions(ramlt_gpu *h, uint32_t K, double *a, uint8_t *flags);
 /* PartitionIndex::dump text (partition.hpp:30, partition.cpp:104-245). */
 RAMLT_API int ramlt_gpu_read_partition(ramlt_gpu *h, char *buf, uint64_t cap);
+/* The same dump with caller-supplied per-region visit counts (n = region
+ * count): a sharded caller (one process per GPU) passes the SUM over ranks of
+ * ramlt_gpu_visits_device, since leaf visits are split over the shards between
+ * refine barriers. */
+RAMLT_API int ramlt_gpu_read_partition_visits(ramlt_gpu *h, const uint64_t *visits, uint64_t n, char *buf,
+                                              uint64_t cap);
+/* Current path length k (vertices, camera included; Path::vertices.size(),
+ * core/path.hpp:28-35) of every chain of the handle, in chain order. */
+RAMLT_API int ramlt_gpu_read_chain_lengths(ramlt_gpu *h, int32_t *k);
 
 /* ---- multi-GPU plumbing (chains shard across ranks) ----
  * The caller (e.g. torch.distributed over NCCL) owns the collective; the

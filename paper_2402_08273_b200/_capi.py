@@ -128,6 +128,7 @@ SIGNATURES = {
     "ramlt_gpu_set_b": (C.c_int, [H, C.c_double]),
     "ramlt_gpu_init_chains": (C.c_int, [H]),
     "ramlt_gpu_run": (C.c_int, [H, C.c_uint64]),
+    "ramlt_gpu_run_steps": (C.c_int, [H, C.c_uint32, P(C.c_uint64), P(C.c_uint32)]),
     "ramlt_gpu_render": (C.c_int, [H]),
     "ramlt_gpu_synchronize": (C.c_int, [H]),
     "ramlt_gpu_read_stats": (C.c_int, [H, P(ramlt_stats)]),
@@ -139,6 +140,8 @@ SIGNATURES = {
     "ramlt_gpu_read_metrics": (C.c_int, [H, P(C.c_double), C.c_uint64, P(C.c_uint64)]),
     "ramlt_gpu_read_decisions": (C.c_int, [H, C.c_uint32, P(C.c_double), P(C.c_uint8)]),
     "ramlt_gpu_read_partition": (C.c_int, [H, C.c_char_p, C.c_uint64]),
+    "ramlt_gpu_read_partition_visits": (C.c_int, [H, P(C.c_uint64), C.c_uint64, C.c_char_p, C.c_uint64]),
+    "ramlt_gpu_read_chain_lengths": (C.c_int, [H, P(C.c_int32)]),
     "ramlt_gpu_set_stream": (C.c_int, [H, vp]),
     "ramlt_gpu_film_device": (C.c_int, [H, P(P(C.c_double)), P(C.c_uint64)]),
     "ramlt_gpu_adapt_exchange": (C.c_int, [H, P(P(C.c_uint64)), P(P(C.c_uint64)),

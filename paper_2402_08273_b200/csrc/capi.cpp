@@ -467,6 +467,9 @@ int ramlt_gpu_reduce_b(ramlt_gpu *h, const double *p, uint64_t n, double *b, dou
 int ramlt_gpu_set_b(ramlt_gpu *h, double b) { RAMLT_H(h->eng->set_b(b)); }
 int ramlt_gpu_init_chains(ramlt_gpu *h) { RAMLT_H(h->eng->init_chains()); }
 int ramlt_gpu_run(ramlt_gpu *h, uint64_t m) { RAMLT_H(h->eng->run(m)); }
+int ramlt_gpu_run_steps(ramlt_gpu *h, uint32_t n, uint64_t *done, uint32_t *executed) {
+    RAMLT_H(uint64_t d = h->eng->run_steps(n, executed); if (done) *done = d);
+}
 int ramlt_gpu_render(ramlt_gpu *h) { RAMLT_H(h->eng->render()); }
 int ramlt_gpu_synchronize(ramlt_gpu *h) { RAMLT_H(h->eng->synchronize()); }
 int ramlt_gpu_read_stats(ramlt_gpu *h, ramlt_stats *o) { RAMLT_H(h->eng->read_stats(o)); }
@@ -486,6 +489,13 @@ int ramlt_gpu_read_metrics(ramlt_gpu *h, double *rows, uint64_t cap, uint64_t *n
 }
 int ramlt_gpu_read_decisions(ramlt_gpu *h, uint32_t K, double *a, uint8_t *f) {
     RAMLT_H(h->eng->read_decisions(K, a, f));
+}
+int ramlt_gpu_read_chain_lengths(ramlt_gpu *h, int32_t *k) { RAMLT_H(h->eng->read_chain_lengths(k)); }
+int ramlt_gpu_read_partition_visits(ramlt_gpu *h, const uint64_t *visits, uint64_t n, char *buf, uint64_t cap) {
+    RAMLT_H(std::string s = h->eng->read_partition_visits(visits, n); if (buf && cap) {
+        std::strncpy(buf, s.c_str(), cap - 1);
+        buf[cap - 1] = '\0';
+    });
 }
 int ramlt_gpu_read_partition(ramlt_gpu *h, char *buf, uint64_t cap) {
     RAMLT_H(std::string s = h->eng->read_partition(); if (buf && cap) {

@@ -39,6 +39,7 @@ public:
     virtual void set_b(double b) = 0;
     virtual void init_chains() = 0;
     virtual void run(uint64_t mutations) = 0;
+    virtual uint64_t run_steps(uint32_t n, uint32_t *executed) = 0;
     virtual void render() = 0;
     virtual void synchronize() = 0;
     virtual void read_stats(ramlt_stats *out) = 0;
@@ -49,7 +50,10 @@ public:
     virtual uint64_t read_trace(ramlt_trace_row *rows, uint64_t cap) = 0;
     virtual uint64_t read_metrics(double *rows, uint64_t cap) = 0;
     virtual void read_decisions(uint32_t K, double *a, uint8_t *flags) = 0;
+    virtual void read_chain_lengths(int32_t *k) = 0;
     virtual std::string read_partition() = 0;
+    // the dump with caller-supplied per-region visit counts (sharded runs: the SUM over shards)
+    virtual std::string read_partition_visits(const uint64_t *visits, uint64_t n) = 0;
     virtual void set_stream(void *stream) = 0;
     virtual void film_device(double **film, uint64_t *n) = 0;
     virtual void adapt_exchange(uint64_t **cnt, uint64_t **fx, uint64_t **last, uint64_t *n) = 0;

@@ -21,8 +21,10 @@ namespace ramlt_b200 {
 #define RAMLT_CUDA(x)                                                                              \
     do {                                                                                           \
         cudaError_t e_ = (x);                                                                      \
-        if (e_ != cudaSuccess)                                                                     \
+        if (e_ != cudaSuccess) {                                                                   \
+            cudaGetLastError(); /* a failed launch must not resurface at the next check */         \
             throw CudaError(std::string("cuda: ") + cudaGetErrorString(e_) + " at " #x);           \
+        }                                                                                          \
     } while (0)
 
 template <class T> struct DBuf {
@@ -61,6 +63,7 @@ public:
     }
     void init_chains() override;
     void run(uint64_t mutations) override;
+    uint64_t run_steps(uint32_t n, uint32_t *executed) override;
     void render() override;
     void synchronize() override { RAMLT_CUDA(cudaStreamSynchronize(stream_)); }
     void read_stats(ramlt_stats *out) override;
@@ -71,7 +74,12 @@ public:
     uint64_t read_trace(ramlt_trace_row *rows, uint64_t cap) override;
     uint64_t read_metrics(double *rows, uint64_t cap) override;
     void read_decisions(uint32_t K, double *a, uint8_t *flags) override;
-    std::string read_partition() override;
+    void read_chain_lengths(int32_t *k) override {
+        RAMLT_CUDA(cudaStreamSynchronize(stream_));
+        RAMLT_CUDA(cudaMemcpy(k, klen_.p, static_cast<size_t>(C_) * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    std::string read_partition() override { return read_partition_visits(nullptr, 0); }
+    std::string read_partition_visits(const uint64_t *visits, uint64_t n) override;
     void set_stream(void *stream) override {
         stream_ = static_cast<cudaStream_t>(stream);
         own_stream_ = false;
@@ -216,6 +224,13 @@ private:
     uint64_t b_n_ = 0;
     bool b_set_ = false, chains_ready_ = false;
     uint64_t done_ = 0, next_refine_, next_metrics_;
+    // run_steps: the open span of the canonical span loop (boundaries at the
+    // configured total, refine and metrics barriers -- what run(d.mutations) uses)
+    bool span_open_ = false;
+    uint64_t sp_start_ = 0, sp_end_ = 0;
+    unsigned long long sp_per_ = 0, sp_rem_ = 0;
+    int sp_steps_ = 0, sp_j_ = 0;
+    void span_boundary();
     std::vector<std::array<double, 6>> metrics_;   // time, at, rrmse, acceptance, accepted sum, proposals
     std::chrono::steady_clock::time_point t0_;
     bool t0_set_ = false;
@@ -970,8 +985,10 @@ bool EngineT<R>::launch_coop(int j0, int j1, unsigned long long span_start, unsi
     if (coop_state_ == 0 || j1 <= j0)
         return coop_state_ != 0 && j1 <= j0;
     if (const char *v = std::getenv("RAMLT_COOP"))
-        if (std::string(v) == "0")
+        if (std::string(v) == "0") {
             coop_state_ = 0;
+            return false;
+        }
     void (*kern)(rd::StepParams<R>, rd::CoopArgs<R>) = nullptr;
 #define RAMLT_PICK(RK)                                                                              \
     switch (use_bvh_ ? 0 : G_) {                                                                    \
@@ -1179,6 +1196,8 @@ template <class R> double EngineT<R>::rrmse_now(uint64_t at) {
 template <class R> void EngineT<R>::run(uint64_t mutations) {
     if (!chains_ready_)
         throw std::logic_error("run before init_chains");
+    if (span_open_)
+        throw std::logic_error("run() inside a span opened by run_steps(): finish it with run_steps");
     if (!t0_set_) {
         RAMLT_CUDA(cudaStreamSynchronize(stream_));
         t0_ = std::chrono::steady_clock::now();
@@ -1221,19 +1240,91 @@ template <class R> void EngineT<R>::run(uint64_t mutations) {
             }
         }
         done_ += span;
-        if (done_ == next_refine_) {
-            if (exchange_interval_ && (pkind_ == 2 || pkind_ == 4))
-                refine_pending_ = true;   // caller all-reduces visits, then ramlt_gpu_refine
-            else
-                refine();
-            next_refine_ += d_.m_refine;
-        }
-        if (done_ == next_metrics_ || done_ == d_.mutations) {
-            flush_metrics(done_);
-            next_metrics_ = done_ + d_.metrics_interval;
-        }
+        span_boundary();
     }
     fold();
+}
+
+// Barrier work at the end of a span (core/driver.cpp:298-312): refine, metrics row.
+template <class R> void EngineT<R>::span_boundary() {
+    if (done_ == next_refine_) {
+        if (exchange_interval_ && (pkind_ == 2 || pkind_ == 4))
+            refine_pending_ = true;   // caller all-reduces visits, then ramlt_gpu_refine
+        else
+            refine();
+        next_refine_ += d_.m_refine;
+    }
+    if (done_ == next_metrics_ || done_ == d_.mutations) {
+        flush_metrics(done_);
+        next_metrics_ = done_ + d_.metrics_interval;
+    }
+}
+
+// Advance up to n lockstep steps of the canonical span loop -- the spans
+// run(d.mutations) would use, so per-chain step counts (span % chains extra
+// steps to the first chains, core/driver.cpp:283-291) do not depend on how
+// often the caller stops -- returning early at the end of the current span
+// (a barrier: refine / metrics row / total).  Sharded callers exchange between
+// calls; with a refine pending (quadtree, exchange mode) no step runs until the
+// caller has all-reduced the visits and called ramlt_gpu_refine.  Returns the
+// global mutation count reached; *executed = lockstep steps run.
+template <class R> uint64_t EngineT<R>::run_steps(uint32_t n, uint32_t *executed) {
+    if (!chains_ready_)
+        throw std::logic_error("run before init_chains");
+    if (!t0_set_) {
+        RAMLT_CUDA(cudaStreamSynchronize(stream_));
+        t0_ = std::chrono::steady_clock::now();
+        t0_set_ = true;
+    }
+    finalized_ = false;
+    if (executed)
+        *executed = 0;
+    if (n == 0 || (!span_open_ && refine_pending_))
+        return done_;
+    const uint32_t fuse = d_.steps_per_launch ? d_.steps_per_launch : 256;
+    if (!span_open_) {
+        uint64_t end = done_ < d_.mutations ? d_.mutations : std::numeric_limits<uint64_t>::max();
+        end = std::min({end, next_refine_, next_metrics_});
+        const uint64_t span = end - done_;
+        sp_start_ = done_;
+        sp_end_ = end;
+        sp_per_ = span / static_cast<uint64_t>(Ctot_);
+        sp_rem_ = span % static_cast<uint64_t>(Ctot_);
+        sp_steps_ = static_cast<int>(sp_per_ + (sp_rem_ ? 1 : 0));
+        sp_j_ = 0;
+        span_open_ = true;
+    }
+    const int j1 = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(sp_steps_),
+                                                        static_cast<uint64_t>(sp_j_) + n));
+    if (ctl_ == 0) {
+        for (int j = sp_j_; j < j1; j += static_cast<int>(fuse)) {
+            int je = std::min(j1, j + static_cast<int>(fuse));
+            launch_step(j, je, sp_start_, sp_per_, sp_rem_, false);
+            steps_since_fold_ += static_cast<uint64_t>(je - j);
+            if (sizeof(R) == 4 && steps_since_fold_ >= 4096)
+                fold();
+        }
+    } else {
+        for (int j = sp_j_; j < j1; ++j) {
+            launch_step(j, j + 1, sp_start_, sp_per_, sp_rem_, true);
+            adapt_after_step(j, sp_start_);
+            if (sizeof(R) == 4 && ++steps_since_fold_ >= 4096)
+                fold();
+        }
+    }
+    if (executed)
+        *executed = static_cast<uint32_t>(j1 - sp_j_);
+    sp_j_ = j1;
+    fold();
+    if (sp_j_ == sp_steps_) {
+        span_open_ = false;
+        done_ = sp_end_;
+        span_boundary();
+        return done_;
+    }
+    const uint64_t j = static_cast<uint64_t>(sp_j_);
+    return sp_start_ + (j <= sp_per_ ? j * static_cast<uint64_t>(Ctot_)
+                                     : sp_per_ * static_cast<uint64_t>(Ctot_) + sp_rem_);
 }
 
 template <class R> void EngineT<R>::render() {
@@ -1461,14 +1552,21 @@ template <class R> void EngineT<R>::read_decisions(uint32_t K, double *a, uint8_
         }
 }
 
-template <class R> std::string EngineT<R>::read_partition() {
+template <class R> std::string EngineT<R>::read_partition_visits(const uint64_t *ext, uint64_t n_ext) {
     // PartitionIndex::dump formats (core/partition.cpp:104-121, 138-147, 175-190, 229-245)
     uint64_t n = static_cast<uint64_t>(n_regions_host_);
     std::vector<double> lam(n);
     std::vector<uint64_t> nn(n);
     read_regions(lam.data(), nn.data(), n);
     std::vector<unsigned long long> vis(n);
-    RAMLT_CUDA(cudaMemcpy(vis.data(), visits_.p, n * 8, cudaMemcpyDeviceToHost));
+    if (ext) {
+        if (n_ext != n)
+            throw std::invalid_argument("partition dump: visit array length differs from the region count");
+        for (uint64_t i = 0; i < n; ++i)
+            vis[i] = ext[i];
+    } else {
+        RAMLT_CUDA(cudaMemcpy(vis.data(), visits_.p, n * 8, cudaMemcpyDeviceToHost));
+    }
     std::ostringstream os;
     auto leaf_line = [&](int region, double u0, double v0, double u1, double v1) {
         double l = ctl_ == 0 ? d_.lambda_init : lam[region];

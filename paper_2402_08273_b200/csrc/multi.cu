@@ -172,9 +172,7 @@ public:
             RAMLT_MCUDA(cudaSetDevice(dev_[i]));
             RAMLT_MCUDA(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming));
         }
-        next_refine_ = d.m_refine;
         next_metrics_ = d.metrics_interval;
-        next_film_ = static_cast<uint64_t>(film_sync_) * static_cast<uint64_t>(C);
         RAMLT_MCUDA(cudaSetDevice(dev_[0]));
     }
 
@@ -224,7 +222,9 @@ public:
     }
 
     // ---- the span loop with the exchanges ------------------------------------------------
-    void run(uint64_t mutations) override {
+    // Every shard advances the same canonical lockstep steps (EngineT::run_steps),
+    // then the exchanges run; adaptive strategies exchange after every step.
+    uint64_t run_steps(uint32_t n, uint32_t *executed) override {
         if (!chains_ready_)
             throw std::logic_error("run before init_chains");
         if (!t0_set_) {
@@ -232,40 +232,59 @@ public:
             t0_ = std::chrono::steady_clock::now();
             t0_set_ = true;
         }
-        const uint64_t C = static_cast<uint64_t>(d_.chains);
-        const uint64_t target = done_ + mutations;
-        while (done_ < target) {
-            uint64_t end = target;
-            if (adaptive_)
-                end = std::min(end, (done_ / C + 1) * C);   // one lockstep step per exchange
-            if (quadtree_)
-                end = std::min(end, next_refine_);
+        uint32_t total = 0;
+        while (total < n) {
+            uint32_t k = adaptive_ ? 1u : n - total;
             if (film_sync_)
-                end = std::min(end, next_film_);
-            end = std::min(end, next_metrics_);
-            const uint64_t chunk = end - done_;
+                k = std::min<uint32_t>(k, film_sync_ - static_cast<uint32_t>(steps_ % film_sync_));
+            uint64_t reached = done_;
+            uint32_t ex = 0;
             for (size_t i = 0; i < sh_.size(); ++i) {
                 on(static_cast<int>(i));
-                sh_[i]->run(chunk);
+                reached = sh_[i]->run_steps(k, &ex);   // identical on every shard
             }
-            done_ = end;
-            film_dirty_ = true;
-            if (adaptive_)
-                exchange_adaptation();
-            if (quadtree_ && done_ == next_refine_) {
+            done_ = reached;
+            steps_ += ex;
+            total += ex;
+            if (ex) {
+                film_dirty_ = true;
+                if (adaptive_)
+                    exchange_adaptation();
+            }
+            bool refined = false;
+            if (quadtree_) {
                 on(0);
-                if (sh_[0]->refine_pending())
+                if (sh_[0]->refine_pending()) {
                     exchange_refine();
-                next_refine_ += d_.m_refine;
+                    refined = true;
+                }
             }
-            if (film_sync_ && done_ == next_film_) {
+            if (film_sync_ && ex && steps_ % film_sync_ == 0)
                 sync_film();
-                next_film_ += static_cast<uint64_t>(film_sync_) * C;
-            }
-            if (done_ == next_metrics_ || done_ == d_.mutations) {
+            if (done_ == next_metrics_ || (done_ == d_.mutations && last_row_ != done_)) {
                 push_row();
                 next_metrics_ = done_ + d_.metrics_interval;
             }
+            if (!ex && !refined)
+                break;
+        }
+        if (executed)
+            *executed = total;
+        return done_;
+    }
+
+    // run(m): whole lockstep steps until m more mutations are done (exact when
+    // the target is a span boundary, e.g. the configured total; otherwise the
+    // last step may pass it by less than one lockstep step).
+    void run(uint64_t mutations) override {
+        const uint64_t C = static_cast<uint64_t>(d_.chains);
+        const uint64_t target = done_ + mutations;
+        while (done_ < target) {
+            uint64_t need = std::max<uint64_t>(1, (target - done_) / C);
+            uint32_t ex = 0;
+            run_steps(static_cast<uint32_t>(std::min<uint64_t>(need, 1u << 20)), &ex);
+            if (!ex)
+                throw std::logic_error("multi-device run made no progress");
         }
     }
 
@@ -290,7 +309,7 @@ public:
         } else {
             run(d_.mutations - std::min(d_.mutations, done_));
         }
-        if (rows_.empty() || static_cast<uint64_t>(rows_.back()[1]) != done_)
+        if (last_row_ != done_)
             push_row();
         sync_film();
     }
@@ -380,9 +399,35 @@ public:
             sh_[i]->read_decisions(K, a ? a + o : nullptr, flags ? flags + o : nullptr);
         }
     }
+    void read_chain_lengths(int32_t *k) override {
+        for (size_t i = 0; i < sh_.size(); ++i) {
+            on(static_cast<int>(i));
+            sh_[i]->read_chain_lengths(k + off_[i]);
+        }
+    }
     std::string read_partition() override {
+        // leaf visit counts live split over the shards between refines: dump their SUM
+        std::vector<uint64_t> tot, part;
+        for (size_t i = 0; i < sh_.size(); ++i) {
+            on(static_cast<int>(i));
+            uint64_t *v = nullptr, n = 0;
+            sh_[i]->visits_device(&v, &n);
+            sh_[i]->synchronize();
+            part.assign(n, 0);
+            if (n)
+                RAMLT_MCUDA(cudaMemcpy(part.data(), v, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+            if (i == 0)
+                tot = part;
+            else
+                for (uint64_t q = 0; q < n && q < tot.size(); ++q)
+                    tot[q] += part[q];
+        }
         on(0);
-        return sh_[0]->read_partition();
+        return sh_[0]->read_partition_visits(tot.data(), tot.size());
+    }
+    std::string read_partition_visits(const uint64_t *visits, uint64_t n) override {
+        on(0);
+        return sh_[0]->read_partition_visits(visits, n);
     }
     void set_reference(const float *rgb, int width, int height) override {
         on(0);
@@ -473,7 +518,9 @@ private:
                                                 arrays[i][q], dev_[i], n * sizeof(unsigned long long), st(0)));
         }
     }
-    // broadcast the root's arrays to every shard, after the root's reduction
+    // broadcast the root's arrays to every shard, after the root's reduction; the
+    // root stream then waits for every copy, so the root's next writes (apply,
+    // refine, splats) cannot race with a peer still reading its buffers
     void broadcast(const std::vector<std::vector<unsigned long long *>> &arrays, size_t bytes_each) {
         const int ns = static_cast<int>(sh_.size());
         on(0);
@@ -484,6 +531,17 @@ private:
             for (size_t q = 0; q < arrays[0].size(); ++q)
                 RAMLT_MCUDA(cudaMemcpyPeerAsync(arrays[i][q], dev_[i], arrays[0][q], dev_[0], bytes_each, st(i)));
         }
+        join_root();
+    }
+    void join_root() {
+        const int ns = static_cast<int>(sh_.size());
+        for (int i = 1; i < ns; ++i) {
+            on(i);
+            RAMLT_MCUDA(cudaEventRecord(ev_[i], st(i)));
+        }
+        on(0);
+        for (int i = 1; i < ns; ++i)
+            RAMLT_MCUDA(cudaStreamWaitEvent(st(0), ev_[i], 0));
     }
     unsigned grid(size_t n) const { return static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 148 * 8)); }
 
@@ -572,6 +630,7 @@ private:
             RAMLT_MCUDA(cudaStreamWaitEvent(st(i), ev_[0], 0));
             RAMLT_MCUDA(cudaMemcpyPeerAsync(film[i], dev_[i], film[0], dev_[0], n * sizeof(double), st(i)));
         }
+        join_root();
         film_dirty_ = false;
     }
 
@@ -593,6 +652,7 @@ private:
             rr = rrmse(done_);
         double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
         rows_.push_back({t, static_cast<double>(done_), rr, den > 0 ? num / den : 0.0});
+        last_row_ = done_;
     }
 
     ramlt_render_desc d_;
@@ -603,7 +663,8 @@ private:
     std::vector<cudaEvent_t> ev_;
     bool adaptive_ = false, quadtree_ = false, has_ref_ = false;
     bool b_set_ = false, chains_ready_ = false, film_dirty_ = false, t0_set_ = false;
-    uint64_t done_ = 0, next_refine_ = 0, next_metrics_ = 0, next_film_ = 0, launches_ = 0;
+    uint64_t done_ = 0, next_metrics_ = 0, steps_ = 0, launches_ = 0;
+    uint64_t last_row_ = std::numeric_limits<uint64_t>::max();
     std::chrono::steady_clock::time_point t0_;
     std::vector<std::array<double, 4>> rows_;
     DevBuf<unsigned long long> xstage_;

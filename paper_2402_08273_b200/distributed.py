@@ -7,7 +7,10 @@
                     last mutation index) SUM/SUM/MAX all-reduce per lockstep
                     step, then the same deterministic update on every rank
                     (G-invariant: integer sums do not depend on the partition);
-  * framebuffer  -- fp64 film SUM all-reduce at sync points.
+  * quadtree     -- per-region visit counts SUM-reduced at every m_refine
+                    barrier, then the same deterministic refine on every rank;
+  * framebuffer  -- delta SUM all-reduce of the fp64 film every 2^12 lockstep
+                    steps (configs[4]), at metrics rows and at the end.
 
 Chain c keeps its global id everywhere (RNG stream, decision order), so a
 Fixed-strategy run is identical at any GPU count.  The same code runs on CPU
@@ -124,15 +127,6 @@ def sharded_sync(engine):
     sync_refine(engine)
 
 
-def reduce_film(engine):
-    """SUM all-reduce of the fp64 film in place on every rank (NCCL)."""
-    import torch.distributed as dist
-    ptr, n = engine.film_device()
-    t = device_tensor(ptr, n, "<f8")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return t
-
-
 def reduce_film_host(film: np.ndarray, device=None) -> np.ndarray:
     """SUM all-reduce of a host film (gloo / CPU path)."""
     import torch
@@ -142,46 +136,176 @@ def reduce_film_host(film: np.ndarray, device=None) -> np.ndarray:
     return t.cpu().numpy()
 
 
-class ShardedRender:
-    """run_render over torch.distributed ranks: one engine per rank/GPU."""
+def sync_film(engine, synced):
+    """Delta SUM all-reduce of the fp64 film (core/film.cpp:22-27 merge, done
+    periodically): every rank's film becomes the global film, each rank's
+    contribution counted once.  ``synced`` is the global film of the previous
+    sync (zeros at first; updated in place)."""
+    import torch.distributed as dist
+    ptr, n = engine.film_device()
+    t = device_tensor(ptr, n, "<f8")
+    delta = t - synced
+    dist.all_reduce(delta, op=dist.ReduceOp.SUM)
+    synced.add_(delta)
+    t.copy_(synced)
+    return t
 
-    def __init__(self, scene, cfg, exchange_every: int = 1):
+
+class ShardedRender:
+    """run_render over torch.distributed ranks: one engine per rank/GPU.
+
+    Chains shard by global id (ShardPlan).  Runs are chunked so that every
+    exchange happens at the same global mutation count on every rank:
+      * adaptive strategies: the pooled adaptation exchange every
+        ``exchange_every`` lockstep steps (1 = G-invariant, identical to one GPU);
+      * RA-quadtree: runs end exactly at every m_refine barrier, where the
+        visits are SUM-reduced and every rank refines identically
+        (core/partition.cpp:68-100, core/driver.cpp:300-304);
+      * the film every ``film_sync_steps`` lockstep steps (configs[4]: 2^12,
+        0 = only at metrics rows and the end) and at metrics rows, so the
+        image, the luminance and the rRMSE are global on every rank;
+      * b once (substream partials gathered in order).
+    """
+
+    def __init__(self, scene, cfg, exchange_every: int = 1, film_sync_steps: int = 4096):
+        import time
         import torch
         import torch.distributed as dist
         from .render import Engine
-        self.world = dist.get_world_size()
-        self.rank = dist.get_rank()
+        init = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size() if init else 1
+        self.rank = dist.get_rank() if init else 0
         self.plan = ShardPlan(cfg.chains, self.world, self.rank)
         local = torch.cuda.current_device()
         self.cfg = cfg
         self.engine = Engine(scene, shard_config(cfg, self.plan, local))
         self.engine.set_stream(torch.cuda.current_stream().cuda_stream)
         self.adaptive = cfg.strategy != "fixed"
-        self.exchange_every = exchange_every
+        self.quadtree = cfg.strategy == "ra-quadtree"
+        self.exchange_every = max(1, int(exchange_every))
+        self.film_sync_steps = int(film_sync_steps)
+        self.done = 0           # global mutations
+        self.steps = 0          # lockstep steps (film merge cadence)
+        self.next_metrics = cfg.metrics_interval
+        self._last_row = -1
+        self.rows = []          # MetricsRow (time, mutations, rrmse, interval acceptance), global
+        self._synced = None
+        self._film_dirty = False
+        self._has_ref = False
+        self._acc_last = (0.0, 0.0)
+        self._t0 = None
+        self._time = time.perf_counter
         if self.adaptive and self.world > 1:
-            self.engine.set_exchange_interval(exchange_every)
+            self.engine.set_exchange_interval(self.exchange_every)
+
+    def set_reference(self, image):
+        self.engine.set_reference(image)
+        self._has_ref = True
 
     def estimate_b(self):
+        if self.world == 1:
+            return self.engine.estimate_b()
         return all_gather_b(self.engine, self.cfg, self.plan)
 
+    def init_chains(self):
+        self.engine.init_chains()
+
     def run(self, mutations: int):
+        """Advance the render by ``mutations`` global mutations.  One rank:
+        the engine's own span loop (exact).  Several ranks: whole lockstep steps
+        of the canonical span loop (Engine.run_steps: the spans a single GPU
+        uses, so every chain's decisions equal the single-GPU run), with the
+        exchanges between steps; a target that is not a span boundary may be
+        passed by less than one lockstep step."""
+        if self._t0 is None:
+            self._t0 = self._time()
         C = self.cfg.chains
-        if not self.adaptive or self.world == 1:
-            self.engine.run(mutations)
+        target = self.done + mutations
+        if self.world == 1:
+            while self.done < target:
+                end = min(target, self.next_metrics)
+                self.engine.run(end - self.done)
+                self.done = end
+                self._film_dirty = True
+                if self.done == self.next_metrics or self.done == self.cfg.mutations:
+                    self._push_row()
+                    self.next_metrics = self.done + self.cfg.metrics_interval
             return
-        step = C * self.exchange_every
-        done = 0
-        while done < mutations:
-            m = min(step, mutations - done)
-            self.engine.run(m)
-            sharded_sync(self.engine)
-            done += m
+        while self.done < target:
+            n = self.exchange_every if self.adaptive else max(1, (target - self.done) // C)
+            if self.film_sync_steps:
+                n = min(n, self.film_sync_steps - self.steps % self.film_sync_steps)
+            done, ex = self.engine.run_steps(n)
+            self.done = done
+            self.steps += ex
+            if ex:
+                self._film_dirty = True
+                if self.adaptive:
+                    exchange_adaptation(self.engine)
+            refined = self.quadtree and sync_refine(self.engine)
+            if self.film_sync_steps and ex and self.steps % self.film_sync_steps == 0:
+                self.sync_film()
+            if self.done == self.next_metrics or (self.done == self.cfg.mutations and self._last_row != self.done):
+                self._push_row()
+                self.next_metrics = self.done + self.cfg.metrics_interval
+            if not ex and not refined:
+                raise RuntimeError("sharded run made no progress")
+
+    def sync_film(self):
+        import torch
+        if self.world == 1:
+            self._film_dirty = False
+            return
+        if self._synced is None:
+            _, n = self.engine.film_device()
+            self._synced = torch.zeros(n, dtype=torch.float64, device="cuda")
+        sync_film(self.engine, self._synced)
+        self._film_dirty = False
+
+    def global_acceptance(self):
+        """(accepted sum, perturbation proposals) over all ranks so far."""
+        import torch
+        import torch.distributed as dist
+        s = self.engine.stats()
+        t = torch.tensor([s.mean_acceptance * s.perturbation_proposals, float(s.perturbation_proposals)],
+                         dtype=torch.float64, device="cuda")
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t[0]), float(t[1])
+
+    def _push_row(self):
+        if self._film_dirty:
+            self.sync_film()
+        a, n = self.global_acceptance()
+        a0, n0 = self._acc_last
+        self._acc_last = (a, n)
+        rr = self.engine.rrmse(self.done) if self._has_ref else float("nan")
+        self.rows.append((self._time() - self._t0, self.done, rr, (a - a0) / (n - n0) if n > n0 else 0.0))
+        self._last_row = self.done
+
+    def partition_dump(self) -> str:
+        """PartitionIndex::dump with the leaf visit counts summed over ranks."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return self.engine.partition_dump()
+        ptr, n = self.engine.visits_device()
+        v = device_tensor(ptr, n, "<u8").view(dtype=torch.int64).clone()
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        return self.engine.partition_dump(visits=v.cpu().numpy().astype(np.uint64))
+
+    def image(self):
+        if self._film_dirty:
+            self.sync_film()
+        return self.engine.image()
 
     def render(self):
         self.estimate_b()
         self.engine.init_chains()
-        self.run(self.cfg.mutations)
-        return reduce_film(self.engine)
+        self.run(self.cfg.mutations - self.done)
+        self.sync_film()
+        ptr, n = self.engine.film_device()
+        return device_tensor(ptr, n, "<f8")
 
 
 class ShardedMix:

@@ -166,9 +166,11 @@ def parse_scene(text: str, origin: str = "<string>") -> Scene:
 
 
 class Engine:
-    """One engine handle (one GPU, one chain shard)."""
+    """One engine handle: one GPU and one chain shard, or -- with ``devices`` --
+    every chain over several GPUs of this process (ramlt_gpu_create_multi:
+    peer-memory exchanges, film merged every ``film_sync_steps`` lockstep steps)."""
 
-    def __init__(self, scene, cfg: RenderConfig):
+    def __init__(self, scene, cfg: RenderConfig, devices=None, film_sync_steps: int = 4096):
         self.lib = _capi.load()
         self.cfg = cfg
         if isinstance(scene, str):
@@ -176,7 +178,12 @@ class Engine:
         self.scene = scene
         self._desc = cfg.to_c()
         h = C.c_void_p()
-        rc = self.lib.ramlt_gpu_create(C.byref(scene.desc), C.byref(self._desc), C.byref(h))
+        if devices is not None:
+            devs = (C.c_int32 * max(len(devices), 1))(*devices)
+            rc = self.lib.ramlt_gpu_create_multi(C.byref(scene.desc), C.byref(self._desc), len(devices), devs,
+                                                 film_sync_steps, C.byref(h))
+        else:
+            rc = self.lib.ramlt_gpu_create(C.byref(scene.desc), C.byref(self._desc), C.byref(h))
         if rc:
             _raise(rc, self.lib.ramlt_gpu_last_create_error().decode())
         self.h = h
@@ -220,6 +227,13 @@ class Engine:
 
     def run(self, mutations: int):
         self._check(self.lib.ramlt_gpu_run(self.h, mutations))
+
+    def run_steps(self, n: int):
+        """Up to n lockstep steps of the canonical span loop (stops at a span
+        end); returns (global mutations reached, steps executed)."""
+        done, ex = C.c_uint64(), C.c_uint32()
+        self._check(self.lib.ramlt_gpu_run_steps(self.h, n, C.byref(done), C.byref(ex)))
+        return done.value, ex.value
 
     def render(self):
         self._check(self.lib.ramlt_gpu_render(self.h))
@@ -289,9 +303,22 @@ class Engine:
             self.h, K, a.ctypes.data_as(C.POINTER(C.c_double)), f.ctypes.data_as(C.POINTER(C.c_uint8))))
         return a, f
 
-    def partition_dump(self) -> str:
+    def chain_lengths(self) -> np.ndarray:
+        """Current path length k (vertices incl. the camera) of every chain."""
+        k = np.zeros(self.cfg.chains, np.int32)
+        self._check(self.lib.ramlt_gpu_read_chain_lengths(self.h, k.ctypes.data_as(C.POINTER(C.c_int32))))
+        return k
+
+    def partition_dump(self, visits: Optional[np.ndarray] = None) -> str:
+        """PartitionIndex::dump; ``visits`` overrides the per-region visit
+        counts (sharded runs pass the SUM over ranks)."""
         buf = C.create_string_buffer(1 << 24)
-        self._check(self.lib.ramlt_gpu_read_partition(self.h, buf, 1 << 24))
+        if visits is None:
+            self._check(self.lib.ramlt_gpu_read_partition(self.h, buf, 1 << 24))
+        else:
+            v = np.ascontiguousarray(visits, np.uint64)
+            self._check(self.lib.ramlt_gpu_read_partition_visits(
+                self.h, v.ctypes.data_as(C.POINTER(C.c_uint64)), v.size, buf, 1 << 24))
         return buf.value.decode()
 
     # --- multi-GPU plumbing ------------------------------------------------
@@ -340,6 +367,13 @@ class Engine:
         self._ref = img
         self._check(self.lib.ramlt_gpu_set_reference(self.h, img.ctypes.data_as(C.POINTER(C.c_float)), w, h))
 
+    def rrmse(self, at: int) -> float:
+        """MetricsRow.rrmse (core/driver.cpp:265-272) of the current film at
+        ``at`` mutations; NaN without a reference image."""
+        out = C.c_double()
+        self._check(self.lib.ramlt_gpu_rrmse(self.h, at, C.byref(out)))
+        return out.value
+
     def trace_benchmark(self, n_rays: int):
         """Diagnostic: (kernel ms, hits) of n_rays incoherent closest-hit rays
         through the BVH traversal alone (ramlt_gpu_trace_benchmark)."""
@@ -362,10 +396,12 @@ class Engine:
 
 
 def run_render(scene, cfg: RenderConfig, b: Optional[float] = None,
-               reference: Optional[np.ndarray] = None) -> RenderResult:
+               reference: Optional[np.ndarray] = None, devices=None,
+               film_sync_steps: int = 4096) -> RenderResult:
     """run_render (core/driver.hpp:80): estimate_b, chain init, span loop, reduce.
-    ``reference`` is RenderConfig::reference (an (H, W, 3) float32 image)."""
-    eng = Engine(scene, cfg)
+    ``reference`` is RenderConfig::reference (an (H, W, 3) float32 image);
+    ``devices`` (e.g. [0, 1, ..., 7]) runs the chains over several GPUs."""
+    eng = Engine(scene, cfg, devices=devices, film_sync_steps=film_sync_steps)
     try:
         if b is not None:
             eng.set_b(b)
