@@ -27,6 +27,11 @@ struct Options {
     int rng = RAMLT_RNG_PHILOX;     // RAMLT_RNG_PCG32 reproduces the reference's streams
     int device = -1;
     unsigned log_steps = 0;
+    // Several GPUs of this process (e.g. {0,...,7}): one handle over all of them
+    // (ramlt_gpu_create_multi), chains sharded by global id -- the drop-in for the
+    // reference's thread-per-chain loop (core/driver.cpp:282-297) on 1..8 B200s.
+    std::vector<int> devices;
+    unsigned film_sync_steps = 4096;   // configs[4]: film merged every 2^12 lockstep steps
 };
 
 inline void rethrow(int rc, const char *msg) {
@@ -135,10 +140,24 @@ inline RenderResult run_render(const std::string &scene_text, const RenderConfig
                                const Options &opt = {}) {
     ramlt_render_desc d = to_desc(cfg, opt);
     ramlt_gpu *h = nullptr;
-    rethrow(ramlt_gpu_create_from_text(scene_text.c_str(), "<scene>", &d, &h),
-            ramlt_gpu_last_create_error());
+    if (opt.devices.size() > 1) {
+        std::vector<int32_t> devs(opt.devices.begin(), opt.devices.end());
+        rethrow(ramlt_gpu_create_multi_from_text(scene_text.c_str(), "<scene>", &d, static_cast<int32_t>(devs.size()),
+                                                 devs.data(), opt.film_sync_steps, &h),
+                ramlt_gpu_last_create_error());
+    } else {
+        if (opt.devices.size() == 1)
+            d.device = opt.devices[0];
+        rethrow(ramlt_gpu_create_from_text(scene_text.c_str(), "<scene>", &d, &h), ramlt_gpu_last_create_error());
+    }
     RenderResult r;
     try {
+        // RenderConfig::reference (core/driver.hpp:38): metrics rows carry the rRMSE
+        // of the running image against it (core/driver.cpp:265-272)
+        if (cfg.reference)
+            rethrow(ramlt_gpu_set_reference(h, cfg.reference->data.data(), cfg.reference->width,
+                                            cfg.reference->height),
+                    ramlt_gpu_last_error(h));
         rethrow(ramlt_gpu_render(h), ramlt_gpu_last_error(h));
         fill_result(h, cfg.width, cfg.height, r);
         if (cfg.dump_partition) {

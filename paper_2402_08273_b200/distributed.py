@@ -90,15 +90,44 @@ def device_tensor(ptr: int, n: int, typestr: str):
     return torch.as_tensor(_CudaArray(ptr, n, typestr), device="cuda")
 
 
+def _u64(engine_ptr_n):
+    import torch
+    ptr, n = engine_ptr_n
+    return device_tensor(ptr, n, "<u8").view(dtype=torch.int64) if n else None
+
+
+def adapt_tensors(engine):
+    """Zero-copy int64 views of the engine's pooled exchange buffers (count,
+    fixed-point sum, last index); engines may provide ``adapt_tensors`` themselves
+    (the CPU host-logic tests pass CPU tensors)."""
+    if hasattr(engine, "adapt_tensors"):
+        return engine.adapt_tensors()
+    cnt, fx, last, n = engine.adapt_exchange()
+    if not n:
+        return None
+    return _u64((cnt, n)), _u64((fx, n)), _u64((last, n))
+
+
+def visits_tensor(engine):
+    if hasattr(engine, "visits_tensor"):
+        return engine.visits_tensor()
+    return _u64(engine.visits_device())
+
+
+def film_tensor(engine):
+    if hasattr(engine, "film_tensor"):
+        return engine.film_tensor()
+    ptr, n = engine.film_device()
+    return device_tensor(ptr, n, "<f8")
+
+
 def exchange_adaptation(engine):
     """Pooled adaptation exchange after a lockstep step: SUM counts and
     fixed-point sums, MAX last index, then apply identically on every rank."""
     import torch.distributed as dist
-    cnt, fx, last, n = engine.adapt_exchange()
-    if n:
-        tc = device_tensor(cnt, n, "<u8").view(dtype=__import__("torch").int64)
-        tf = device_tensor(fx, n, "<u8").view(dtype=__import__("torch").int64)
-        tl = device_tensor(last, n, "<u8").view(dtype=__import__("torch").int64)
+    t = adapt_tensors(engine)
+    if t is not None:
+        tc, tf, tl = t
         dist.all_reduce(tc, op=dist.ReduceOp.SUM)
         dist.all_reduce(tf, op=dist.ReduceOp.SUM)
         dist.all_reduce(tl, op=dist.ReduceOp.MAX)
@@ -109,13 +138,11 @@ def sync_refine(engine):
     """Deferred quadtree refine of a sharded run: SUM the
     per-region visit counts, refine identically on every rank, and keep the
     carried-over counts on rank 0 only."""
-    import torch
     import torch.distributed as dist
     if not engine.refine_pending():
         return False
-    ptr, n = engine.visits_device()
-    if n:
-        v = device_tensor(ptr, n, "<u8").view(dtype=torch.int64)
+    v = visits_tensor(engine)
+    if v is not None:
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
     engine.refine(keep_counts=dist.get_rank() == 0)
     return True
@@ -142,8 +169,7 @@ def sync_film(engine, synced):
     contribution counted once.  ``synced`` is the global film of the previous
     sync (zeros at first; updated in place)."""
     import torch.distributed as dist
-    ptr, n = engine.film_device()
-    t = device_tensor(ptr, n, "<f8")
+    t = film_tensor(engine)
     delta = t - synced
     dist.all_reduce(delta, op=dist.ReduceOp.SUM)
     synced.add_(delta)
@@ -167,7 +193,7 @@ class ShardedRender:
       * b once (substream partials gathered in order).
     """
 
-    def __init__(self, scene, cfg, exchange_every: int = 1, film_sync_steps: int = 4096):
+    def __init__(self, scene, cfg, exchange_every: int = 1, film_sync_steps: int = 4096, engine=None):
         import time
         import torch
         import torch.distributed as dist
@@ -176,10 +202,14 @@ class ShardedRender:
         self.world = dist.get_world_size() if init else 1
         self.rank = dist.get_rank() if init else 0
         self.plan = ShardPlan(cfg.chains, self.world, self.rank)
-        local = torch.cuda.current_device()
         self.cfg = cfg
-        self.engine = Engine(scene, shard_config(cfg, self.plan, local))
-        self.engine.set_stream(torch.cuda.current_stream().cuda_stream)
+        if engine is not None:      # host-logic tests: an engine stand-in on CPU tensors
+            self.engine, self.device = engine, "cpu"
+        else:
+            local = torch.cuda.current_device()
+            self.engine = Engine(scene, shard_config(cfg, self.plan, local))
+            self.engine.set_stream(torch.cuda.current_stream().cuda_stream)
+            self.device = "cuda"
         self.adaptive = cfg.strategy != "fixed"
         self.quadtree = cfg.strategy == "ra-quadtree"
         self.exchange_every = max(1, int(exchange_every))
@@ -257,8 +287,7 @@ class ShardedRender:
             self._film_dirty = False
             return
         if self._synced is None:
-            _, n = self.engine.film_device()
-            self._synced = torch.zeros(n, dtype=torch.float64, device="cuda")
+            self._synced = torch.zeros_like(film_tensor(self.engine))
         sync_film(self.engine, self._synced)
         self._film_dirty = False
 
@@ -268,7 +297,7 @@ class ShardedRender:
         import torch.distributed as dist
         s = self.engine.stats()
         t = torch.tensor([s.mean_acceptance * s.perturbation_proposals, float(s.perturbation_proposals)],
-                         dtype=torch.float64, device="cuda")
+                         dtype=torch.float64, device=self.device)
         if self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t[0]), float(t[1])
@@ -289,8 +318,7 @@ class ShardedRender:
         import torch.distributed as dist
         if self.world == 1:
             return self.engine.partition_dump()
-        ptr, n = self.engine.visits_device()
-        v = device_tensor(ptr, n, "<u8").view(dtype=torch.int64).clone()
+        v = visits_tensor(self.engine).clone()
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
         return self.engine.partition_dump(visits=v.cpu().numpy().astype(np.uint64))
 
@@ -304,8 +332,7 @@ class ShardedRender:
         self.engine.init_chains()
         self.run(self.cfg.mutations - self.done)
         self.sync_film()
-        ptr, n = self.engine.film_device()
-        return device_tensor(ptr, n, "<f8")
+        return film_tensor(self.engine)
 
 
 class ShardedMix:
