@@ -302,13 +302,25 @@ template <> __device__ __forceinline__ float mix_unit<float>(uint32_t hi, uint32
 // independent Philox chains (instruction-level parallelism instead of five
 // serial out-of-line refills) and the words are picked from registers.  Same
 // words, same order, same arithmetic as mix_step.
-template <class R, int KT>
-__device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixRegs<R, 8> &cs, Rng<RNG_PHILOX> &rng,
-                                               bool &accepted) {
+// The draw half of a configs[1] step (Philox, D = 8): every word the step can
+// consume is known from the draw counter alone -- [c0, c0+16) for the
+// proposal, [c0+16, c0+18) for the accept draw -- so the five Philox blocks,
+// the eight normal quantiles and the accept uniform can be computed before
+// sigma (the pending lambda update) is known.  k_mix_coop computes them while
+// its grid barrier completes.  ok = false: odd counter alignment (generic path).
+template <class R> struct Px8Pre {
+    R z[8];
+    R ua;
+    bool ok;
+};
+
+template <class R>
+__device__ __forceinline__ void px8_pre(const Rng<RNG_PHILOX> &rng, Px8Pre<R> &pre) {
     const unsigned long long c0 = rng.draw;
     const unsigned off = static_cast<unsigned>(c0 & 3ull);
-    if (off & 1u)
-        return mix_step<R, RNG_PHILOX, 8, KT>(P, sigma, cs, rng, accepted);
+    pre.ok = !(off & 1u);
+    if (!pre.ok)
+        return;
     const unsigned long long b = c0 >> 2;
     const uint32_t k0 = static_cast<uint32_t>(rng.key), k1 = static_cast<uint32_t>(rng.key >> 32);
     const uint32_t s0 = static_cast<uint32_t>(rng.stream), s1 = static_cast<uint32_t>(rng.stream >> 32);
@@ -326,11 +338,22 @@ __device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixReg
 #pragma unroll
     for (int i = 0; i < 18; ++i)
         u[i] = off ? w[i + 2] : w[i];
+#pragma unroll
+    for (int d = 0; d < 8; ++d)
+        pre.z[d] = nquantile<R>(mix_unit<R>(u[2 * d], u[2 * d + 1]));
+    pre.ua = mix_unit<R>(u[16], u[17]);
+}
+
+// The rest of the step once sigma is known: propose, evaluate, accept.
+template <class R, int KT>
+__device__ __forceinline__ double px8_finish(const MixP<R> &P, R sigma, MixRegs<R, 8> &cs, Rng<RNG_PHILOX> &rng,
+                                             const Px8Pre<R> &pre, bool &accepted) {
+    const unsigned long long c0 = rng.draw;
     R y[8];
     bool in = true;
 #pragma unroll
     for (int d = 0; d < 8; ++d) {
-        y[d] = cs.x[d] + sigma * nquantile<R>(mix_unit<R>(u[2 * d], u[2 * d + 1]));
+        y[d] = cs.x[d] + sigma * pre.z[d];
         in = in && (y[d] >= R(0) && y[d] <= R(1));
     }
     double a = 0.0;
@@ -341,7 +364,7 @@ __device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixReg
         a = rr > R(0) ? (rr < R(1) ? static_cast<double>(rr) : 1.0) : 0.0;
     }
     accepted = false;
-    if (a > 0.0 && mix_unit<R>(u[16], u[17]) < static_cast<R>(a)) {
+    if (a > 0.0 && pre.ua < static_cast<R>(a)) {
         accepted = true;
 #pragma unroll
         for (int d = 0; d < 8; ++d)
@@ -353,6 +376,18 @@ __device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixReg
     cs.asum += a;
     cs.nacc += accepted ? 1u : 0u;
     return a;
+}
+
+// configs[1] path (Philox, D = 8): the step's words are computed up front as
+// independent Philox blocks (ILP) instead of serial out-of-line refills.
+template <class R, int KT>
+__device__ __forceinline__ double mix_step_px8(const MixP<R> &P, R sigma, MixRegs<R, 8> &cs, Rng<RNG_PHILOX> &rng,
+                                               bool &accepted) {
+    Px8Pre<R> pre;
+    px8_pre<R>(rng, pre);
+    if (!pre.ok)
+        return mix_step<R, RNG_PHILOX, 8, KT>(P, sigma, cs, rng, accepted);
+    return px8_finish<R, KT>(P, sigma, cs, rng, pre, accepted);
 }
 
 // Dispatch: the batched-draw form where it applies.
@@ -558,7 +593,7 @@ template <class R> __global__ void k_mix_apply_literal(MixP<R> P, unsigned long 
 // mode 2: literal: per-chain (region, a) to HBM, barrier, canonical-order
 //         sequential apply by one thread, barrier.
 template <class R, int RK, int DT, int KT>
-__global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long j0, unsigned long long j1, int mode) {
+__global__ void __launch_bounds__(512) k_mix_coop(MixP<R> P, unsigned long long j0, unsigned long long j1, int mode) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long wsum[8];
@@ -574,13 +609,26 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
     unsigned long long n = P.n[0], pn = P.pend_n[0], pf = P.pend_fx[0];
     unsigned long long tfx = 0, tvis = 0;
     R sigma = P.sig[0];
+    // mode 0 with Philox and D = 8: the next step's draws are computed between
+    // the barrier arrival and the wait (split-phase barrier), hiding the wait
+    constexpr bool kPre = RK == RNG_PHILOX && DT == 8;
+    Px8Pre<R> pre;
+    bool have_pre = false;
     for (unsigned long long j = j0; j < j1; ++j) {
         int r = -1;
         double a = 0.0;
         if (active) {
             r = mix_region(P, cs);
             bool acc;
-            a = mix_step_any<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
+            if constexpr (kPre) {
+                if (mode == 0 && have_pre && pre.ok)
+                    a = px8_finish<R, KT>(P, sigma, *reinterpret_cast<MixRegs<R, 8> *>(&cs), rng, pre, acc);
+                else
+                    a = mix_step_any<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
+            } else {
+                a = mix_step_any<R, RK, DT, KT>(P, mode == 0 ? sigma : __ldcg(&P.sig[r]), cs, rng, acc);
+            }
+            have_pre = false;
             mix_log(P, c, j, a, acc);
             mix_record(P, c, j, cs);
         }
@@ -595,11 +643,20 @@ __global__ void __launch_bounds__(256) k_mix_coop(MixP<R> P, unsigned long long 
             if ((threadIdx.x & 31) == 0)
                 wsum[threadIdx.x >> 5] = ws;
             __syncthreads();
-            if (threadIdx.x == 0) {
+            unsigned long long v = 0;
+            if (threadIdx.x == 0) {   // arrive
                 unsigned long long b = 1ull << 48;
                 for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
                     b += wsum[w];
-                unsigned long long v = atomicAdd(&P.gbuf[j % 3], b) + b;
+                v = atomicAdd(&P.gbuf[j % 3], b) + b;
+            }
+            if constexpr (kPre) {   // overlap: the next step's words do not depend on sigma
+                if (active && j + 1 < j1) {
+                    px8_pre<R>(*reinterpret_cast<Rng<RNG_PHILOX> *>(&rng), pre);
+                    have_pre = true;
+                }
+            }
+            if (threadIdx.x == 0) {   // wait
                 const unsigned long long want = static_cast<unsigned long long>(gridDim.x);
                 while ((v >> 48) < want) {
                     if (RAMLT_MIX_SPIN_NS > 0)
@@ -828,7 +885,7 @@ private:
     cudaStream_t stream_ = nullptr;
     bool own_stream_ = true;
     int coop_blocks_ = -1;   // resident capacity of k_mix_coop in blocks (-1 unknown)
-    int coop_threads_ = 256; // RAMLT_MIX_COOP_THREADS: 128 / 256
+    int coop_threads_ = 0;   // 0: SM-balanced blocks; RAMLT_MIX_COOP_THREADS: a fixed block size (multiple of 32)
     uint64_t steps_ = 0, launches_ = 0;
     MBuf<R> x_, lp_, sig_;
     MBuf<unsigned long long> rng0_, rng1_;
@@ -864,7 +921,7 @@ MixEngineT<R>::MixEngineT(const MixHostTarget &t, const ramlt_mix_desc &d) : d_(
         RAMLT_MCUDA(cudaSetDevice(d.device));
     RAMLT_MCUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     if (const char *v = std::getenv("RAMLT_MIX_COOP_THREADS"))
-        coop_threads_ = std::atoi(v) == 128 ? 128 : 256;
+        coop_threads_ = std::max(0, std::min(512, std::atoi(v) / 32 * 32));
     C_ = d.chains;
     D_ = t.D;
     K_ = t.K;
@@ -1054,7 +1111,20 @@ void MixEngineT<R>::launch_run(uint64_t steps) {
     const int blocks = (C_ + threads - 1) / threads;
     // cooperative kernel: 256-thread blocks halve the barrier arrivals; the
     // busiest SM holds the same number of chains as with 128-thread blocks
-    const int cthreads = coop_threads_;
+    // cooperative kernel: every SM gets the same number of chains (k blocks per
+    // SM of ceil(C / (k SMs)) threads rounded up to a warp, <= 256): fixed
+    // 256-thread blocks made 256 blocks for 65,536 chains on 148 SMs, so the
+    // barrier waited every step for the SMs holding two blocks.
+    int cthreads = coop_threads_;
+    if (cthreads <= 0) {
+        int dev = 0, nsm = 148;
+        RAMLT_MCUDA(cudaGetDevice(&dev));
+        RAMLT_MCUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int per_block = 256;
+        const int k = std::max(1, (C_ + nsm * per_block - 1) / (nsm * per_block));
+        const int nb = nsm * k;
+        cthreads = std::min(per_block, std::max(32, ((C_ + nb - 1) / nb + 31) / 32 * 32));
+    }
     const int cblocks = (C_ + cthreads - 1) / cthreads;
     auto ev_begin = [&]() -> std::pair<cudaEvent_t, cudaEvent_t> {
         std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
