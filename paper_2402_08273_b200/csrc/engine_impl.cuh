@@ -243,6 +243,17 @@ private:
     double step_ms_ = 0.0;
     uint64_t step_launches_ = 0;
     void drain_events();
+    // launch configuration cache: the dynamic-smem attribute is set and the
+    // occupancy queried once per (kernel, smem) instead of on every launch
+    // (per-step launches of small-chain runs are host-bound)
+    struct LaunchCfg {
+        const void *kern;
+        size_t smem;
+        int per_sm;
+    };
+    std::vector<LaunchCfg> lcfg_;
+    int sms_ = 0;
+    int prepare(const void *kern, size_t smem, int carveout = -1);
 };
 
 // ---------------------------------------------------------------------------------------
@@ -533,6 +544,24 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         trace_alpha_.alloc(tcap);
     }
     RAMLT_CUDA(cudaStreamSynchronize(stream_));
+}
+
+template <class R> int EngineT<R>::prepare(const void *kern, size_t smem, int carveout) {
+    for (const LaunchCfg &c : lcfg_)
+        if (c.kern == kern && c.smem == smem)
+            return c.per_sm;
+    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (carveout >= 0)   // RAMLT_CO_CARVEOUT: shared-memory share of the L1/smem pool (percent)
+        RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
+    int per_sm = 0;
+    RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    if (!sms_) {
+        int dev = 0;
+        RAMLT_CUDA(cudaGetDevice(&dev));
+        RAMLT_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
+    }
+    lcfg_.push_back({kern, smem, per_sm});
+    return per_sm;
 }
 
 template <class R> void EngineT<R>::drain_events() {
@@ -911,7 +940,7 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
         RAMLT_PICK(rd::RNG_PCG)
     }
 #undef RAMLT_PICK
-    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_)));
+    prepare(reinterpret_cast<const void *>(kern), smem_);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d_.profile_kernels) {
         if (ev_.size() >= 4096)
@@ -942,14 +971,8 @@ void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
     P.co_stack_off = static_cast<unsigned>(smem);
     if (use_bvh_)
         smem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
-    RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (co_carveout_ >= 0)   // RAMLT_CO_CARVEOUT: shared-memory share of the L1/smem pool (percent)
-        RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, co_carveout_));
-    int per_sm = 0;
-    RAMLT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
-    int dev = 0, sms = 148;
-    RAMLT_CUDA(cudaGetDevice(&dev));
-    RAMLT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int per_sm = prepare(reinterpret_cast<const void *>(kern), smem, co_carveout_);
+    const int sms = sms_;
     unsigned want = static_cast<unsigned>((C_ + 127) / 128);
     unsigned blocks = P.steal ? std::min<unsigned>(want, static_cast<unsigned>(std::max(per_sm, 1) * sms)) : want;
     P.pv_scratch = nullptr;
