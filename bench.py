@@ -119,7 +119,7 @@ def reference_rays_per_mutation(wl: dict, scene_text: str, threads: int):
     reference was not built."""
     from oracle.abi import OracleConfig, OracleLib, RefLib, REF_LOG_SO
     big = wl["scene"] == "clusters"
-    per = 16 if big else 256
+    per = 32 if big else 256
     cfg = OracleConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=threads,
                        mutations=threads * per, width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=16 if big else 4096, seed=3,
