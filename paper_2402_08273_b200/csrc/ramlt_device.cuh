@@ -340,6 +340,83 @@ __device__ __forceinline__ bool hit_tri(const TriD<R> &tr, V3<R> o, V3<R> d, R &
     return false;
 }
 
+// Two triangles at a time for the brute-force scans: the determinant and u
+// test of both are computed back to back (independent chains: ILP), the rest
+// only when either passed -- the same operations and order per triangle as
+// hit_tri, so the same results; a miss returns +inf.  The scans stay in index
+// order with strict '<' (the linear scan's first minimum).
+template <class R>
+__device__ __forceinline__ void hit_tri2(const TriD<R> &ta, const TriD<R> &tb, V3<R> o, V3<R> d, R &xa, R &xb) {
+    const V3<R> pa = cross(d, ta.e2), pb = cross(d, tb.e2);
+    const R deta = dot(ta.e1, pa), detb = dot(tb.e1, pb);
+    const R inva = R(1) / deta, invb = R(1) / detb;
+    const V3<R> tva = sub(o, ta.a), tvb = sub(o, tb.a);
+    const R ua = dot(tva, pa) * inva, ub = dot(tvb, pb) * invb;
+    const bool oka = !(M<R>::abs(deta) < R(1e-14)) && !(ua < R(0) || ua > R(1));
+    const bool okb = !(M<R>::abs(detb) < R(1e-14)) && !(ub < R(0) || ub > R(1));
+    xa = xb = M<R>::inf();
+    if (oka || okb) {
+        const V3<R> qa = cross(tva, ta.e1), qb = cross(tvb, tb.e1);
+        const R va = dot(d, qa) * inva, vb = dot(d, qb) * invb;
+        const R tta = dot(ta.e2, qa) * inva, ttb = dot(tb.e2, qb) * invb;
+        if (oka && !(va < R(0) || ua + va > R(1)) && tta > R(kEpsD))
+            xa = tta;
+        if (okb && !(vb < R(0) || ub + vb > R(1)) && ttb > R(kEpsD))
+            xb = ttb;
+    }
+}
+
+#ifndef RAMLT_SCAN2
+#define RAMLT_SCAN2 1
+#endif
+// Closest hit over triangles first, first + step, ... < n (index order, strict '<').
+template <class R>
+__device__ __forceinline__ void scan_tris(const TriD<R> *tri, int first, int n, int step, V3<R> o, V3<R> d,
+                                          R &best, int &bi, int base) {
+    int j = first;
+#if RAMLT_SCAN2
+    for (; j + step < n; j += 2 * step) {
+        R xa, xb;
+        hit_tri2(tri[j], tri[j + step], o, d, xa, xb);
+        if (xa < best) {
+            best = xa;
+            bi = base + j;
+        }
+        if (xb < best) {
+            best = xb;
+            bi = base + j + step;
+        }
+    }
+#endif
+    for (; j < n; j += step) {
+        R t;
+        if (hit_tri(tri[j], o, d, t) && t < best) {
+            best = t;
+            bi = base + j;
+        }
+    }
+}
+
+// Any triangle of first, first + step, ... < n with a root below lim.
+template <class R>
+__device__ __forceinline__ bool any_tri(const TriD<R> *tri, int first, int n, int step, V3<R> o, V3<R> d, R lim) {
+    int j = first;
+#if RAMLT_SCAN2
+    for (; j + step < n; j += 2 * step) {
+        R xa, xb;
+        hit_tri2(tri[j], tri[j + step], o, d, xa, xb);
+        if (xa < lim || xb < lim)
+            return true;
+    }
+#endif
+    for (; j < n; j += step) {
+        R t;
+        if (hit_tri(tri[j], o, d, t) && t < lim)
+            return true;
+    }
+    return false;
+}
+
 // Read-only vector loads of BVH records (fp32: 2 x 32 B per node, 3 x 16 B per
 // leaf triangle through the non-coherent path) instead of one scalar load per
 // field.  The 256-bit node loads (LDG.E.ENL2.256, sm_100) raise the traversal
@@ -692,13 +769,7 @@ __device__ __forceinline__ bool intersect(const SceneView<R> &s, V3<R> o, V3<R> 
             bi = i;
         }
     }
-    for (int j = g.lane; j < s.ntri; j += G) {
-        R t;
-        if (hit_tri(s.tri[j], o, d, t) && t < best) {
-            best = t;
-            bi = s.nsph + j;
-        }
-    }
+    scan_tris(s.tri, g.lane, s.ntri, G, o, d, best, bi, s.nsph);
     if (G > 1) {
 #pragma unroll
         for (int off = G / 2; off > 0; off >>= 1) {
@@ -758,11 +829,8 @@ __device__ __forceinline__ bool visible(const SceneView<R> &s, V3<R> a, V3<R> b,
         if (hit_sphere(s.sph[i], a, d, t) && t < lim)
             occ = true;
     }
-    for (int j = g.lane; j < s.ntri && !occ; j += G) {
-        R t;
-        if (hit_tri(s.tri[j], a, d, t) && t < lim)
-            occ = true;
-    }
+    if (!occ)
+        occ = any_tri(s.tri, g.lane, s.ntri, G, a, d, lim);
     if (G > 1)
         occ = __any_sync(g.mask, occ);
     return !occ;

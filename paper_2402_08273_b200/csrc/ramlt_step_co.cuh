@@ -53,14 +53,7 @@ __device__ __forceinline__ int trace_ray(const SceneView<R> &s, const RayReq<R> 
             bi = i;
         }
     }
-#pragma unroll 2
-    for (int j = 0; j < s.ntri; ++j) {
-        R t;
-        if (hit_tri(s.tri[j], r.o, r.d, t) && t < best) {
-            best = t;
-            bi = s.nsph + j;
-        }
-    }
+    scan_tris(s.tri, 0, s.ntri, 1, r.o, r.d, best, bi, s.nsph);
     t_out = best;
     return bi;
     }
