@@ -303,12 +303,20 @@ def run_ours(args, wl, scene_text):
         dist.all_reduce(rays_t, op=dist.ReduceOp.SUM)
     k = eng.chain_lengths()
     k_bar = float(k.mean()) if k.size else float("nan")
+    ceiling = None
+    if wl["scene"] == "clusters" and rank == 0:
+        # the traversal-only ceiling of this BVH (k_trace_bench: the step kernel's
+        # traversal loop on incoherent closest-hit rays), measured after the timed region
+        eng.trace_benchmark(1 << 22)
+        n_rays = 1 << 26
+        tms, _ = eng.trace_benchmark(n_rays)
+        ceiling = n_rays / (tms / 1e3)
     eng.close()
     return dict(value=value, ms=ms_max, launches=launches, step_ms=step_ms,
                 step_launches=step_launches, rays_dev=float(rays_t.item()), muts=muts, clocks=clk.summary(),
                 world=world, rank=rank, local=local, mutations_per_rank=muts * plan.count / C,
                 acceptance=acc_window, burnin=dict(steps=burn, acceptance=burn_acc, max=args.burnin_max),
-                k_bar=k_bar)
+                k_bar=k_bar, ceiling=ceiling)
 
 
 def run_e2e(args, wl):
@@ -622,6 +630,14 @@ def main():
              if wl["scene"] == "clusters" else "k_step (chain-step megakernel)")
     roofline.update({"kernel": kname,
                      "kernel_share": res["step_ms"] / res["ms"] if res["ms"] else None})
+    if res.get("ceiling"):
+        dev_rays = res["rays_dev"] / (res["ms"] / 1e3) / max(res["world"], 1)
+        roofline["traversal_ceiling"] = {
+            "k_trace_bench_rays_per_s": res["ceiling"], "in_step_rays_per_s_per_gpu": dev_rays,
+            "frac": dev_rays / res["ceiling"],
+            "note": "the step kernel's BVH traversal loop alone on incoherent closest-hit rays, same BVH, "
+                    "same GPU (latency-bound: ncu long-scoreboard on node loads); the measured ceiling the "
+                    "in-step ray rate is compared with"}
     cpu = None
     if not args.no_cpu_baseline and res["world"] == 1:
         sample = args.cpu_sample or wl["cpu_sample"]
