@@ -297,6 +297,9 @@ def run_ours(args, wl, scene_text):
     launches = s1.kernel_launches - s0.kernel_launches
     step_ms = (s1.step_kernel_ms - s0.step_kernel_ms)
     step_launches = s1.step_kernel_launches - s0.step_kernel_launches
+    trace_ms = s1.trace_kernel_ms - s0.trace_kernel_ms
+    trace_launches = s1.trace_kernel_launches - s0.trace_kernel_launches
+    wf_rounds = s1.wavefront_rounds - s0.wavefront_rounds
     rays_dev = (s1.rays_closest + s1.rays_visibility) - (s0.rays_closest + s0.rays_visibility)
     rays_t = torch.tensor([float(rays_dev)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -313,7 +316,8 @@ def run_ours(args, wl, scene_text):
         ceiling = n_rays / (tms / 1e3)
     eng.close()
     return dict(value=value, ms=ms_max, launches=launches, step_ms=step_ms,
-                step_launches=step_launches, rays_dev=float(rays_t.item()), muts=muts, clocks=clk.summary(),
+                step_launches=step_launches, trace_ms=trace_ms, trace_launches=trace_launches,
+                wf_rounds=wf_rounds, rays_local=float(rays_dev), rays_dev=float(rays_t.item()), muts=muts, clocks=clk.summary(),
                 world=world, rank=rank, local=local, mutations_per_rank=muts * plan.count / C,
                 acceptance=acc_window, burnin=dict(steps=burn, acceptance=burn_acc, max=args.burnin_max),
                 k_bar=k_bar, ceiling=ceiling)
@@ -630,6 +634,23 @@ def main():
              if wl["scene"] == "clusters" else "k_step (chain-step megakernel)")
     roofline.update({"kernel": kname,
                      "kernel_share": res["step_ms"] / res["ms"] if res["ms"] else None})
+    if wl["bound"] != "fp32" and res.get("trace_ms"):
+        # wavefront step: the dominant kernel is the BVH tracer k_wf_trace; its
+        # algorithmic bytes are this rank's device rays x B_ray over its summed
+        # launch time (the chain-state traffic belongs to k_wf_logic)
+        ach = res["rays_local"] * b_ray / (res["trace_ms"] / 1e3) / 1e9
+        roofline.update({
+            "achieved": ach, "frac": ach / peak,
+            "work_per_unit": f"B_ray = {levels} BVH levels x 64 B + 4 x 48 B = {b_ray:.0f} B per device ray "
+                             f"(SURVEY.md §8(d) per-ray term); {res['rays_local'] / max(res['trace_launches'], 1):.0f} "
+                             f"rays per launch on average",
+            "kernel": "k_wf_trace (wavefront BVH tracer: persistent, dynamic ray fetch, while-while rounds)",
+            "kernel_share": res["trace_ms"] / res["ms"] if res["ms"] else None,
+            "launches": res["trace_launches"],
+            "step": {"wavefront_rounds_per_step": res["wf_rounds"] / max(args.steps, 1),
+                     "k_wf_logic_share": (res["step_ms"] - res["trace_ms"]) / res["ms"] if res["ms"] else None,
+                     "state_model_bytes_per_mutation": bytes_per_mut,
+                     "state_model_note": "R_m x B_ray + B_state (the whole-step byte model of round 1)"}})
     if res.get("ceiling"):
         dev_rays = res["rays_dev"] / (res["ms"] / 1e3) / max(res["world"], 1)
         roofline["traversal_ceiling"] = {

@@ -165,6 +165,9 @@ typedef struct ramlt_stats {
     uint64_t kernel_launches;    /* engine kernels launched so far */
     double step_kernel_ms;       /* summed event time of chain-step launches (profile_kernels) */
     uint64_t step_kernel_launches;
+    double trace_kernel_ms;      /* wavefront steps: summed event time of the k_wf_trace launches */
+    uint64_t trace_kernel_launches;
+    uint64_t wavefront_rounds;   /* wavefront steps: logic/trace rounds launched */
 } ramlt_stats;
 
 /* UpdateEvent trace row (driver.hpp:59-62, adaptation.hpp:51-56). */

@@ -67,7 +67,8 @@ class ramlt_stats(C.Structure):
         ("rays_closest", C.c_uint64), ("rays_visibility", C.c_uint64),
         ("n_tallies", C.c_uint64), ("n_trace", C.c_uint64), ("n_metrics", C.c_uint64),
         ("kernel_launches", C.c_uint64), ("step_kernel_ms", C.c_double),
-        ("step_kernel_launches", C.c_uint64),
+        ("step_kernel_launches", C.c_uint64), ("trace_kernel_ms", C.c_double),
+        ("trace_kernel_launches", C.c_uint64), ("wavefront_rounds", C.c_uint64),
     ]
 
 

@@ -60,7 +60,8 @@ struct Builder {
     std::vector<int32_t> &idx;
     std::vector<BvhBuildNode> nodes;
     int leaf_max;
-    int bins = 32;          // RAMLT_BVH_BINS: binned-SAH bins per axis (<= 64); 32: traversal +4 % over 16
+    int bins = 64;          // RAMLT_BVH_BINS: binned-SAH bins per axis (<= 256); c5 scene, node fetches per path ray
+                            // (tools/bvh_stats.cpp): 16 -> 32 bins -4 %, 32 -> 64 -6 %, 128 / 256 no further gain
     double sah_ct = 0.0;    // RAMLT_BVH_CT > 0: SAH leaf termination, node cost / triangle cost
     int depth = 0;
     int par_depth = -1;                 // >= 0: defer subtrees starting at this depth
@@ -68,7 +69,7 @@ struct Builder {
 
     Builder(Shared *s, int lm) : sh(s), tb(s->tb), cen(s->cen), idx(s->idx), leaf_max(lm) {
         if (const char *v = std::getenv("RAMLT_BVH_BINS"))
-            bins = std::max(4, std::min(64, std::atoi(v)));
+            bins = std::max(4, std::min(256, std::atoi(v)));
         if (const char *v = std::getenv("RAMLT_BVH_CT"))
             sah_ct = std::atof(v);
     }
@@ -104,7 +105,7 @@ struct Builder {
         cb.reset();
         for (int i = s; i < e; ++i)
             cb.grow(&cen[3 * idx[i]]);
-        constexpr int BMAX = 64;
+        constexpr int BMAX = 256;
         const int B = bins;
         double best_cost = std::numeric_limits<double>::infinity();
         int best_axis = -1, best_bin = -1;
@@ -263,7 +264,26 @@ BvhBuild build_bvh(const double *tris, size_t n, int leaf_max) {
             b.par_depth = 6;
             b.tasks = &tasks;
         }
-        int32_t r = b.build(0, static_cast<int>(n), 0);
+        // Large triangles (room walls, area lights) split off at the root: their
+        // boxes span the scene, and binned on centroids they would inflate the
+        // boxes of the clusters they share bins with.  RAMLT_BVH_ISOLATE: the
+        // threshold as a fraction of the scene box's surface area (0: off).
+        // c5 scene: 1e-3 isolates the 20 room/light triangles, node fetches per
+        // path ray 67.9 -> 62.5 (tools/bvh_stats.cpp).
+        double iso = 1e-3;
+        if (const char *v = std::getenv("RAMLT_BVH_ISOLATE"))
+            iso = std::atof(v);
+        int m_large = 0;
+        if (iso > 0.0) {
+            Box all = b.range_box(0, static_cast<int>(n));
+            const double lim = iso * all.area();
+            auto mid = std::stable_partition(sh.idx.begin(), sh.idx.end(),
+                                             [&](int32_t t) { return sh.tb[t].area() > lim; });
+            m_large = static_cast<int>(mid - sh.idx.begin());
+            if (m_large == static_cast<int>(n))
+                m_large = 0;
+        }
+        int32_t r = m_large > 0 ? b.node(0, m_large, static_cast<int>(n), 0) : b.build(0, static_cast<int>(n), 0);
         if (r < 0)   // degenerate set collapsed into one leaf
             wrap_leaf(r);
         std::vector<Builder *> subs(tasks.size(), nullptr);

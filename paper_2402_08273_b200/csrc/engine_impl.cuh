@@ -6,6 +6,8 @@
 #include "engine.h"
 #include "ramlt_kernels.cuh"
 #include "ramlt_step_co.cuh"
+#include "ramlt_wavefront.cuh"
+#include "bvh_layout.h"
 
 #include <algorithm>
 #include <chrono>
@@ -139,6 +141,7 @@ private:
                      unsigned long long rem, bool record);
     void adapt_after_step(int j, unsigned long long span_start);
     template <bool INIT = false> void launch_step_co(const rd::StepParams<R> &P);
+    template <int RK> void launch_step_wf(rd::StepParams<R> P);
     bool launch_coop(int j0, int j1, unsigned long long span_start, unsigned long long per,
                      unsigned long long rem);
     int coop_state_ = -1;   // -1 unknown, 0 unavailable, 1 usable
@@ -171,8 +174,7 @@ private:
     DBuf<rd::SphD<R>> sph_;
     DBuf<rd::MatD<R>> mat_;
     DBuf<rd::V3<R>> emit_;
-    DBuf<rd::BvhNodeD<R>> bvh_;
-    DBuf<rd::TriT<R>> trt_;
+    DBuf<unsigned char> bvh_;   // BVH units: nodes + leaf triangle records (bvh_layout.h)
     bool use_bvh_ = false;
     int bvh_depth_ = 0;
     // chains
@@ -199,6 +201,17 @@ private:
     int init_refill_ = 8;     // the same for chain initialisation (RAMLT_CO_INIT_REFILL; c4 init 8/16/24/32: 0.81/0.84/0.85/0.95 s)
     int refill_ = 24;         // k_step_co (BVH): RAMLT_CO_REFILL idle lanes end a traversal round (c4: 4/8/16/24/28/32 -> 62.3/65.8/70.0/71.8/72.2/71.3 M)
     int co_carveout_ = -1;    // k_step_co: RAMLT_CO_CARVEOUT percent (-1: driver default)
+    // wavefront step (BVH scenes, ramlt_wavefront.cuh): RAMLT_STEP_KERNEL=wf (default) | co
+    bool use_wf_ = false;
+    int wf_refill_ = 8;       // k_wf_trace: RAMLT_WF_REFILL idle lanes end a traversal round
+    int wf_check_ = 4;        // rounds between host checks of the queue length (RAMLT_WF_CHECK)
+    DBuf<uint4> wf_state_;
+    DBuf<rd::GV<R>> wf_pv_;
+    DBuf<rd::WfRay<R>> wf_rays_[2];
+    DBuf<rd::WfHit<R>> wf_hits_[2];
+    DBuf<unsigned> wf_cnt_;   // queue lengths [2], trace work counter
+    unsigned *wf_host_ = nullptr;   // pinned: queue length read back every wf_check_ rounds
+    uint64_t wf_rounds_ = 0;
     // film
     DBuf<double> film64_;
     DBuf<float4> film32_;
@@ -239,9 +252,9 @@ private:
     ramlt_stats final_{};
     bool finalized_ = false;
     // live kernel timing (profile_kernels): event pairs around chain-step launches
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_;
-    double step_ms_ = 0.0;
-    uint64_t step_launches_ = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_, ev_trace_;
+    double step_ms_ = 0.0, trace_ms_ = 0.0;
+    uint64_t step_launches_ = 0, trace_launches_ = 0;
     void drain_events();
     // launch configuration cache: the dynamic-smem attribute is set and the
     // occupancy queried once per (kernel, smem) instead of on every launch
@@ -356,42 +369,9 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         for (size_t i = 0; i < tris.size(); ++i)
             ordered[i] = tris[static_cast<size_t>(bb.order[i])];
         tris.swap(ordered);
-        std::vector<rd::TriT<R>> trt(tris.size());
-        for (size_t i = 0; i < tris.size(); ++i) {
-            const rd::TriD<R> &t = tris[i];
-            trt[i].a[0] = t.a.x, trt[i].a[1] = t.a.y, trt[i].a[2] = t.a.z;
-            trt[i].e1[0] = t.e1.x, trt[i].e1[1] = t.e1.y, trt[i].e1[2] = t.e1.z;
-            trt[i].e2[0] = t.e2.x, trt[i].e2[1] = t.e2.y, trt[i].e2[2] = t.e2.z;
-            trt[i].orig = t.orig;
-        }
-        trt_.alloc(trt.size());
-        RAMLT_CUDA(cudaMemcpy(trt_.p, trt.data(), trt.size() * sizeof(trt[0]), cudaMemcpyHostToDevice));
-        auto down = [](double x) {
-            R r = static_cast<R>(x);
-            if (static_cast<double>(r) > x)
-                r = std::nextafter(r, -std::numeric_limits<R>::infinity());
-            return r;
-        };
-        auto up = [](double x) {
-            R r = static_cast<R>(x);
-            if (static_cast<double>(r) < x)
-                r = std::nextafter(r, std::numeric_limits<R>::infinity());
-            return r;
-        };
-        std::vector<rd::BvhNodeD<R>> nodes(bb.nodes.size());
-        for (size_t i = 0; i < nodes.size(); ++i) {
-            const BvhBuildNode &b = bb.nodes[i];
-            for (int k = 0; k < 3; ++k) {
-                nodes[i].lo0[k] = down(b.lo[0][k]);
-                nodes[i].hi0[k] = up(b.hi[0][k]);
-                nodes[i].lo1[k] = down(b.lo[1][k]);
-                nodes[i].hi1[k] = up(b.hi[1][k]);
-            }
-            nodes[i].c0 = b.child[0];
-            nodes[i].c1 = b.child[1];
-        }
-        bvh_.alloc(nodes.size());
-        RAMLT_CUDA(cudaMemcpy(bvh_.p, nodes.data(), nodes.size() * sizeof(nodes[0]), cudaMemcpyHostToDevice));
+        std::vector<unsigned char> units = layout_bvh<R>(bb, tris);
+        bvh_.alloc(units.size());
+        RAMLT_CUDA(cudaMemcpy(bvh_.p, units.data(), units.size(), cudaMemcpyHostToDevice));
     }
     std::vector<rd::SphD<R>> sphs(hs_.sph.size());
     for (size_t i = 0; i < hs_.sph.size(); ++i) {
@@ -462,12 +442,18 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     // scenes with the lane-group megakernel; RAMLT_STEP_KERNEL=mega|co|co_static overrides.
     use_co_ = use_bvh_;
     use_co_init_ = use_bvh_;
+    use_wf_ = use_bvh_;
     if (const char *v = std::getenv("RAMLT_INIT_KERNEL"))
         use_co_init_ = std::string(v) == "co";
     if (const char *v = std::getenv("RAMLT_STEP_KERNEL")) {
-        use_co_ = std::string(v) == "co" || std::string(v) == "co_static";
+        use_co_ = std::string(v) == "co" || std::string(v) == "co_static" || std::string(v) == "wf";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
+        use_wf_ = use_bvh_ && std::string(v) == "wf";
     }
+    if (const char *v = std::getenv("RAMLT_WF_REFILL"))
+        wf_refill_ = std::min(32, std::max(1, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_WF_CHECK"))
+        wf_check_ = std::min(64, std::max(1, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_CO_PV"))
         co_pv_global_ = std::string(v) != "smem";
     if (const char *v = std::getenv("RAMLT_CO_CARVEOUT"))
@@ -575,9 +561,25 @@ template <class R> void EngineT<R>::drain_events() {
         cudaEventDestroy(e.second);
     }
     ev_.clear();
+    for (auto &e : ev_trace_) {
+        RAMLT_CUDA(cudaEventSynchronize(e.second));
+        float ms = 0.f;
+        RAMLT_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+        trace_ms_ += ms;
+        ++trace_launches_;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    ev_trace_.clear();
 }
 
 template <class R> EngineT<R>::~EngineT() {
+    if (wf_host_)
+        cudaFreeHost(wf_host_);
+    for (auto &e : ev_trace_) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
     for (auto &e : ev_) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -672,7 +674,6 @@ template <class R> rd::StepParams<R> EngineT<R>::params() const {
     P.scene.cam.area = static_cast<R>(cb_.area);
     P.scene.cam.sensor = static_cast<R>(cb_.sensor);
     P.scene.bvh = use_bvh_ ? bvh_.p : nullptr;
-    P.scene.trt = use_bvh_ ? trt_.p : nullptr;
     P.C = C_;
     P.C_total = Ctot_;
     P.chain_off = off_;
@@ -918,7 +919,15 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     if (G_ == 1 && use_co_) {
         P.steal = steal_;
         P.refill = refill_;
-        launch_step_co(P);
+        if (use_wf_) {
+            P.refill = wf_refill_;
+            if (d_.rng == RAMLT_RNG_PHILOX)
+                launch_step_wf<rd::RNG_PHILOX>(P);
+            else
+                launch_step_wf<rd::RNG_PCG>(P);
+        } else {
+            launch_step_co(P);
+        }
         return;
     }
     const long long threads = static_cast<long long>(C_) * G_;
@@ -943,7 +952,7 @@ void EngineT<R>::launch_step(int j0, int j1, unsigned long long span_start, unsi
     prepare(reinterpret_cast<const void *>(kern), smem_);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d_.profile_kernels) {
-        if (ev_.size() >= 4096)
+        if (ev_.size() + ev_trace_.size() >= 4096)
             drain_events();
         RAMLT_CUDA(cudaEventCreate(&e0));
         RAMLT_CUDA(cudaEventCreate(&e1));
@@ -985,7 +994,7 @@ void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
     RAMLT_CUDA(cudaMemsetAsync(work_.p, 0, sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d_.profile_kernels && !INIT) {
-        if (ev_.size() >= 4096)
+        if (ev_.size() + ev_trace_.size() >= 4096)
             drain_events();
         RAMLT_CUDA(cudaEventCreate(&e0));
         RAMLT_CUDA(cudaEventCreate(&e1));
@@ -995,6 +1004,86 @@ void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
     ++launches_;
     RAMLT_CUDA(cudaGetLastError());
     if (d_.profile_kernels && !INIT) {
+        RAMLT_CUDA(cudaEventRecord(e1, stream_));
+        ev_.emplace_back(e0, e1);
+    }
+}
+
+// Wavefront lockstep step (ramlt_wavefront.cuh): k_wf_logic / k_wf_trace rounds
+// until no chain has a ray pending.  The queue length is read back every
+// wf_check_ rounds; the rounds launched past the last ray find empty queues
+// and exit at once.
+template <class R>
+template <int RK>
+void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
+    const size_t C = static_cast<size_t>(C_);
+    constexpr int K = rd::Chunks<rd::WfState<R, RK>>::K;
+    if (wf_state_.n < K * C) {
+        wf_state_.alloc(K * C);
+        wf_pv_.alloc(static_cast<size_t>(d_.max_vertices) * C);
+        for (int q = 0; q < 2; ++q) {
+            wf_rays_[q].alloc(C);
+            wf_hits_[q].alloc(C);
+        }
+        wf_cnt_.alloc(4);
+        if (!wf_host_)
+            RAMLT_CUDA(cudaMallocHost(&wf_host_, sizeof(unsigned)));
+    }
+    auto logic = rd::k_wf_logic<R, RK>;
+    auto trace = rd::k_wf_trace<R>;
+    const size_t lsmem = smem_;
+    size_t tsmem = (smem_ + 15) & ~size_t(15);
+    P.co_stack_off = static_cast<unsigned>(tsmem);
+    tsmem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
+    const int lper = prepare(reinterpret_cast<const void *>(logic), lsmem);
+    const int tper = prepare(reinterpret_cast<const void *>(trace), tsmem);
+    const unsigned lblocks = std::min<unsigned>(static_cast<unsigned>((C + 127) / 128),
+                                                static_cast<unsigned>(std::max(lper, 1) * sms_));
+    const unsigned tblocks = static_cast<unsigned>(std::max(tper, 1) * sms_);
+    unsigned *cnt = wf_cnt_.p;
+    RAMLT_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned), stream_));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (d_.profile_kernels) {
+        if (ev_.size() + ev_trace_.size() >= 4096)
+            drain_events();
+        RAMLT_CUDA(cudaEventCreate(&e0));
+        RAMLT_CUDA(cudaEventCreate(&e1));
+        RAMLT_CUDA(cudaEventRecord(e0, stream_));
+    }
+    rd::WfParams<R> W;
+    W.trace_work = cnt + 2;
+    W.state = wf_state_.p;
+    W.pv = wf_pv_.p;
+    for (int r = 0;; ++r) {
+        const int a = r & 1;
+        W.rays_in = wf_rays_[a ^ 1].p;
+        W.hits_in = wf_hits_[a ^ 1].p;
+        W.n_in = cnt + (a ^ 1);
+        W.rays_out = wf_rays_[a].p;
+        W.n_out = cnt + a;
+        logic<<<lblocks, 128, lsmem, stream_>>>(P, W, r == 0 ? 1 : 0);
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        if (d_.profile_kernels) {
+            RAMLT_CUDA(cudaEventCreate(&t0));
+            RAMLT_CUDA(cudaEventCreate(&t1));
+            RAMLT_CUDA(cudaEventRecord(t0, stream_));
+        }
+        trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_[a].p, wf_hits_[a].p, cnt + a, cnt + 2, cnt + (a ^ 1));
+        if (d_.profile_kernels) {
+            RAMLT_CUDA(cudaEventRecord(t1, stream_));
+            ev_trace_.emplace_back(t0, t1);
+        }
+        launches_ += 2;
+        ++wf_rounds_;
+        RAMLT_CUDA(cudaGetLastError());
+        if (r % wf_check_ == wf_check_ - 1) {
+            RAMLT_CUDA(cudaMemcpyAsync(wf_host_, cnt + a, sizeof(unsigned), cudaMemcpyDeviceToHost, stream_));
+            RAMLT_CUDA(cudaStreamSynchronize(stream_));
+            if (*wf_host_ == 0)
+                break;
+        }
+    }
+    if (d_.profile_kernels) {
         RAMLT_CUDA(cudaEventRecord(e1, stream_));
         ev_.emplace_back(e0, e1);
     }
@@ -1063,7 +1152,7 @@ bool EngineT<R>::launch_coop(int j0, int j1, unsigned long long span_start, unsi
     void *args[] = {&P, &A};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d_.profile_kernels) {
-        if (ev_.size() >= 4096)
+        if (ev_.size() + ev_trace_.size() >= 4096)
             drain_events();
         RAMLT_CUDA(cudaEventCreate(&e0));
         RAMLT_CUDA(cudaEventCreate(&e1));
@@ -1451,6 +1540,9 @@ template <class R> void EngineT<R>::read_stats(ramlt_stats *out) {
     drain_events();
     s.step_kernel_ms = step_ms_;
     s.step_kernel_launches = step_launches_;
+    s.trace_kernel_ms = trace_ms_;
+    s.trace_kernel_launches = trace_launches_;
+    s.wavefront_rounds = wf_rounds_;
     *out = s;
 }
 

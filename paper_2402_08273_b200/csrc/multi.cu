@@ -339,6 +339,9 @@ public:
                 s.kernel_launches += si.kernel_launches;
                 s.step_kernel_ms = std::max(s.step_kernel_ms, si.step_kernel_ms);
                 s.step_kernel_launches += si.step_kernel_launches;
+                s.trace_kernel_ms = std::max(s.trace_kernel_ms, si.trace_kernel_ms);
+                s.trace_kernel_launches += si.trace_kernel_launches;
+                s.wavefront_rounds = std::max(s.wavefront_rounds, si.wavefront_rounds);
             }
             acc_sum += si.mean_acceptance * static_cast<double>(si.perturbation_proposals);
             lum += si.film_luminance;

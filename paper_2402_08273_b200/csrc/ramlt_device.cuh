@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace rd {
@@ -228,21 +229,52 @@ template <class R> struct TriD {   // a, e1 = b - a, e2 = c - a, n = normalize(c
     int pad_;
 };
 
-// Leaf-test record of a BVH-ordered triangle: only what Moeller-Trumbore reads
-// (48 B in fp32); the hit record (normal, material, emitter) comes from TriD.
-template <class R> struct alignas(16) TriT {
+// ---- BVH record formats -------------------------------------------------------------
+// One array of fixed-size units holds the whole BVH: internal nodes (one unit)
+// and, in place of each leaf, its triangles' leaf-test records (TU units
+// each).  The two children of a node are stored back to back at `base`:
+// child 0 at base, child 1 right after it (1 unit for an internal node,
+// cnt * TU units for a leaf of cnt triangles).  Traversal is bound by the
+// L1 data pipe -- one wavefront per 32 B sector a lane touches (k_trace_bench:
+// l1tex data-pipe wavefronts 93 % of peak, profiles/r02h) -- so records are
+// sized in sectors: a quantised node is one 32 B sector (RAMLT_QNODE=1), a
+// leaf triangle two (two 256-bit loads instead of three 16 B loads).
+#ifndef RAMLT_QNODE
+#define RAMLT_QNODE 0
+#endif
+// Leaf-test record: what Moeller-Trumbore reads plus the triangle's index in
+// the scene (tie-break) and its position in the BVH-ordered TriD array (hit
+// record: normal, material, emitter).  64 B in fp32, 128 B in fp64.
+template <class R> struct alignas(sizeof(R) == 4 ? 64 : 128) TriT {
     R a[3], e1[3], e2[3];
-    int orig;
+    int orig, pos;
 };
-
-// BVH2 node: both children's boxes (padded outward at build time); child >= 0
-// internal node, < 0 leaf ~((first << 4) | count) into the reordered triangles.
-template <class R> struct alignas(16) BvhNodeD {
+// Quantised node (RAMLT_QNODE=1): the children's boxes as 8-bit offsets on a
+// per-axis power-of-two grid anchored at `org` (rounded outward at build
+// time, so the decoded box contains the padded exact box).  32 B in fp32.
+//   ex[k]: biased exponent of the grid step 2^(ex[k] - 127)
+//   meta: cnt0 | cnt1 << 4 (0: internal child)
+//   q: lo0 xyz, hi0 xyz, lo1 xyz, hi1 xyz
+template <class R> struct alignas(sizeof(R) == 4 ? 32 : 64) QNode {
+    R org[3];
+    uint8_t ex[3], meta;
+    uint8_t q[12];
+    int32_t base;
+};
+// Plain node (RAMLT_QNODE=0): both children's boxes in R, same child rule.
+template <class R> struct alignas(sizeof(R) == 4 ? 64 : 128) PNode {
     R lo0[3], hi0[3], lo1[3], hi1[3];
-    int c0, c1;
+    int32_t base, meta;
 };
-static_assert(sizeof(BvhNodeD<float>) == 64, "ld_node reads 4 x 16 B");
-static_assert(sizeof(TriT<float>) == 48, "ld_trit reads 3 x 16 B");
+template <class R> struct BvhFmt {
+    using Node = typename std::conditional<RAMLT_QNODE != 0, QNode<R>, PNode<R>>::type;
+    static constexpr int U = static_cast<int>(sizeof(Node));              // unit bytes
+    static constexpr int TU = static_cast<int>(sizeof(TriT<R>)) / U;      // units per triangle
+};
+static_assert(sizeof(QNode<float>) == 32 && sizeof(TriT<float>) == 64, "fp32 records are 1 and 2 sectors");
+static_assert(sizeof(TriT<double>) % sizeof(QNode<double>) == 0 && sizeof(TriT<double>) % sizeof(PNode<double>) == 0,
+              "triangle records are whole units");
+static_assert(sizeof(TriT<float>) % sizeof(PNode<float>) == 0, "triangle records are whole units");
 template <class R> struct SphD {
     V3<R> c;
     R r;
@@ -265,8 +297,7 @@ template <class R> struct SceneView {
     const V3<R> *emit;
     int ntri, nsph;
     CamD<R> cam;
-    const BvhNodeD<R> *bvh;   // null: brute force over (smem-staged) triangles
-    const TriT<R> *trt;       // BVH-ordered leaf-test records (with bvh)
+    const unsigned char *bvh;   // BVH units (nodes + leaf triangles); null: brute force over smem-staged triangles
 };
 
 template <class R> struct Hit {
@@ -417,38 +448,28 @@ __device__ __forceinline__ bool any_tri(const TriD<R> *tri, int first, int n, in
     return false;
 }
 
-// Read-only vector loads of BVH records (fp32: 2 x 32 B per node, 3 x 16 B per
-// leaf triangle through the non-coherent path) instead of one scalar load per
-// field.  The 256-bit node loads (LDG.E.ENL2.256, sm_100) raise the traversal
-// probe from 941 to 1080 M incoherent rays/s (profiles/r01h/trace_bench.txt).
-template <class R> __device__ __forceinline__ BvhNodeD<R> ld_node(const BvhNodeD<R> *p) { return *p; }
-// sm_100 256-bit loads (LDG.E.ENL2.256): a 64 B node in two requests.
+// ---- BVH record loads -------------------------------------------------------------------
+// sm_100 256-bit loads (LDG.E.ENL2.256): one 32 B sector per request.
 __device__ __forceinline__ void ldg256(const void *p, float4 &a, float4 &b) {
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
         : "l"(p));
 }
-template <> __device__ __forceinline__ BvhNodeD<float> ld_node(const BvhNodeD<float> *p) {
-    float4 a, b, c, e;
-    ldg256(p, a, b);
-    ldg256(reinterpret_cast<const char *>(p) + 32, c, e);
-    BvhNodeD<float> n;
-    n.lo0[0] = a.x, n.lo0[1] = a.y, n.lo0[2] = a.z, n.hi0[0] = a.w;
-    n.hi0[1] = b.x, n.hi0[2] = b.y, n.lo1[0] = b.z, n.lo1[1] = b.w;
-    n.lo1[2] = c.x, n.hi1[0] = c.y, n.hi1[1] = c.z, n.hi1[2] = c.w;
-    n.c0 = __float_as_int(e.x);
-    n.c1 = __float_as_int(e.y);
-    return n;
+
+// Leaf-test record of the triangle at BVH unit address p (two sectors in fp32).
+template <class R> __device__ __forceinline__ TriT<R> ld_trit(const unsigned char *p) {
+    return *reinterpret_cast<const TriT<R> *>(p);
 }
-template <class R> __device__ __forceinline__ TriT<R> ld_trit(const TriT<R> *p) { return *p; }
-template <> __device__ __forceinline__ TriT<float> ld_trit(const TriT<float> *p) {
-    const float4 *q = reinterpret_cast<const float4 *>(p);
-    float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+template <> __device__ __forceinline__ TriT<float> ld_trit<float>(const unsigned char *p) {
+    float4 a, b;
+    ldg256(p, a, b);
+    const float4 c = __ldg(reinterpret_cast<const float4 *>(p + 32));
     TriT<float> t;
     t.a[0] = a.x, t.a[1] = a.y, t.a[2] = a.z, t.e1[0] = a.w;
     t.e1[1] = b.x, t.e1[2] = b.y, t.e2[0] = b.z, t.e2[1] = b.w;
     t.e2[2] = c.x;
     t.orig = __float_as_int(c.y);
+    t.pos = __float_as_int(c.z);
     return t;
 }
 
@@ -492,13 +513,9 @@ template <> struct Slack<double> {
     static __device__ __forceinline__ double v() { return 1.0 + 1e-13; }
 };
 
-// Slab test as fma(lo, inv, -o*inv): one FFMA per plane; the outward padding
-// and the relative slack absorb the different rounding.
+// Slab test on the six plane parameters of one box.
 template <class R>
-__device__ __forceinline__ bool slab(const R lo[3], const R hi[3], V3<R> oinv, V3<R> inv, R tcap, R &tnear) {
-    R tx0 = M<R>::fma(lo[0], inv.x, -oinv.x), tx1 = M<R>::fma(hi[0], inv.x, -oinv.x);
-    R ty0 = M<R>::fma(lo[1], inv.y, -oinv.y), ty1 = M<R>::fma(hi[1], inv.y, -oinv.y);
-    R tz0 = M<R>::fma(lo[2], inv.z, -oinv.z), tz1 = M<R>::fma(hi[2], inv.z, -oinv.z);
+__device__ __forceinline__ bool slab_t(R tx0, R tx1, R ty0, R ty1, R tz0, R tz1, R tcap, R &tnear) {
     R tmin = fmax(fmax(fmin(tx0, tx1), fmin(ty0, ty1)), fmin(tz0, tz1));
     R tmax = fmin(fmin(fmax(tx0, tx1), fmax(ty0, ty1)), fmax(tz0, tz1));
     tmax = tmax * Slack<R>::v();
@@ -512,6 +529,102 @@ template <class R> __device__ __forceinline__ V3<R> safe_inv(V3<R> d) {
     R y = M<R>::abs(d.y) < tiny ? M<R>::copysign(tiny, d.y) : d.y;
     R z = M<R>::abs(d.z) < tiny ? M<R>::copysign(tiny, d.z) : d.z;
     return mk(R(1) / x, R(1) / y, R(1) / z);
+}
+
+// Child references: >= 0 internal node (unit index), < 0 leaf ~((unit << 4) | cnt).
+__device__ __forceinline__ void child_refs(int base, unsigned meta, int tu, int &c0, int &c1) {
+    const int n0 = static_cast<int>(meta & 15u), n1 = static_cast<int>((meta >> 4) & 15u);
+    const int b1 = base + (n0 ? n0 * tu : 1);
+    c0 = n0 ? ~((base << 4) | n0) : base;
+    c1 = n1 ? ~((b1 << 4) | n1) : b1;
+}
+
+template <class R> struct NodeHit {
+    R t0, t1;
+    int c0, c1;
+    bool h0, h1;
+};
+
+// Quantised planes: plane = org + q * 2^e, so t = (plane - o) / d = q * A + B
+// with A = 2^e * inv (exact: a power-of-two scaling) and B = org * inv - o * inv
+// (one FMA per axis and node), then one FMA per plane as for unquantised boxes.
+__device__ __forceinline__ float qbyte(unsigned w, unsigned i) {
+    // 2^23 + byte as a float bit pattern (one PRMT), minus 2^23: exact
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | i)) - 8388608.0f;
+}
+
+template <class R>
+__device__ __forceinline__ NodeHit<R> visit_node(const unsigned char *__restrict__ bvh, int node, V3<R> inv,
+                                                 V3<R> oinv, R tcap) {
+    NodeHit<R> r;
+    if constexpr (RAMLT_QNODE != 0) {
+        const QNode<R> n = *reinterpret_cast<const QNode<R> *>(bvh + static_cast<size_t>(node) * BvhFmt<R>::U);
+        auto scale = [](uint8_t e) {
+            return sizeof(R) == 4 ? R(__uint_as_float(static_cast<unsigned>(e) << 23))
+                                  : R(__longlong_as_double(static_cast<long long>(e - 127 + 1023) << 52));
+        };
+        const V3<R> A = mk(scale(n.ex[0]) * inv.x, scale(n.ex[1]) * inv.y, scale(n.ex[2]) * inv.z);
+        const V3<R> B = mk(M<R>::fma(n.org[0], inv.x, -oinv.x), M<R>::fma(n.org[1], inv.y, -oinv.y),
+                           M<R>::fma(n.org[2], inv.z, -oinv.z));
+        R t[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+            const int ax = k % 3;
+            t[k] = M<R>::fma(R(n.q[k]), ax == 0 ? A.x : (ax == 1 ? A.y : A.z), ax == 0 ? B.x : (ax == 1 ? B.y : B.z));
+        }
+        r.h0 = slab_t(t[0], t[3], t[1], t[4], t[2], t[5], tcap, r.t0);
+        r.h1 = slab_t(t[6], t[9], t[7], t[10], t[8], t[11], tcap, r.t1);
+        child_refs(n.base, n.meta, BvhFmt<R>::TU, r.c0, r.c1);
+    } else {
+        const PNode<R> n = *reinterpret_cast<const PNode<R> *>(bvh + static_cast<size_t>(node) * BvhFmt<R>::U);
+        r.h0 = slab_t(M<R>::fma(n.lo0[0], inv.x, -oinv.x), M<R>::fma(n.hi0[0], inv.x, -oinv.x),
+                      M<R>::fma(n.lo0[1], inv.y, -oinv.y), M<R>::fma(n.hi0[1], inv.y, -oinv.y),
+                      M<R>::fma(n.lo0[2], inv.z, -oinv.z), M<R>::fma(n.hi0[2], inv.z, -oinv.z), tcap, r.t0);
+        r.h1 = slab_t(M<R>::fma(n.lo1[0], inv.x, -oinv.x), M<R>::fma(n.hi1[0], inv.x, -oinv.x),
+                      M<R>::fma(n.lo1[1], inv.y, -oinv.y), M<R>::fma(n.hi1[1], inv.y, -oinv.y),
+                      M<R>::fma(n.lo1[2], inv.z, -oinv.z), M<R>::fma(n.hi1[2], inv.z, -oinv.z), tcap, r.t1);
+        child_refs(n.base, static_cast<unsigned>(n.meta), BvhFmt<R>::TU, r.c0, r.c1);
+    }
+    return r;
+}
+
+// fp32: one 256-bit load per node (quantised) or two (plain).
+template <>
+__device__ __forceinline__ NodeHit<float> visit_node<float>(const unsigned char *__restrict__ bvh, int node,
+                                                            V3<float> inv, V3<float> oinv, float tcap) {
+    NodeHit<float> r;
+    const unsigned char *p = bvh + static_cast<size_t>(node) * BvhFmt<float>::U;
+    float4 a, b;
+    ldg256(p, a, b);
+#if RAMLT_QNODE
+    // a = org xyz, (ex0 ex1 ex2 meta); b = q[0..3], q[4..7], q[8..11], base
+    const unsigned w3 = __float_as_uint(a.w), w4 = __float_as_uint(b.x), w5 = __float_as_uint(b.y),
+                   w6 = __float_as_uint(b.z);
+    const float Ax = __uint_as_float((w3 & 0xFFu) << 23) * inv.x;
+    const float Ay = __uint_as_float(((w3 >> 8) & 0xFFu) << 23) * inv.y;
+    const float Az = __uint_as_float(((w3 >> 16) & 0xFFu) << 23) * inv.z;
+    const float Bx = fmaf(a.x, inv.x, -oinv.x), By = fmaf(a.y, inv.y, -oinv.y), Bz = fmaf(a.z, inv.z, -oinv.z);
+    r.h0 = slab_t(fmaf(qbyte(w4, 0), Ax, Bx), fmaf(qbyte(w4, 3), Ax, Bx), fmaf(qbyte(w4, 1), Ay, By),
+                  fmaf(qbyte(w5, 0), Ay, By), fmaf(qbyte(w4, 2), Az, Bz), fmaf(qbyte(w5, 1), Az, Bz), tcap, r.t0);
+    r.h1 = slab_t(fmaf(qbyte(w5, 2), Ax, Bx), fmaf(qbyte(w6, 1), Ax, Bx), fmaf(qbyte(w5, 3), Ay, By),
+                  fmaf(qbyte(w6, 2), Ay, By), fmaf(qbyte(w6, 0), Az, Bz), fmaf(qbyte(w6, 3), Az, Bz), tcap, r.t1);
+    child_refs(__float_as_int(b.w), w3 >> 24, BvhFmt<float>::TU, r.c0, r.c1);
+#else
+    float4 c, e;
+    ldg256(p + 32, c, e);
+    // lo0 xyz hi0 x | hi0 yz lo1 xy | lo1 z hi1 xyz | base meta
+    r.h0 = slab_t(fmaf(a.x, inv.x, -oinv.x), fmaf(a.w, inv.x, -oinv.x), fmaf(a.y, inv.y, -oinv.y),
+                  fmaf(b.x, inv.y, -oinv.y), fmaf(a.z, inv.z, -oinv.z), fmaf(b.y, inv.z, -oinv.z), tcap, r.t0);
+    r.h1 = slab_t(fmaf(b.z, inv.x, -oinv.x), fmaf(c.y, inv.x, -oinv.x), fmaf(b.w, inv.y, -oinv.y),
+                  fmaf(c.z, inv.y, -oinv.y), fmaf(c.x, inv.z, -oinv.z), fmaf(c.w, inv.z, -oinv.z), tcap, r.t1);
+    child_refs(__float_as_int(e.x), __float_as_uint(e.y), BvhFmt<float>::TU, r.c0, r.c1);
+#endif
+    return r;
+}
+
+// Triangle record k of the leaf that starts at unit `first`.
+template <class R> __device__ __forceinline__ const unsigned char *leaf_tri(const unsigned char *bvh, int first, int k) {
+    return bvh + static_cast<size_t>(first + k * BvhFmt<R>::TU) * BvhFmt<R>::U;
 }
 
 // BVH2 traversal state of one ray for the coroutine kernel (bvh_trace below is
@@ -581,24 +694,20 @@ template <class R> struct BvhTrav {
         return sp < SSTACK ? ss[sp * 128] : sl[sp - SSTACK];
     }
 
-    // Node / triangle bases are passed from the kernel parameters (constant
-    // bank) rather than read through a SceneView the register allocator may
-    // have spilled: that reload sat on every node fetch's dependency chain.
-    __device__ __forceinline__ bool step(const SceneView<R> &s) { return step(s.bvh, s.trt, s.nsph); }
-    __device__ __forceinline__ bool step(const BvhNodeD<R> *__restrict__ nodes, const TriT<R> *__restrict__ trt,
-                                         int nsph) {
+    // The BVH base is passed from the kernel parameters (constant bank) rather
+    // than read through a SceneView the register allocator may have spilled:
+    // that reload sat on every node fetch's dependency chain.
+    __device__ __forceinline__ bool step(const SceneView<R> &s) { return step(s.bvh, s.nsph); }
+    __device__ __forceinline__ bool step(const unsigned char *__restrict__ bvh, int nsph) {
         while (node >= 0 && node != DONE) {
-            const BvhNodeD<R> n = ld_node(nodes + node);
-            R t0, t1;
-            bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
-            bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
-            if (h0 && h1) {
-                bool near0 = t0 <= t1;
+            const NodeHit<R> n = visit_node<R>(bvh, node, inv, oinv, best);
+            if (n.h0 && n.h1) {
+                bool near0 = n.t0 <= n.t1;
                 push(near0 ? n.c1 : n.c0);
                 node = near0 ? n.c0 : n.c1;
-            } else if (h0) {
+            } else if (n.h0) {
                 node = n.c0;
-            } else if (h1) {
+            } else if (n.h1) {
                 node = n.c1;
             } else {
                 node = pop();
@@ -615,8 +724,8 @@ template <class R> struct BvhTrav {
         while (leaf < 0) {
             int code = ~leaf;
             int first = code >> 4, cnt = code & 15;
-            for (int k = first; k < first + cnt; ++k) {
-                const TriT<R> tr = ld_trit(trt + k);
+            for (int k = 0; k < cnt; ++k) {
+                const TriT<R> tr = ld_trit<R>(leaf_tri<R>(bvh, first, k));
                 R t;
                 if (!hit_tri_t(tr, o, d, t))
                     continue;
@@ -624,7 +733,7 @@ template <class R> struct BvhTrav {
                 if (t < best || (t == best && kk < key)) {
                     best = t;
                     key = kk;
-                    pos = k;
+                    pos = tr.pos;
                     if (any) {
                         node = DONE;
                         leaf = 0;
@@ -670,17 +779,14 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
     int leaf = 0;    // postponed leaf code (< 0) or 0
     for (;;) {
         while (node >= 0 && node != DONE) {
-            const BvhNodeD<R> n = ld_node(s.bvh + node);
-            R t0, t1;
-            bool h0 = slab(n.lo0, n.hi0, oinv, inv, best, t0);
-            bool h1 = slab(n.lo1, n.hi1, oinv, inv, best, t1);
-            if (h0 && h1) {
-                bool near0 = t0 <= t1;
+            const NodeHit<R> n = visit_node<R>(s.bvh, node, inv, oinv, best);
+            if (n.h0 && n.h1) {
+                bool near0 = n.t0 <= n.t1;
                 stack[sp++] = near0 ? n.c1 : n.c0;
                 node = near0 ? n.c0 : n.c1;
-            } else if (h0) {
+            } else if (n.h0) {
                 node = n.c0;
-            } else if (h1) {
+            } else if (n.h1) {
                 node = n.c1;
             } else {
                 node = sp ? stack[--sp] : DONE;
@@ -697,8 +803,8 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
         while (leaf < 0) {
             int code = ~leaf;
             int first = code >> 4, cnt = code & 15;
-            for (int k = first; k < first + cnt; ++k) {
-                const TriT<R> tr = ld_trit(s.trt + k);
+            for (int k = 0; k < cnt; ++k) {
+                const TriT<R> tr = ld_trit<R>(leaf_tri<R>(s.bvh, first, k));
                 R t;
                 if (!hit_tri_t(tr, o, d, t))
                     continue;
@@ -706,7 +812,7 @@ __device__ int bvh_trace(const SceneView<R> &s, V3<R> o, V3<R> d, R lim, R &best
                 if (t < best || (t == best && kk < key)) {
                     best = t;
                     key = kk;
-                    pos = k;
+                    pos = tr.pos;
                     if (any_hit)
                         return pos;
                 }

@@ -786,7 +786,7 @@ k_step_co(StepParams<R> P, unsigned int *work) {
                 unsigned idle = __ballot_sync(0xffffffffu, !want && (have || !exhausted));
                 if (!busy || __popc(idle) >= P.refill)
                     break;
-                if (want && tv.step(P.scene.bvh, P.scene.trt, P.scene.nsph)) {
+                if (want && tv.step(P.scene.bvh, P.scene.nsph)) {
                     co.res_prim = tv.prim(S);
                     co.res_t = tv.best;
                     want = false;
@@ -866,7 +866,7 @@ k_trace_bench(StepParams<R> P, unsigned long long n, unsigned *work, unsigned lo
             unsigned idle = __ballot_sync(0xffffffffu, !want && !exhausted);
             if (!busy || __popc(idle) >= P.refill)
                 break;
-            if (want && tv.step(P.scene.bvh, P.scene.trt, P.scene.nsph)) {
+            if (want && tv.step(P.scene.bvh, P.scene.nsph)) {
                 h += tv.pos >= 0 ? 1u : 0u;
                 want = false;
             }
