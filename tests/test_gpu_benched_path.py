@@ -1,5 +1,7 @@
 """Parity of the benched path itself: the kernel behind
-bench.py's c4/c5 lines is k_step_co<float, Philox, BVH> with pooled
+bench.py's c4/c5 lines is the wavefront step (k_wf_logic<float, Philox> +
+k_wf_trace<float>: the coroutine StepCo advanced between BVH trace rounds;
+round 1 / early round 2: the fused coroutine kernel k_step_co) with pooled
 RA-quadtree lens adaptation on the 2^20 + 20 triangle clustered room.
 
   (i)   f64 at full scene size: the same kernel family (coroutine step, BVH,
@@ -55,14 +57,15 @@ def full_scene_oracle(big_scene, oracle_lib):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("launch", ["coop", "per_step"])
+@pytest.mark.parametrize("launch", ["coop", "per_step", "wavefront"])
 def test_f64_full_scene_bvh_matches_linear_scan_oracle(launch, big_scene, full_scene_oracle, monkeypatch):
-    """per_step = the benched launch structure (one k_step_co launch per lockstep
-    step + k_adapt_pool_accum / k_adapt_pool_apply), coop = the whole span in one
-    cooperative launch (small chain counts)."""
+    """wavefront = the benched launch structure (k_wf_logic / k_wf_trace rounds per
+    lockstep step + k_adapt_pool_accum / k_adapt_pool_apply), per_step = one fused
+    k_step_co launch per lockstep step, coop = the whole span in one cooperative
+    launch (small chain counts)."""
     o = full_scene_oracle
-    monkeypatch.setenv("RAMLT_STEP_KERNEL", "co")   # the benched kernel family (default with a BVH)
-    if launch == "per_step":
+    monkeypatch.setenv("RAMLT_STEP_KERNEL", "wf" if launch == "wavefront" else "co")
+    if launch != "coop":
         monkeypatch.setenv("RAMLT_COOP", "0")
     eng = _engine(big_scene, **FULL, precision="f64", rng="philox", adapt_mode="pooled", accel="bvh",
                   log_steps=K_FULL, dump_partition=True)
@@ -87,10 +90,13 @@ def test_f64_full_scene_bvh_matches_linear_scan_oracle(launch, big_scene, full_s
     eng.close()
 
 
+@pytest.mark.parametrize("kernel", ["wf", "co"])
 @pytest.mark.parametrize("strategy,rng", [("fixed", "pcg32"), ("fixed", "philox"), ("ra-quadtree", "philox")])
-def test_f32_bvh_equals_f32_brute_force(strategy, rng, monkeypatch):
+def test_f32_bvh_equals_f32_brute_force(strategy, rng, kernel, monkeypatch):
+    """kernel = the BVH run's step (wf: wavefront rounds, the benched default; co: the
+    fused coroutine kernel); the brute-force run always steps with the coroutine kernel."""
     from paper_2402_08273_b200 import scenes
-    monkeypatch.setenv("RAMLT_STEP_KERNEL", "co")
+    monkeypatch.setenv("RAMLT_STEP_KERNEL", kernel)
     monkeypatch.setenv("RAMLT_INIT_KERNEL", "co")
     monkeypatch.setenv("RAMLT_COOP", "0")
     scene = scenes.cluster_room(n_tris=2000, clusters=8, seed=3)
