@@ -47,6 +47,16 @@ WORKLOADS = {
 C2 = dict(chains=65536, steps=4096, dim=8, n_comp=4, target_seed=0, strategy="global",
           desc="C2 analytic target: 4 anisotropic Gaussians in [0,1]^8, 65,536 chains x 4,096 steps, "
                "Global (scalar lambda) pooled adaptation")
+
+
+def m_refine_for(chains: int) -> int:
+    """The paper's M_refine = 10^7 global mutations (core/driver.hpp:30), rounded to the
+    nearest multiple of the chain count so that every span is a whole number of lockstep
+    steps and every chain takes the same number of steps (SURVEY.md §8 C1 rule; the raw
+    10^7 splits each span of 8,388,608 chains into a full and a 19 % lockstep step)."""
+    return max(1, round(10_000_000 / chains)) * chains
+
+
 METRIC = "MLT mutations/sec"
 UNIT = "mutations/s"
 
@@ -229,7 +239,7 @@ def run_ours(args, wl, scene_text):
                        mutations=C * wl["steps_per_chain"], width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=1,
                        precision="f32", rng="philox", device=local, profile_kernels=True,
-                       metrics_interval=C * wl["steps_per_chain"])
+                       metrics_interval=C * wl["steps_per_chain"], m_refine=m_refine_for(C))
     # one process per GPU: chains shard by global id; pooled adaptation exchanged
     # every lockstep step, quadtree visits at every refine barrier, the film every
     # 2^12 lockstep steps (configs[4]) -- distributed.ShardedRender
@@ -339,7 +349,7 @@ def run_e2e(args, wl):
                        mutations=Cn * steps, width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=2,
                        precision="f32", rng="philox", device=0,
-                       metrics_interval=Cn * steps)
+                       metrics_interval=Cn * steps, m_refine=m_refine_for(Cn))
     text = wl["scene_text"].encode()
     img = np.zeros((wl["height"], wl["width"], 3), np.float32)
     torch.cuda.synchronize()
@@ -373,7 +383,7 @@ def run_e2e_sharded(args, wl):
     cfg = RenderConfig(strategy=wl["strategy"], perturbation=wl["perturbation"], chains=Cn,
                        mutations=Cn * steps, width=wl["width"], height=wl["height"],
                        max_vertices=wl["max_vertices"], b_samples=1_000_000, seed=2,
-                       precision="f32", rng="philox", metrics_interval=Cn * steps)
+                       precision="f32", rng="philox", metrics_interval=Cn * steps, m_refine=m_refine_for(Cn))
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -552,7 +562,9 @@ def main():
               "step": "one lockstep mutation of every chain",
               "l2": "inputs larger than the 126 MB L2, no flush (chain path SoA: c3 134 MB, c4 400 MB, "
                     "c5 3.2 GB; c4/c5 BVH + triangles ~120 MB)",
-              "rng": "philox4x32-10", "adaptation": "pooled" if wl["chains"] > 4096 else "literal"}
+              "rng": "philox4x32-10", "adaptation": "pooled" if wl["chains"] > 4096 else "literal",
+              "m_refine": m_refine_for(wl["chains"]),
+              "m_refine_note": "the multiple of the chain count nearest the paper's 10^7 (whole lockstep steps per span)"}
 
     if args.impl == "reference":
         if rank != 0:

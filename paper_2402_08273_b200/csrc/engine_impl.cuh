@@ -205,11 +205,14 @@ private:
     bool use_wf_ = false;
     int wf_refill_ = 8;       // k_wf_trace: RAMLT_WF_REFILL idle lanes end a traversal round
     int wf_check_ = 4;        // rounds between host checks of the queue length (RAMLT_WF_CHECK)
+    bool wf_poll_ = false;    // RAMLT_WF_POLL=1: poll the queue length every wf_check_ rounds even for one-step launches
     DBuf<uint4> wf_state_;
     DBuf<rd::GV<R>> wf_pv_;
-    DBuf<rd::WfRay<R>> wf_rays_[2];
-    DBuf<rd::WfHit<R>> wf_hits_[2];
-    DBuf<unsigned> wf_cnt_;   // queue lengths [2], trace work counter
+    DBuf<rd::WfRay<R>> wf_rays_;   // one round's rays: up to max_vertices - 1 per chain (a visibility batch)
+    DBuf<rd::WfHit<R>> wf_hits_;   // closest-hit answers by chain
+    DBuf<unsigned> wf_occ_;        // visibility-batch answers by chain (bit k: ray k occluded)
+    DBuf<int> wf_cq_[2];           // chain queues (ping-pong)
+    DBuf<unsigned> wf_cnt_;        // chain-queue lengths [0,1], trace work counter [2], ray-queue lengths [3,4]
     unsigned *wf_host_ = nullptr;   // pinned: queue length read back every wf_check_ rounds
     uint64_t wf_rounds_ = 0;
     // film
@@ -450,8 +453,13 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         steal_ = std::string(v) == "co_static" ? 0 : 1;
         use_wf_ = use_bvh_ && std::string(v) == "wf";
     }
+    // ray records carry (chain, batch ordinal) in 27 + 5 bits
+    if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
+        use_wf_ = false;
     if (const char *v = std::getenv("RAMLT_WF_REFILL"))
         wf_refill_ = std::min(32, std::max(1, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_WF_POLL"))
+        wf_poll_ = std::string(v) == "1";
     if (const char *v = std::getenv("RAMLT_WF_CHECK"))
         wf_check_ = std::min(64, std::max(1, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_CO_PV"))
@@ -1018,21 +1026,28 @@ template <int RK>
 void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     const size_t C = static_cast<size_t>(C_);
     constexpr int K = rd::Chunks<rd::WfState<R, RK>>::K;
+    const size_t per_chain = static_cast<size_t>(std::max<int>(1, static_cast<int>(d_.max_vertices) - 1));
     if (wf_state_.n < K * C) {
         wf_state_.alloc(K * C);
         wf_pv_.alloc(static_cast<size_t>(d_.max_vertices) * C);
-        for (int q = 0; q < 2; ++q) {
-            wf_rays_[q].alloc(C);
-            wf_hits_[q].alloc(C);
-        }
-        wf_cnt_.alloc(4);
+        wf_rays_.alloc(C * per_chain);
+        wf_hits_.alloc(C);
+        wf_occ_.alloc(C);
+        for (int q = 0; q < 2; ++q)
+            wf_cq_[q].alloc(C);
+        wf_cnt_.alloc(8);
         if (!wf_host_)
             RAMLT_CUDA(cudaMallocHost(&wf_host_, sizeof(unsigned)));
     }
     auto logic = rd::k_wf_logic<R, RK>;
     auto trace = rd::k_wf_trace<R>;
-    const size_t lsmem = smem_;
+    size_t lsmem = smem_;
     size_t tsmem = (smem_ + 15) & ~size_t(15);
+    rd::StepParams<R> PL = P;   // k_wf_logic's parameters: co_stack_off = its shared-memory coroutine states
+#if RAMLT_WF_SMEM
+    PL.co_stack_off = static_cast<unsigned>(tsmem);
+    lsmem = tsmem + static_cast<size_t>(128) * sizeof(rd::WfState<R, RK>);
+#endif
     P.co_stack_off = static_cast<unsigned>(tsmem);
     tsmem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
     const int lper = prepare(reinterpret_cast<const void *>(logic), lsmem);
@@ -1041,7 +1056,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
                                                 static_cast<unsigned>(std::max(lper, 1) * sms_));
     const unsigned tblocks = static_cast<unsigned>(std::max(tper, 1) * sms_);
     unsigned *cnt = wf_cnt_.p;
-    RAMLT_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned), stream_));
+    RAMLT_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (d_.profile_kernels) {
         if (ev_.size() + ev_trace_.size() >= 4096)
@@ -1052,23 +1067,30 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     }
     rd::WfParams<R> W;
     W.trace_work = cnt + 2;
+    W.rays = wf_rays_.p;
+    W.hits = wf_hits_.p;
+    W.occ = wf_occ_.p;
     W.state = wf_state_.p;
     W.pv = wf_pv_.p;
+    const bool poll = P.j1 - P.j0 > 1 || wf_poll_;
+    const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2;
     for (int r = 0;; ++r) {
         const int a = r & 1;
-        W.rays_in = wf_rays_[a ^ 1].p;
-        W.hits_in = wf_hits_[a ^ 1].p;
+        W.cq_in = wf_cq_[a ^ 1].p;
         W.n_in = cnt + (a ^ 1);
-        W.rays_out = wf_rays_[a].p;
+        W.cq_out = wf_cq_[a].p;
         W.n_out = cnt + a;
-        logic<<<lblocks, 128, lsmem, stream_>>>(P, W, r == 0 ? 1 : 0);
+        W.n_rays = cnt + 3 + a;
+        logic<<<lblocks, 128, lsmem, stream_>>>(PL, W, r == 0 ? 1 : 0);
         cudaEvent_t t0 = nullptr, t1 = nullptr;
         if (d_.profile_kernels) {
             RAMLT_CUDA(cudaEventCreate(&t0));
             RAMLT_CUDA(cudaEventCreate(&t1));
             RAMLT_CUDA(cudaEventRecord(t0, stream_));
         }
-        trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_[a].p, wf_hits_[a].p, cnt + a, cnt + 2, cnt + (a ^ 1));
+        // traces this round's rays; zeroes the counters the next round's logic appends to
+        trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 3 + a, cnt + 2,
+                                                 cnt + (a ^ 1), cnt + 3 + (a ^ 1));
         if (d_.profile_kernels) {
             RAMLT_CUDA(cudaEventRecord(t1, stream_));
             ev_trace_.emplace_back(t0, t1);
@@ -1076,7 +1098,14 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         launches_ += 2;
         ++wf_rounds_;
         RAMLT_CUDA(cudaGetLastError());
-        if (r % wf_check_ == wf_check_ - 1) {
+        // A mutation yields at most max_vertices + 1 times (max_vertices - 1 closest-hit
+        // rays, the eval_contribution batch, the eye_path_density batch), so a
+        // one-step launch needs max_vertices + 2 logic rounds: they are enqueued
+        // without a host round trip and the queue length is read back once, after
+        // the last (a nonzero length -- never seen -- just continues the loop).
+        // Multi-step launches (Fixed strategy) poll every wf_check_ rounds instead.
+        const bool last_planned = !poll && r + 1 >= planned;
+        if (last_planned || (poll && r % wf_check_ == wf_check_ - 1)) {
             RAMLT_CUDA(cudaMemcpyAsync(wf_host_, cnt + a, sizeof(unsigned), cudaMemcpyDeviceToHost, stream_));
             RAMLT_CUDA(cudaStreamSynchronize(stream_));
             if (*wf_host_ == 0)

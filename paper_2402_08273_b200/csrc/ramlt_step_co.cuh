@@ -123,12 +123,30 @@ template <class R> struct PropS {
 
 enum { CO_RAY_PENDING = 1, CO_STEP_DONE = 2 };
 
+// Where a coroutine's rays go.  NoSink: one pending ray at a time in `ray`, traced by
+// the caller (k_step_co).  A batching sink (ramlt_wavefront.cuh, BATCH = true) takes
+// the rays itself -- reserve(n) slots, put(slot, o, d, lim, k) -- so the independent
+// visibility rays of eval_contribution / eye_path_density leave in ONE yield
+// (ordinal k, answered by occluded(k)) instead of one yield per segment.
+struct NoSink {
+    static constexpr bool BATCH = false;
+    // never called (BATCH is false); present so both arms of `if (Sink::BATCH)` compile
+    // -- a case label may not sit inside an `if constexpr` block
+    __device__ __forceinline__ unsigned reserve(unsigned) const { return 0u; }
+    template <class V, class T> __device__ __forceinline__ void put(unsigned, V, V, T, int) const {}
+    __device__ __forceinline__ void null(unsigned) const {}
+    __device__ __forceinline__ void begin_batch() const {}
+    __device__ __forceinline__ bool occluded(int) const { return false; }
+};
+
 #define CO_RAY(O, D, LIM, N)                                                                       \
     do {                                                                                           \
         ray.o = (O);                                                                               \
         ray.d = (D);                                                                               \
         ray.lim = (LIM);                                                                           \
         pc = (N);                                                                                  \
+        if constexpr (Sink::BATCH)                                                                 \
+            sink.put(sink.reserve(1u), ray.o, ray.d, ray.lim, 0);                                  \
         return CO_RAY_PENDING;                                                                     \
     case (N):;                                                                                     \
     } while (0)
@@ -172,8 +190,81 @@ template <class R, int RK, bool INIT = false> struct StepCo {
     int ek, ei;
     unsigned attempts;             // INIT (init_attempts < 2^32)
 
+    template <class Sink = NoSink>
     __device__ __forceinline__ int advance(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
-                                           RayCount &rc, unsigned long long index);
+                                           RayCount &rc, unsigned long long index, Sink sink = Sink{});
+
+    // Batching sinks: every visibility ray eval_contribution can ask for (segments
+    // 0..endpoint of a perturbation, all segments of a large step), in segment order;
+    // stops at the first segment whose geometry ends the evaluation.  Returns the
+    // slots reserved (unused ones are null rays).
+    template <class Sink>
+    __device__ __forceinline__ int emit_eval_rays(const CurPathV<R> &cur, const PvSmem<R> &pv, Sink &sink) const {
+        const int nseg = ek - 1;
+        const int nmax = choose ? min(nseg, endpoint + 1) : nseg;
+        if (nmax <= 0)
+            return 0;
+        const unsigned base = sink.reserve(static_cast<unsigned>(nmax));
+        sink.begin_batch();
+        PropS<R> prop{pv, head_end, &cur};
+        int nb = 0;
+        for (int e = 0; e < nmax; ++e) {
+            Vx<R> av = prop.get(e);
+            Vx<R> bv = prop.get(e + 1);
+            if (e > 0 && av.emi >= 0)
+                break;
+            V3<R> dd = sub(bv.p, av.p);
+            R d2 = dot(dd, dd);
+            if (d2 <= R(0))
+                break;
+            V3<R> dir = dvs(dd, M<R>::sqrt(d2));
+            R sg = av.spec ? M<R>::abs(dot(bv.n, dir)) / d2
+                           : M<R>::abs(dot(av.n, dir)) * M<R>::abs(dot(bv.n, dir)) / d2;
+            if (sg <= R(0))
+                break;
+            R dist = len(dd);
+            if (dist <= R(2) * R(kEpsD))
+                break;
+            sink.put(base + static_cast<unsigned>(nb), av.p, dvs(dd, dist), dist - R(kEpsD), nb);
+            ++nb;
+        }
+        for (int q = nb; q < nmax; ++q)
+            sink.null(base + static_cast<unsigned>(q));
+        return nmax;
+    }
+    // The visibility rays of eye_path_density(current path), in segment order.
+    template <class Sink>
+    __device__ __forceinline__ int emit_eyeden_rays(const CurPathV<R> &cur, Sink &sink) const {
+        const int nseg = cs.k - 1;
+        if (nseg <= 0)
+            return 0;
+        const unsigned base = sink.reserve(static_cast<unsigned>(nseg));
+        sink.begin_batch();
+        int nb = 0;
+        for (int e = 0; e < nseg; ++e) {
+            Vx<R> av = cur.get(e);
+            Vx<R> bv = cur.get(e + 1);
+            if (e > 0 && av.emi >= 0)
+                break;
+            V3<R> dd = sub(bv.p, av.p);
+            R d2 = dot(dd, dd);
+            R cval = R(0);
+            if (d2 > R(0)) {
+                V3<R> dir = dvs(dd, M<R>::sqrt(d2));
+                cval = M<R>::abs(dot(bv.n, dir)) / d2;
+            }
+            if (cval <= R(0))
+                break;
+            R dist = len(dd);
+            if (dist <= R(2) * R(kEpsD))
+                break;
+            sink.put(base + static_cast<unsigned>(nb), av.p, dvs(dd, dist), dist - R(kEpsD), nb);
+            ++nb;
+        }
+        for (int q = nb; q < nseg; ++q)
+            sink.null(base + static_cast<unsigned>(q));
+        return nseg;
+    }
 
     // INIT: write the found path (vertices 1..kp-1, contribution) and the
     // chain's fresh counters and step stream -- what init_chain stores.
@@ -205,9 +296,10 @@ template <class R, int RK, bool INIT = false> struct StepCo {
 };
 
 template <class R, int RK, bool INIT>
+template <class Sink>
 __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> &P, const SceneView<R> &S,
                                                       const PvSmem<R> &pv, RayCount &rc,
-                                                      unsigned long long index) {
+                                                      unsigned long long index, Sink sink) {
     CurPathV<R> cur{P.ch.verts, P.C, c, S.cam.pos, S.cam.fwd};
     switch (pc) {
     case 0: {
@@ -407,6 +499,14 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
             R imp = cam_importance(S.cam, w0);
             ef = mk(imp, imp, imp);
         }
+        if (Sink::BATCH) {   // all the segments' visibility rays in one yield
+            if (emit_eval_rays(cur, pv, sink) > 0) {
+                pc = 5;
+                return CO_RAY_PENDING;
+            }
+        case 5:
+            i = 0;   // ordinal of the next answer
+        }
         for (ei = 0; ei + 1 < ek; ++ei) {
             {
                 PropS<R> prop{pv, head_end, &cur};
@@ -437,9 +537,14 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
                 d = dvs(dd, dist);
                 ray.lim = dist - R(kEpsD);
             }
-            CO_RAY(o, d, ray.lim, 3);
-            if (res_prim >= 0)
-                goto eval_fail;
+            if (Sink::BATCH) {
+                if (sink.occluded(i++))
+                    goto eval_fail;
+            } else {
+                CO_RAY(o, d, ray.lim, 3);
+                if (res_prim >= 0)
+                    goto eval_fail;
+            }
         eval_seg_visible:
             {
                 ef = scl(ef, eseg);
@@ -516,6 +621,14 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
                 goto ed_done;
             ep = static_cast<double>(p0);
         }
+        if (Sink::BATCH) {
+            if (emit_eyeden_rays(cur, sink) > 0) {
+                pc = 6;
+                return CO_RAY_PENDING;
+            }
+        case 6:
+            i = 0;
+        }
         for (ei = 0; ei + 1 < cs.k; ++ei) {
             {
                 Vx<R> av = cur.get(ei);
@@ -561,9 +674,14 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
                 goto ed_apply;
             }
         ed_ray:
-            CO_RAY(o, d, ef.y, 4);
-            if (res_prim >= 0)
-                ef.x = R(0);
+            if (Sink::BATCH) {
+                if (sink.occluded(i++))
+                    ef.x = R(0);
+            } else {
+                CO_RAY(o, d, ef.y, 4);
+                if (res_prim >= 0)
+                    ef.x = R(0);
+            }
         ed_apply:
             if (ei == 0)
                 ep *= static_cast<double>(ef.x);          // p *= area_conversion(path[0], path[1])

@@ -4,12 +4,19 @@
 // (ramlt_step_co.cuh).  Instead of tracing inside the coroutine kernel, a
 // lockstep step alternates two kernels until no chain has a ray pending:
 //
-//   k_wf_logic  one thread per chain with a pending ray (compacted queue):
-//               resume the coroutine with its hit, advance it to its next ray
-//               cast (or the end of its step), append the ray to the next
-//               queue with a warp-aggregated atomic;
+//   k_wf_logic  one thread per chain that yielded (compacted chain queue):
+//               resume the coroutine with its answer, advance it to its next
+//               yield (or the end of its step); its rays go into the round's
+//               ray queue and the chain into the next chain queue, both with
+//               warp-aggregated atomics.  A yield is one closest-hit ray
+//               (retrace, large-step bounce) or ALL the visibility rays of
+//               eval_contribution / eye_path_density at once (they do not
+//               depend on each other), so a mutation takes ~closest-hit rays
+//               + 2 rounds instead of one round per ray;
 //   k_wf_trace  persistent, one ray per lane, dynamic ray fetch and
-//               while-while BVH rounds over the queue, writing (t, prim).
+//               while-while BVH rounds over the queue, writing (t, prim) by
+//               chain for closest hits and OR-ing bit k of the chain's
+//               occlusion mask for an occluded visibility ray k.
 //
 // Between rounds the coroutine state lives in HBM as 16-byte chunks indexed
 // [chunk][chain] (coalesced vectorised loads/stores); the proposal vertices
@@ -24,11 +31,14 @@
 
 namespace rd {
 
-// Pending ray of chain c: 32 B in fp32 (one sector).
+// Pending ray: 32 B in fp32 (one sector).  `ck` = chain | ordinal << 27: ordinal 0
+// for a closest-hit ray (answer in hits[chain]); ordinal k of a visibility batch
+// sets bit k of occ[chain] when occluded.  lim <= 0 marks an unused slot.
+constexpr int kWfChainBits = 27;
 template <class R> struct alignas(sizeof(R) * 8) WfRay {
     R o[3], lim;
     R d[3];
-    int c;
+    int ck;
 };
 template <class R> struct alignas(sizeof(R) * 2) WfHit {
     R t;
@@ -42,34 +52,131 @@ template <class R, int RK> struct WfState {
 };
 
 template <class R> struct WfParams {
-    const WfRay<R> *rays_in;   // previous round's queue (round > 0)
-    const WfHit<R> *hits_in;
+    const int *cq_in;          // chains resumed this round (round > 0)
     const unsigned *n_in;
-    WfRay<R> *rays_out;        // this round's queue
+    int *cq_out;               // chains that yielded this round
     unsigned *n_out;
+    WfRay<R> *rays;            // this round's ray queue
+    unsigned *n_rays;
     unsigned *trace_work;      // zeroed here for the following k_wf_trace
+    const WfHit<R> *hits;      // closest-hit answers, by chain
+    unsigned *occ;             // visibility-batch answers, by chain (bit k = ray k occluded)
     uint4 *state;              // WfState as 16 B chunks: chunk k of chain c at state[k * C + c]
     GV<R> *pv;                 // proposal vertices, vertex i of chain c at pv[i * C + c]
 };
 
+// The coroutine's rays go straight into the round's ray queue (StepCo::advance, BATCH).
+template <class R> struct WfSink {
+    static constexpr bool BATCH = true;
+    WfRay<R> *rays;
+    unsigned *n_rays;
+    unsigned *occ_g;
+    int c;
+    unsigned occ;   // answers of the batch this chain is resumed from
+    // n slots per calling lane: one atomic for the lanes converged here
+    __device__ __forceinline__ unsigned reserve(unsigned n) const {
+        const unsigned act = __activemask();
+        const unsigned lane = threadIdx.x & 31;
+        const unsigned lt = (1u << lane) - 1u;
+        unsigned pre = 0, tot = 0;
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {   // n < 32
+            const unsigned mb = __ballot_sync(act, (n >> b) & 1u);
+            pre += static_cast<unsigned>(__popc(mb & lt)) << b;
+            tot += static_cast<unsigned>(__popc(mb)) << b;
+        }
+        const int leader = __ffs(act) - 1;
+        unsigned base = 0;
+        if (static_cast<int>(lane) == leader)
+            base = atomicAdd(n_rays, tot);
+        base = __shfl_sync(act, base, leader);
+        return base + pre;
+    }
+    __device__ __forceinline__ void put(unsigned slot, V3<R> o, V3<R> d, R lim, int k) const {
+        WfRay<R> r;
+        r.o[0] = o.x, r.o[1] = o.y, r.o[2] = o.z;
+        r.lim = lim;
+        r.d[0] = d.x, r.d[1] = d.y, r.d[2] = d.z;
+        r.ck = c | (k << kWfChainBits);
+        rays[slot] = r;
+    }
+    __device__ __forceinline__ void null(unsigned slot) const {
+        WfRay<R> r;
+        r.o[0] = r.o[1] = r.o[2] = r.lim = R(0);
+        r.d[0] = R(1), r.d[1] = r.d[2] = R(0);
+        r.ck = c;
+        rays[slot] = r;
+    }
+    __device__ __forceinline__ void begin_batch() const { occ_g[c] = 0u; }
+    __device__ __forceinline__ bool occluded(int k) const { return (occ >> k) & 1u; }
+};
+
+// State chunks are whole 32 B sectors moved with 256-bit evict-first loads / stores
+// (LDG/STG.E.EF.ENL2.256): a chain's chunk never shares a sector with its neighbour's,
+// so a queue that no longer holds consecutive chains costs no half-used sectors.
+// RAMLT_WF_CHUNK32=0: 16 B chunks (the first wavefront build), kept for A/B runs.
+#ifndef RAMLT_WF_CHUNK32
+#define RAMLT_WF_CHUNK32 1
+#endif
+// RAMLT_WF_SMEM=1: the resumed coroutine lives in shared memory (one WfState per
+// thread) instead of the thread's local memory.
+#ifndef RAMLT_WF_SMEM
+#define RAMLT_WF_SMEM 0
+#endif
+struct __align__(32) Sector {
+    unsigned w[8];
+};
+__device__ __forceinline__ Sector ld_sector_cs(const void *p) {
+    Sector r;
+    asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                   "=r"(r.w[6]), "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_sector_cs(void *p, const Sector &r) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.w[0]), "r"(r.w[1]),
+                 "r"(r.w[2]), "r"(r.w[3]), "r"(r.w[4]), "r"(r.w[5]), "r"(r.w[6]), "r"(r.w[7])
+                 : "memory");
+}
+
 template <class T> struct Chunks {
+#if RAMLT_WF_CHUNK32
+    static constexpr int K = 2 * static_cast<int>((sizeof(T) + 31) / 32);   // in uint4 units
+    Sector w[K / 2];
+#else
     static constexpr int K = static_cast<int>((sizeof(T) + 15) / 16);
     uint4 w[K];
+#endif
 };
 
 template <class T> __device__ __forceinline__ void ld_state(T &v, const uint4 *__restrict__ base, size_t C, int c) {
     Chunks<T> b;
+#if RAMLT_WF_CHUNK32
+    const Sector *p = reinterpret_cast<const Sector *>(base);
+#pragma unroll
+    for (int k = 0; k < Chunks<T>::K / 2; ++k)
+        b.w[k] = ld_sector_cs(p + static_cast<size_t>(k) * C + c);
+#else
 #pragma unroll
     for (int k = 0; k < Chunks<T>::K; ++k)
         b.w[k] = __ldcs(base + static_cast<size_t>(k) * C + c);
+#endif
     memcpy(&v, &b, sizeof(T));
 }
 template <class T> __device__ __forceinline__ void st_state(const T &v, uint4 *__restrict__ base, size_t C, int c) {
     Chunks<T> b;
     memcpy(&b, &v, sizeof(T));
+#if RAMLT_WF_CHUNK32
+    Sector *p = reinterpret_cast<Sector *>(base);
+#pragma unroll
+    for (int k = 0; k < Chunks<T>::K / 2; ++k)
+        st_sector_cs(p + static_cast<size_t>(k) * C + c, b.w[k]);
+#else
 #pragma unroll
     for (int k = 0; k < Chunks<T>::K; ++k)
         __stcs(base + static_cast<size_t>(k) * C + c, b.w[k]);
+#endif
 }
 
 template <class R, int RK>
@@ -82,7 +189,12 @@ __global__ void __launch_bounds__(128) k_wf_logic(StepParams<R> P, WfParams<R> W
     RayCount rc;
     const unsigned stride = gridDim.x * blockDim.x;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+#if RAMLT_WF_SMEM
+        WfState<R, RK> &s = reinterpret_cast<WfState<R, RK> *>(smem + P.co_stack_off)[threadIdx.x];
+#else
         WfState<R, RK> s;
+#endif
+        WfSink<R> sink{W.rays, W.n_rays, W.occ, 0, 0u};
         int c;
         if (round0) {
             c = static_cast<int>(i);
@@ -97,30 +209,26 @@ __global__ void __launch_bounds__(128) k_wf_logic(StepParams<R> P, WfParams<R> W
                 continue;
             }
         } else {
-            c = W.rays_in[i].c;
+            c = W.cq_in[i];
             ld_state(s, W.state, static_cast<size_t>(P.C), c);
-            const WfHit<R> h = W.hits_in[i];
+            const WfHit<R> h = W.hits[c];
             s.co.res_prim = h.prim;
             s.co.res_t = h.t;
+            sink.occ = W.occ[c];
         }
+        sink.c = c;
         const PvSmem<R> pv{W.pv + c, P.C};
         for (;;) {
             const unsigned long long index =
                 P.span_start + static_cast<unsigned long long>(s.j) * P.C_total + P.chain_off + c;
-            if (s.co.advance(P, S, pv, rc, index) == CO_RAY_PENDING) {
+            if (s.co.advance(P, S, pv, rc, index, sink) == CO_RAY_PENDING) {
                 const unsigned act = __activemask();
                 const int leader = __ffs(act) - 1;
                 unsigned base = 0;
                 if (static_cast<int>(threadIdx.x & 31) == leader)
                     base = atomicAdd(W.n_out, static_cast<unsigned>(__popc(act)));
                 base = __shfl_sync(act, base, leader);
-                const unsigned slot = base + __popc(act & ((1u << (threadIdx.x & 31)) - 1u));
-                WfRay<R> r;
-                r.o[0] = s.co.ray.o.x, r.o[1] = s.co.ray.o.y, r.o[2] = s.co.ray.o.z;
-                r.lim = s.co.ray.lim;
-                r.d[0] = s.co.ray.d.x, r.d[1] = s.co.ray.d.y, r.d[2] = s.co.ray.d.z;
-                r.c = c;
-                W.rays_out[slot] = r;
+                W.cq_out[base + __popc(act & ((1u << (threadIdx.x & 31)) - 1u))] = c;
                 st_state(s, W.state, static_cast<size_t>(P.C), c);
                 break;
             }
@@ -145,7 +253,7 @@ template <> __device__ __forceinline__ WfRay<float> ld_ray<float>(const WfRay<fl
     ldg256(p, a, b);
     WfRay<float> r;
     r.o[0] = a.x, r.o[1] = a.y, r.o[2] = a.z, r.lim = a.w;
-    r.d[0] = b.x, r.d[1] = b.y, r.d[2] = b.z, r.c = __float_as_int(b.w);
+    r.d[0] = b.x, r.d[1] = b.y, r.d[2] = b.z, r.ck = __float_as_int(b.w);
     return r;
 }
 
@@ -155,16 +263,18 @@ template <> __device__ __forceinline__ WfRay<float> ld_ray<float>(const WfRay<fl
 #define RAMLT_WF_MINBLOCKS 8
 #endif
 // Persistent closest-hit / any-hit tracer over the queue (the while-while
-// rounds and refill rule of k_trace_bench).  `zero_next` is the counter the
-// next round's k_wf_logic appends to.
+// rounds and refill rule of k_trace_bench).  `zero_a`, `zero_b` are the
+// counters the next round's k_wf_logic appends to.
 template <class R>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? RAMLT_WF_MINBLOCKS : 1)
 k_wf_trace(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restrict__ hits,
-           const unsigned *n_ptr, unsigned *work, unsigned *zero_next) {
+           unsigned *__restrict__ occ, const unsigned *n_ptr, unsigned *work, unsigned *zero_a, unsigned *zero_b) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-        *zero_next = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *zero_a = 0;
+        *zero_b = 0;
+    }
     const unsigned n = *n_ptr;
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -172,8 +282,8 @@ k_wf_trace(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restr
     int tv_sl[BvhTrav<R>::STACK - BvhTrav<R>::SSTACK];
     tv.sl = tv_sl;
     tv.ss = reinterpret_cast<int *>(smem + P.co_stack_off) + threadIdx.x;
-    bool want = false, exhausted = n == 0;
-    unsigned cur = 0;
+    bool want = false, exhausted = n == 0, any = false;
+    int ck = 0;
     for (;;) {
         const unsigned need = __ballot_sync(0xffffffffu, !want && !exhausted);
         if (need) {
@@ -186,16 +296,18 @@ k_wf_trace(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restr
                 const unsigned mine = base + __popc(need & lt);
                 if (mine < n) {
                     const WfRay<R> r = ld_ray(rays + mine);
-                    tv.begin(S, mk(r.o[0], r.o[1], r.o[2]), mk(r.d[0], r.d[1], r.d[2]), r.lim,
-                             r.lim < M<R>::inf());
-                    cur = mine;
-                    want = true;
+                    if (r.lim > R(0)) {   // lim <= 0: unused slot of a batch
+                        any = r.lim < M<R>::inf();
+                        tv.begin(S, mk(r.o[0], r.o[1], r.o[2]), mk(r.d[0], r.d[1], r.d[2]), r.lim, any);
+                        ck = r.ck;
+                        want = true;
+                    }
                 } else {
                     exhausted = true;
                 }
             }
         }
-        if (!__any_sync(0xffffffffu, want))
+        if (!__any_sync(0xffffffffu, want || !exhausted))
             break;
         for (;;) {
             const unsigned busy = __ballot_sync(0xffffffffu, want);
@@ -203,10 +315,17 @@ k_wf_trace(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restr
             if (!busy || __popc(idle) >= P.refill)
                 break;
             if (want && tv.step(P.scene.bvh, P.scene.nsph)) {
-                WfHit<R> h;
-                h.t = tv.best;
-                h.prim = tv.prim(S);
-                hits[cur] = h;
+                const int prim = tv.prim(S);
+                const int c = ck & ((1 << kWfChainBits) - 1);
+                if (any) {
+                    if (prim >= 0)
+                        atomicOr(occ + c, 1u << (static_cast<unsigned>(ck) >> kWfChainBits));
+                } else {
+                    WfHit<R> h;
+                    h.t = tv.best;
+                    h.prim = prim;
+                    hits[c] = h;
+                }
                 want = false;
             }
         }

@@ -21,7 +21,8 @@ text = scenes.SCENES[c["scene"]]()
 C = c["chains"]
 eng = Engine(text, RenderConfig(strategy=c["strategy"], perturbation=c["pert"], chains=C, mutations=C * 4096,
              width=c["res"], height=c["res"], max_vertices=c["maxv"], b_samples=100000, precision="f32",
-             rng="philox", metrics_interval=C * 4096, lanes_per_chain=int(os.environ.get("LANES", "0"))))
+             rng="philox", metrics_interval=C * 4096,
+             m_refine=int(os.environ.get("M_REFINE", "0")) or max(1, round(1e7 / C)) * C, lanes_per_chain=int(os.environ.get("LANES", "0"))))
 s = torch.cuda.current_stream()
 eng.set_stream(s.cuda_stream)
 eng.estimate_b(); eng.init_chains()
