@@ -885,6 +885,9 @@ template <class R> void EngineT<R>::trace_benchmark(uint64_t n_rays, double *ms,
     size_t smem = (smem_ + 15) & ~size_t(15);
     P.co_stack_off = static_cast<unsigned>(smem);
     smem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
+    int cells = 0;   // RAMLT_TB_CELLS=n: rays in (origin cell of an n^3 grid, direction octant) order
+    if (const char *v = std::getenv("RAMLT_TB_CELLS"))
+        cells = std::max(0, std::atoi(v));
     auto kern = rd::k_trace_bench<R>;
     RAMLT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0, dev = 0, sms = 148;
@@ -899,7 +902,7 @@ template <class R> void EngineT<R>::trace_benchmark(uint64_t n_rays, double *ms,
     RAMLT_CUDA(cudaEventCreate(&e0));
     RAMLT_CUDA(cudaEventCreate(&e1));
     RAMLT_CUDA(cudaEventRecord(e0, stream_));
-    kern<<<static_cast<unsigned>(std::max(per_sm, 1) * sms), 128, smem, stream_>>>(P, n_rays, work_.p, h.p, l, e);
+    kern<<<static_cast<unsigned>(std::max(per_sm, 1) * sms), 128, smem, stream_>>>(P, n_rays, work_.p, h.p, l, e, cells);
     RAMLT_CUDA(cudaGetLastError());
     RAMLT_CUDA(cudaEventRecord(e1, stream_));
     RAMLT_CUDA(cudaEventSynchronize(e1));

@@ -942,7 +942,8 @@ __device__ __forceinline__ uint32_t tb_hash(uint32_t x) {
 // fetch with the same refill rule) on synthetic incoherent rays.
 template <class R>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? RAMLT_CO_MINBLOCKS : 1)
-k_trace_bench(StepParams<R> P, unsigned long long n, unsigned *work, unsigned long long *hits, V3<R> lo, V3<R> ext) {
+k_trace_bench(StepParams<R> P, unsigned long long n, unsigned *work, unsigned long long *hits, V3<R> lo, V3<R> ext,
+              int cells) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     const unsigned lane = threadIdx.x & 31;
@@ -970,7 +971,22 @@ k_trace_bench(StepParams<R> P, unsigned long long n, unsigned *work, unsigned lo
                     V3<R> o = mk(lo.x + ext.x * (R(a) * k), lo.y + ext.y * (R(b) * k), lo.z + ext.z * (R(c) * k));
                     R z = R(1) - R(2) * (R(e) * k), ph = R(kTwoPiD) * (R(f) * k);
                     R r = M<R>::sqrt(fmax(R(0), R(1) - z * z));
-                    tv.begin(S, o, mk(r * M<R>::cos(ph), r * M<R>::sin(ph), z), M<R>::inf(), false);
+                    V3<R> dir = mk(r * M<R>::cos(ph), r * M<R>::sin(ph), z);
+                    if (cells > 0) {
+                        // the same ray population in bucket order (origin cell, direction octant):
+                        // what a queue sorted by (cell, octant) would hand to neighbouring lanes
+                        const unsigned long long nb = static_cast<unsigned long long>(cells) * cells * cells * 8ull;
+                        const unsigned long long bkt = static_cast<unsigned long long>(mine) * nb / n;
+                        const unsigned cell = static_cast<unsigned>(bkt >> 3), oct = static_cast<unsigned>(bkt & 7u);
+                        const R inv = R(1) / R(cells);
+                        o = mk(lo.x + ext.x * (R(cell % cells) + R(a) * k) * inv,
+                               lo.y + ext.y * (R((cell / cells) % cells) + R(b) * k) * inv,
+                               lo.z + ext.z * (R(cell / (cells * cells)) + R(c) * k) * inv);
+                        dir = mk((oct & 1u) ? -M<R>::abs(dir.x) : M<R>::abs(dir.x),
+                                 (oct & 2u) ? -M<R>::abs(dir.y) : M<R>::abs(dir.y),
+                                 (oct & 4u) ? -M<R>::abs(dir.z) : M<R>::abs(dir.z));
+                    }
+                    tv.begin(S, o, dir, M<R>::inf(), false);
                     want = true;
                 } else {
                     exhausted = true;
