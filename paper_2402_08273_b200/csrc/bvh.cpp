@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <thread>
 
@@ -64,7 +65,6 @@ struct Builder {
                             // (tools/bvh_stats.cpp): 16 -> 32 bins -4 %, 32 -> 64 -6 %, 128 / 256 no further gain
     double sah_ct = 0.0;    // RAMLT_BVH_CT > 0: SAH leaf termination, node cost / triangle cost
     int depth = 0;
-    int par_depth = -1;                 // >= 0: defer subtrees starting at this depth
     std::vector<Task> *tasks = nullptr;
 
     Builder(Shared *s, int lm) : sh(s), tb(s->tb), cen(s->cen), idx(s->idx), leaf_max(lm) {
@@ -95,70 +95,169 @@ struct Builder {
 
     int32_t leaf(int s, int e) const { return ~((static_cast<int32_t>(s) << 4) | (e - s)); }
 
+    // min/max and counts are order-independent, so the loops over a large range are
+    // cut into per-thread pieces (top levels only: `par_threads` > 1) and merged --
+    // the tree does not depend on the thread count.
+    static constexpr int BMAX = 256;
+    static constexpr int kParMin = 1 << 14;
+    int par_threads = 1;
+    struct Bins {
+        Box bb[3][BMAX];    // valid where cnt > 0 (set on the first triangle of a bin)
+        int cnt[3][BMAX];
+        void reset(int B) {
+            for (int ax = 0; ax < 3; ++ax)
+                std::memset(cnt[ax], 0, static_cast<size_t>(B) * sizeof(int));
+        }
+        void add(int ax, int bi, const Box &bx) {
+            if (cnt[ax][bi]++ == 0)
+                bb[ax][bi] = bx;
+            else
+                bb[ax][bi].grow(bx);
+        }
+    };
+    template <class F> void pieces(int s, int e, F fn) const {   // fn(piece, ps, pe)
+        const int n = e - s;
+        const int T = n >= kParMin ? par_threads : 1;
+        if (T <= 1) {
+            fn(0, s, e);
+            return;
+        }
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t) {
+            const int ps = s + static_cast<int>(static_cast<long long>(n) * t / T);
+            const int pe = s + static_cast<int>(static_cast<long long>(n) * (t + 1) / T);
+            pool.emplace_back([=] { fn(t, ps, pe); });
+        }
+        for (auto &th : pool)
+            th.join();
+    }
+    int n_pieces(int s, int e) const { return e - s >= kParMin ? std::max(par_threads, 1) : 1; }
+
+    Box centroid_box(int s, int e) const {
+        std::vector<Box> part(static_cast<size_t>(n_pieces(s, e)));
+        pieces(s, e, [&](int t, int ps, int pe) {
+            Box cb;
+            cb.reset();
+            for (int i = ps; i < pe; ++i)
+                cb.grow(&cen[3 * idx[i]]);
+            part[static_cast<size_t>(t)] = cb;
+        });
+        Box cb = part[0];
+        for (size_t t = 1; t < part.size(); ++t)
+            cb.grow(part[t]);
+        return cb;
+    }
+
+    // The binned-SAH split of idx[s, e): one pass bins every triangle on all three
+    // axes; the children's bounds are the unions of the winning axis's bins (the
+    // same min/max as a scan of the two halves).  Returns false when no split exists.
+    bool find_split(int s, int e, const Box &cb, int &best_axis, int &best_bin, double &best_cost, Box &lbox,
+                    Box &rbox) const {
+        const int B = bins;
+        double ext[3], scale_lo[3];
+        bool use[3];
+        for (int ax = 0; ax < 3; ++ax) {
+            ext[ax] = cb.hi[ax] - cb.lo[ax];
+            use[ax] = ext[ax] > 0.0;
+            scale_lo[ax] = cb.lo[ax];
+        }
+        const int np = n_pieces(s, e);
+        Bins one;   // uninitialised on purpose: reset(B) below touches the B used bins only
+        std::unique_ptr<Bins[]> many(np > 1 ? new Bins[static_cast<size_t>(np)] : nullptr);
+        Bins *part = np > 1 ? many.get() : &one;
+        pieces(s, e, [&](int t, int ps, int pe) {
+            Bins &b = part[static_cast<size_t>(t)];
+            b.reset(B);
+            for (int i = ps; i < pe; ++i) {
+                const int tr = idx[i];
+                const Box &bx = tb[tr];
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (!use[ax])
+                        continue;
+                    int bi = std::min(B - 1, static_cast<int>((cen[3 * tr + ax] - scale_lo[ax]) / ext[ax] * B));
+                    b.add(ax, bi, bx);
+                }
+            }
+        });
+        Bins &bn = part[0];
+        for (int t = 1; t < np; ++t)
+            for (int ax = 0; ax < 3; ++ax)
+                for (int i = 0; i < B; ++i) {
+                    const Bins &o = part[static_cast<size_t>(t)];
+                    if (o.cnt[ax][i] == 0)
+                        continue;
+                    if (bn.cnt[ax][i] == 0)
+                        bn.bb[ax][i] = o.bb[ax][i];
+                    else
+                        bn.bb[ax][i].grow(o.bb[ax][i]);
+                    bn.cnt[ax][i] += o.cnt[ax][i];
+                }
+        best_cost = std::numeric_limits<double>::infinity();
+        best_axis = -1;
+        best_bin = -1;
+        // Only occupied bins are swept: a split after an empty bin has the sets, hence
+        // the cost, of the split after the occupied bin before it, and the strict `<`
+        // keeps the earlier one -- the same choice as a sweep over all B bins.
+        for (int ax = 0; ax < 3; ++ax) {
+            if (!use[ax])
+                continue;
+            int occ[BMAX], no = 0;
+            for (int i = 0; i < B; ++i)
+                if (bn.cnt[ax][i] > 0)
+                    occ[no++] = i;
+            double ra[BMAX];
+            int rc[BMAX];
+            Box acc;
+            acc.reset();
+            int c = 0;
+            for (int q = no - 1; q >= 0; --q) {   // suffix over occupied bins q..no-1
+                acc.grow(bn.bb[ax][occ[q]]);
+                c += bn.cnt[ax][occ[q]];
+                ra[q] = acc.area();
+                rc[q] = c;
+            }
+            acc.reset();
+            c = 0;
+            for (int q = 0; q + 1 < no; ++q) {
+                acc.grow(bn.bb[ax][occ[q]]);
+                c += bn.cnt[ax][occ[q]];
+                double cost = acc.area() * c + ra[q + 1] * rc[q + 1];
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best_axis = ax;
+                    best_bin = occ[q];
+                }
+            }
+        }
+        if (best_axis < 0)
+            return false;
+        lbox.reset();
+        rbox.reset();
+        for (int i = 0; i < B; ++i)
+            if (bn.cnt[best_axis][i] > 0)
+                (i <= best_bin ? lbox : rbox).grow(bn.bb[best_axis][i]);
+        return true;
+    }
+
     // Builds the subtree over idx[s, e) and returns its child reference.
     int32_t build(int s, int e, int d) {
         depth = std::max(depth, d);
         int n = e - s;
         if (n <= leaf_max || d >= 60)
             return n <= 15 ? leaf(s, e) : split_median(s, e, d);
-        Box cb;
-        cb.reset();
-        for (int i = s; i < e; ++i)
-            cb.grow(&cen[3 * idx[i]]);
-        constexpr int BMAX = 256;
+        const Box cb = centroid_box(s, e);
         const int B = bins;
-        double best_cost = std::numeric_limits<double>::infinity();
-        int best_axis = -1, best_bin = -1;
-        for (int ax = 0; ax < 3; ++ax) {
-            double ext = cb.hi[ax] - cb.lo[ax];
-            if (!(ext > 0.0))
-                continue;
-            Box bb[BMAX];
-            int cnt[BMAX] = {0};
-            for (int i = 0; i < B; ++i)
-                bb[i].reset();
-            for (int i = s; i < e; ++i) {
-                int t = idx[i];
-                int bi = std::min(B - 1, static_cast<int>((cen[3 * t + ax] - cb.lo[ax]) / ext * B));
-                bb[bi].grow(tb[t]);
-                ++cnt[bi];
-            }
-            double la[BMAX], ra[BMAX];
-            int lc[BMAX], rc[BMAX];
-            Box acc;
-            acc.reset();
-            int c = 0;
-            for (int i = 0; i < B; ++i) {
-                acc.grow(bb[i]);
-                c += cnt[i];
-                la[i] = acc.area();
-                lc[i] = c;
-            }
-            acc.reset();
-            c = 0;
-            for (int i = B - 1; i >= 0; --i) {
-                acc.grow(bb[i]);
-                c += cnt[i];
-                ra[i] = acc.area();
-                rc[i] = c;
-            }
-            for (int i = 0; i + 1 < B; ++i) {
-                if (lc[i] == 0 || rc[i + 1] == 0)
-                    continue;
-                double cost = la[i] * lc[i] + ra[i + 1] * rc[i + 1];
-                if (cost < best_cost) {
-                    best_cost = cost;
-                    best_axis = ax;
-                    best_bin = i;
-                }
-            }
-        }
-        if (best_axis < 0)
+        double best_cost;
+        int best_axis, best_bin;
+        Box lbox, rbox;
+        if (!find_split(s, e, cb, best_axis, best_bin, best_cost, lbox, rbox))
             return n <= 15 ? leaf(s, e) : split_median(s, e, d);
         if (sah_ct > 0.0 && n <= 15) {
             // SAH termination: a leaf costs n triangle tests, a split
             // Ct + (A_l n_l + A_r n_r) / A
-            double area = range_box(s, e).area();
+            Box all = lbox;
+            all.grow(rbox);
+            double area = all.area();
             if (area > 0.0 && static_cast<double>(n) <= sah_ct + best_cost / area)
                 return leaf(s, e);
         }
@@ -170,11 +269,11 @@ struct Builder {
         int m = static_cast<int>(mid - idx.begin());
         if (m == s || m == e)
             return split_median(s, e, d);
-        return node(s, m, e, d);
+        return node(s, m, e, d, &lbox, &rbox);
     }
 
     int32_t child(int s, int e, int d, int parent, int slot) {
-        if (tasks && d == par_depth && e - s > leaf_max) {
+        if (tasks && e - s <= kParMin && e - s > leaf_max) {   // small enough for one worker
             tasks->push_back({s, e, d, parent, slot});
             return 0;   // patched after the parallel phase
         }
@@ -196,10 +295,10 @@ struct Builder {
         return node(s, m, e, d);
     }
 
-    int32_t node(int s, int m, int e, int d) {
+    int32_t node(int s, int m, int e, int d, const Box *lb = nullptr, const Box *rb = nullptr) {
         int self = static_cast<int>(nodes.size());
         nodes.emplace_back();
-        Box l = range_box(s, m), r = range_box(m, e);
+        Box l = lb ? *lb : range_box(s, m), r = rb ? *rb : range_box(m, e);
         pad(l);
         pad(r);
         int32_t c0 = child(s, m, d + 1, self, 0);
@@ -255,14 +354,15 @@ BvhBuild build_bvh(const double *tris, size_t n, int leaf_max) {
     if (n <= static_cast<size_t>(b.leaf_max)) {
         wrap_leaf(b.leaf(0, static_cast<int>(n)));
     } else {
-        // Top levels serially; the subtrees below depth `par_depth` on worker
-        // threads (disjoint idx ranges), appended in task order -- the tree
-        // does not depend on the thread count.
+        // Nodes above kParMin triangles are split here with every pass cut across
+        // the threads; the subtrees below them go to worker threads whole (disjoint
+        // idx ranges) and are appended in task order -- the tree does not depend
+        // on the thread count.
         std::vector<Task> tasks;
         unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         if (n >= 65536) {
-            b.par_depth = 6;
             b.tasks = &tasks;
+            b.par_threads = static_cast<int>(std::min(hw, 32u));
         }
         // Large triangles (room walls, area lights) split off at the root: their
         // boxes span the scene, and binned on centroids they would inflate the

@@ -12,6 +12,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 
 using ramlt_b200::EngineBase;
@@ -107,18 +108,26 @@ struct Tok {
 };
 }  // namespace
 
-// parse_scene mirror (core/scene.cpp:104-234): same grammar, same messages.
-static HostScene parse_scene(const std::string &text, const std::string &origin) {
-    HostScene s;
-    std::map<std::string, int> ids;
-    bool have_camera = false;
-    std::vector<std::pair<bool, int>> order;
-    std::string line;
+// Bulk records pre-parsed per text chunk (phase 1, one thread per chunk): the
+// numbers of every "tri" / "sphere" line the fast path accepts, the span of its
+// material token, and every other non-blank line as a `slow` record.  Phase 2
+// walks the records in file order on one thread -- material ids, emitter order
+// and error line numbers depend on everything before a line -- and sends slow
+// records through the istringstream path.
+namespace {
+struct PreRec {
+    const char *lb, *eol;    // the line
+    const char *mb, *me;     // material token (kind 1, 2)
+    int ln;                  // line number within the chunk (1-based)
+    int kind;                // 0 slow, 1 tri, 2 sphere
+    double v[9];
+};
+struct PreChunk {
+    std::vector<PreRec> recs;
+    int lines = 0;
+};
+void pre_parse(const char *cur, const char *end, PreChunk &out) {
     int ln = 0;
-    auto fail = [&](int l, const std::string &msg) {
-        throw std::runtime_error(origin + ":" + std::to_string(l) + ": " + msg);
-    };
-    const char *cur = text.data(), *end = text.data() + text.size();
     while (cur < end) {
         const char *eol = static_cast<const char *>(std::memchr(cur, '\n', static_cast<size_t>(end - cur)));
         if (!eol)
@@ -126,47 +135,119 @@ static HostScene parse_scene(const std::string &text, const std::string &origin)
         const char *lb = cur;
         cur = eol < end ? eol + 1 : end;
         ++ln;
-        {
-            const char *q = lb;
-            while (q < eol && (*q == ' ' || *q == '\t' || *q == '\r'))
-                ++q;
-            if (q == eol || *q == '#')
-                continue;
-            Tok tk{q, eol};
-            const char *tb = q, *te = q;
-            tk.next(tb, te);
-            std::string_view tg(tb, static_cast<size_t>(te - tb));
-            if (tg == "tri") {
+        const char *q = lb;
+        while (q < eol && (*q == ' ' || *q == '\t' || *q == '\r'))
+            ++q;
+        if (q == eol || *q == '#')
+            continue;
+        PreRec r;
+        r.lb = lb, r.eol = eol, r.mb = r.me = nullptr, r.ln = ln, r.kind = 0;
+        Tok tk{q, eol};
+        const char *tb = q, *te = q;
+        tk.next(tb, te);
+        std::string_view tg(tb, static_cast<size_t>(te - tb));
+        if (tg == "tri") {
+            bool ok = true;
+            for (int k = 0; k < 9; ++k)
+                ok = ok && tk.num(r.v[k]);
+            if (ok && tk.next(r.mb, r.me))
+                r.kind = 1;
+        } else if (tg == "sphere") {
+            bool ok = tk.num(r.v[0]) && tk.num(r.v[1]) && tk.num(r.v[2]) && tk.num(r.v[3]);
+            if (ok && r.v[3] > 0.0 && tk.next(r.mb, r.me))
+                r.kind = 2;
+        }
+        out.recs.push_back(r);
+    }
+    out.lines = ln;
+}
+}  // namespace
+
+// parse_scene mirror (core/scene.cpp:104-234): same grammar, same messages.
+static HostScene parse_scene(const std::string &text, const std::string &origin) {
+    HostScene s;
+    std::map<std::string, int> ids;
+    bool have_camera = false;
+    std::vector<std::pair<bool, int>> order;
+    std::string line;
+    auto fail = [&](int l, const std::string &msg) {
+        throw std::runtime_error(origin + ":" + std::to_string(l) + ": " + msg);
+    };
+    // phase 1: chunks cut at line ends, pre-parsed in parallel above 4 MB of text
+    const char *t0 = text.data(), *t1 = text.data() + text.size();
+    unsigned nchunk = 1;
+    if (text.size() >= (size_t(4) << 20))
+        nchunk = std::min(64u, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<const char *> cut(nchunk + 1, t1);
+    cut[0] = t0;
+    for (unsigned i = 1; i < nchunk; ++i) {
+        const char *p = t0 + text.size() / nchunk * i;
+        if (p < cut[i - 1])
+            p = cut[i - 1];
+        const char *nl = static_cast<const char *>(std::memchr(p, '\n', static_cast<size_t>(t1 - p)));
+        cut[i] = nl ? nl + 1 : t1;
+    }
+    std::vector<PreChunk> chunks(nchunk);
+    if (nchunk == 1) {
+        pre_parse(cut[0], cut[1], chunks[0]);
+    } else {
+        std::vector<std::thread> pool;
+        for (unsigned i = 0; i < nchunk; ++i)
+            pool.emplace_back([&, i] {
+                chunks[i].recs.reserve(static_cast<size_t>(cut[i + 1] - cut[i]) / 64 + 16);
+                pre_parse(cut[i], cut[i + 1], chunks[i]);
+            });
+        for (auto &th : pool)
+            th.join();
+    }
+    size_t nrec = 0;
+    for (const PreChunk &ch : chunks)
+        nrec += ch.recs.size();
+    s.tri.reserve(nrec);
+    order.reserve(nrec);
+    // phase 2: file order
+    std::string_view last_name;   // the previous bulk record's material (names never rebind)
+    int last_id = -1;
+    auto lookup = [&](const char *mb, const char *me) {
+        std::string_view nm(mb, static_cast<size_t>(me - mb));
+        if (last_id >= 0 && nm == last_name)
+            return last_id;
+        auto it = ids.find(std::string(nm));
+        if (it == ids.end())
+            return -1;
+        last_name = nm;
+        last_id = it->second;
+        return last_id;
+    };
+    int ln_base = 0;
+    for (const PreChunk &ch : chunks) {
+      for (const PreRec &r : ch.recs) {
+        const int ln = ln_base + r.ln;
+        const char *lb = r.lb, *eol = r.eol;
+        if (r.kind == 1) {
+            const int id = lookup(r.mb, r.me);
+            if (id >= 0) {
                 ramlt_triangle t{};
-                double *v[9] = {&t.a[0], &t.a[1], &t.a[2], &t.b[0], &t.b[1], &t.b[2], &t.c[0], &t.c[1], &t.c[2]};
-                bool ok = true;
-                for (double *x : v)
-                    ok = ok && tk.num(*x);
-                const char *mb, *me;
-                if (ok && tk.next(mb, me)) {
-                    auto it = ids.find(std::string(mb, static_cast<size_t>(me - mb)));
-                    if (it != ids.end()) {
-                        t.material = it->second;
-                        t.emitter = -1;
-                        order.emplace_back(false, static_cast<int>(s.tri.size()));
-                        s.tri.push_back(t);
-                        continue;
-                    }
-                }
-            } else if (tg == "sphere") {
+                std::memcpy(t.a, r.v, 3 * sizeof(double));
+                std::memcpy(t.b, r.v + 3, 3 * sizeof(double));
+                std::memcpy(t.c, r.v + 6, 3 * sizeof(double));
+                t.material = id;
+                t.emitter = -1;
+                order.emplace_back(false, static_cast<int>(s.tri.size()));
+                s.tri.push_back(t);
+                continue;
+            }
+        } else if (r.kind == 2) {
+            const int id = lookup(r.mb, r.me);
+            if (id >= 0) {
                 ramlt_sphere sp{};
-                bool ok = tk.num(sp.center[0]) && tk.num(sp.center[1]) && tk.num(sp.center[2]) && tk.num(sp.radius);
-                const char *mb, *me;
-                if (ok && sp.radius > 0.0 && tk.next(mb, me)) {
-                    auto it = ids.find(std::string(mb, static_cast<size_t>(me - mb)));
-                    if (it != ids.end()) {
-                        sp.material = it->second;
-                        sp.emitter = -1;
-                        order.emplace_back(true, static_cast<int>(s.sph.size()));
-                        s.sph.push_back(sp);
-                        continue;
-                    }
-                }
+                std::memcpy(sp.center, r.v, 3 * sizeof(double));
+                sp.radius = r.v[3];
+                sp.material = id;
+                sp.emitter = -1;
+                order.emplace_back(true, static_cast<int>(s.sph.size()));
+                s.sph.push_back(sp);
+                continue;
             }
         }
         line.assign(lb, static_cast<size_t>(eol - lb));
@@ -273,6 +354,8 @@ static HostScene parse_scene(const std::string &text, const std::string &origin)
         } else {
             fail(ln, "unknown record '" + tag + "'");
         }
+      }
+      ln_base += ch.lines;
     }
     if (!have_camera)
         throw std::runtime_error(origin + ": scene has no camera");

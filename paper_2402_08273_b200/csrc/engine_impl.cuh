@@ -451,7 +451,7 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     if (const char *v = std::getenv("RAMLT_STEP_KERNEL")) {
         use_co_ = std::string(v) == "co" || std::string(v) == "co_static" || std::string(v) == "wf";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
-        use_wf_ = use_bvh_ && std::string(v) == "wf";
+        use_wf_ = std::string(v) == "wf";   // brute-force scenes too (k_wf_trace_brute), G == 1
     }
     // ray records carry (chain, batch ordinal) in 27 + 5 bits
     if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
@@ -1044,6 +1044,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     }
     auto logic = rd::k_wf_logic<R, RK>;
     auto trace = rd::k_wf_trace<R>;
+    auto trace_brute = rd::k_wf_trace_brute<R>;
     size_t lsmem = smem_;
     size_t tsmem = (smem_ + 15) & ~size_t(15);
     rd::StepParams<R> PL = P;   // k_wf_logic's parameters: co_stack_off = its shared-memory coroutine states
@@ -1054,7 +1055,8 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     P.co_stack_off = static_cast<unsigned>(tsmem);
     tsmem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
     const int lper = prepare(reinterpret_cast<const void *>(logic), lsmem);
-    const int tper = prepare(reinterpret_cast<const void *>(trace), tsmem);
+    const int tper = use_bvh_ ? prepare(reinterpret_cast<const void *>(trace), tsmem)
+                              : prepare(reinterpret_cast<const void *>(trace_brute), tsmem);
     const unsigned lblocks = std::min<unsigned>(static_cast<unsigned>((C + 127) / 128),
                                                 static_cast<unsigned>(std::max(lper, 1) * sms_));
     const unsigned tblocks = static_cast<unsigned>(std::max(tper, 1) * sms_);
@@ -1092,8 +1094,12 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
             RAMLT_CUDA(cudaEventRecord(t0, stream_));
         }
         // traces this round's rays; zeroes the counters the next round's logic appends to
-        trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 3 + a, cnt + 2,
-                                                 cnt + (a ^ 1), cnt + 3 + (a ^ 1));
+        if (use_bvh_)
+            trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 3 + a, cnt + 2,
+                                                     cnt + (a ^ 1), cnt + 3 + (a ^ 1));
+        else
+            trace_brute<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 3 + a,
+                                                           cnt + (a ^ 1), cnt + 3 + (a ^ 1));
         if (d_.profile_kernels) {
             RAMLT_CUDA(cudaEventRecord(t1, stream_));
             ev_trace_.emplace_back(t0, t1);

@@ -335,4 +335,43 @@ k_wf_trace(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restr
     }
 }
 
+// Brute-force scenes (primitives staged in shared memory, <= 128 triangles): the
+// same queue traced with the linear scan of core/scene.cpp:57-92 -- one ray per
+// lane, every lane of a warp in the same primitive loop (no per-lane mutation
+// state, so the scan runs at full warp width whatever phase each chain is in).
+template <class R>
+__global__ void __launch_bounds__(128)
+k_wf_trace_brute(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restrict__ hits,
+                 unsigned *__restrict__ occ, const unsigned *n_ptr, unsigned *zero_a, unsigned *zero_b) {
+    extern __shared__ __align__(16) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *zero_a = 0;
+        *zero_b = 0;
+    }
+    const unsigned n = *n_ptr;
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const WfRay<R> r = ld_ray(rays + i);
+        if (!(r.lim > R(0)))   // unused slot of a batch
+            continue;
+        RayReq<R> q;
+        q.o = mk(r.o[0], r.o[1], r.o[2]);
+        q.d = mk(r.d[0], r.d[1], r.d[2]);
+        q.lim = r.lim;
+        R t;
+        const int prim = trace_ray<R, false>(S, q, t);
+        const int c = r.ck & ((1 << kWfChainBits) - 1);
+        if (r.lim < M<R>::inf()) {
+            if (prim >= 0)
+                atomicOr(occ + c, 1u << (static_cast<unsigned>(r.ck) >> kWfChainBits));
+        } else {
+            WfHit<R> h;
+            h.t = t;
+            h.prim = prim;
+            hits[c] = h;
+        }
+    }
+}
+
 }  // namespace rd

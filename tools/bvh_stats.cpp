@@ -9,6 +9,7 @@
 #include "bvh.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -138,7 +139,24 @@ int main(int argc, char **argv) {
         }
     }
     size_t n = coords.size() / 9;
+    auto tb0 = std::chrono::steady_clock::now();
     BvhBuild b = build_bvh(coords.data(), n, leaf_max);
+    double tbuild = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb0).count();
+    {   // FNV-1a over nodes and order: equal trees print equal hashes
+        unsigned long long h = 1469598103934665603ull;
+        auto mix = [&](const void *p, size_t nb) {
+            const unsigned char *q = static_cast<const unsigned char *>(p);
+            for (size_t i = 0; i < nb; ++i)
+                h = (h ^ q[i]) * 1099511628211ull;
+        };
+        for (const BvhBuildNode &nd : b.nodes) {
+            mix(nd.lo, sizeof(nd.lo));
+            mix(nd.hi, sizeof(nd.hi));
+            mix(nd.child, sizeof(nd.child));
+        }
+        mix(b.order.data(), b.order.size() * sizeof(int32_t));
+        std::printf("build %.3f s, tree hash %016llx\n", tbuild, h);
+    }
     std::vector<Tri> t(n);
     for (size_t i = 0; i < n; ++i) {
         const double *c = &coords[9 * static_cast<size_t>(b.order[i])];
