@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -141,7 +142,7 @@ private:
                      unsigned long long rem, bool record);
     void adapt_after_step(int j, unsigned long long span_start);
     template <bool INIT = false> void launch_step_co(const rd::StepParams<R> &P);
-    template <int RK> void launch_step_wf(rd::StepParams<R> P);
+    template <int RK, bool INIT = false> void launch_step_wf(rd::StepParams<R> P);
     bool launch_coop(int j0, int j1, unsigned long long span_start, unsigned long long per,
                      unsigned long long rem);
     int coop_state_ = -1;   // -1 unknown, 0 unavailable, 1 usable
@@ -203,8 +204,10 @@ private:
     int co_carveout_ = -1;    // k_step_co: RAMLT_CO_CARVEOUT percent (-1: driver default)
     // wavefront step (BVH scenes, ramlt_wavefront.cuh): RAMLT_STEP_KERNEL=wf (default) | co
     bool use_wf_ = false;
+    bool use_wf_init_ = false;   // chain initialisation as wavefront rounds (RAMLT_INIT_KERNEL=wf; default with use_wf_)
     int wf_refill_ = 8;       // k_wf_trace: RAMLT_WF_REFILL idle lanes end a traversal round
     int wf_check_ = 4;        // rounds between host checks of the queue length (RAMLT_WF_CHECK)
+    bool wf_log_ = false;     // RAMLT_WF_LOG=1
     bool wf_poll_ = false;    // RAMLT_WF_POLL=1: poll the queue length every wf_check_ rounds even for one-step launches
     DBuf<uint4> wf_state_;
     DBuf<rd::GV<R>> wf_pv_;
@@ -212,7 +215,7 @@ private:
     DBuf<rd::WfHit<R>> wf_hits_;   // closest-hit answers by chain
     DBuf<unsigned> wf_occ_;        // visibility-batch answers by chain (bit k: ray k occluded)
     DBuf<int> wf_cq_[2];           // chain queues (ping-pong)
-    DBuf<unsigned> wf_cnt_;        // chain-queue lengths [0,1], trace work counter [2], ray-queue lengths [3,4]
+    DBuf<unsigned> wf_cnt_;        // chain-queue lengths (ping-pong x yield point), trace work counter, ray-queue lengths
     unsigned *wf_host_ = nullptr;   // pinned: queue length read back every wf_check_ rounds
     uint64_t wf_rounds_ = 0;
     // film
@@ -446,8 +449,10 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     use_co_ = use_bvh_;
     use_co_init_ = use_bvh_;
     use_wf_ = use_bvh_;
-    if (const char *v = std::getenv("RAMLT_INIT_KERNEL"))
-        use_co_init_ = std::string(v) == "co";
+    if (const char *v = std::getenv("RAMLT_INIT_KERNEL")) {
+        use_co_init_ = std::string(v) == "co" || std::string(v) == "wf";
+        use_wf_init_ = std::string(v) == "wf";
+    }
     if (const char *v = std::getenv("RAMLT_STEP_KERNEL")) {
         use_co_ = std::string(v) == "co" || std::string(v) == "co_static" || std::string(v) == "wf";
         steal_ = std::string(v) == "co_static" ? 0 : 1;
@@ -456,8 +461,14 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     // ray records carry (chain, batch ordinal) in 27 + 5 bits
     if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
         use_wf_ = false;
+    if (!std::getenv("RAMLT_INIT_KERNEL"))
+        use_wf_init_ = use_wf_ && use_co_init_ && C_ >= 65536;   // below, the fused kernel's single launch wins
+    if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
+        use_wf_init_ = false;
     if (const char *v = std::getenv("RAMLT_WF_REFILL"))
         wf_refill_ = std::min(32, std::max(1, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_WF_LOG"))
+        wf_log_ = std::string(v) == "1";
     if (const char *v = std::getenv("RAMLT_WF_POLL"))
         wf_poll_ = std::string(v) == "1";
     if (const char *v = std::getenv("RAMLT_WF_CHECK"))
@@ -833,11 +844,21 @@ template <class R> void EngineT<R>::estimate_b(double *b, double *se) {
 
 template <class R> void EngineT<R>::init_chains() {
     rd::StepParams<R> P = params();
-    if (use_co_init_) {   // BVH scenes: the coroutine kernel with dynamic ray fetch
+    if (use_co_init_) {   // BVH scenes: the coroutine, as wavefront rounds or the fused kernel
         P.steal = 1;
         P.refill = init_refill_;
         P.init_attempts = 50000000ull;
-        launch_step_co<true>(P);
+        if (use_wf_init_) {
+            P.refill = wf_refill_;
+            P.j0 = 0;
+            P.j1 = 1;
+            if (d_.rng == RAMLT_RNG_PHILOX)
+                launch_step_wf<rd::RNG_PHILOX, true>(P);
+            else
+                launch_step_wf<rd::RNG_PCG, true>(P);
+        } else {
+            launch_step_co<true>(P);
+        }
         check_err("init");
         chains_ready_ = true;
         return;
@@ -1025,10 +1046,10 @@ void EngineT<R>::launch_step_co(const rd::StepParams<R> &P0) {
 // wf_check_ rounds; the rounds launched past the last ray find empty queues
 // and exit at once.
 template <class R>
-template <int RK>
+template <int RK, bool INIT>
 void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     const size_t C = static_cast<size_t>(C_);
-    constexpr int K = rd::Chunks<rd::WfState<R, RK>>::K;
+    constexpr int K = rd::Chunks<rd::WfState<R, RK, INIT>>::K;
     const size_t per_chain = static_cast<size_t>(std::max<int>(1, static_cast<int>(d_.max_vertices) - 1));
     if (wf_state_.n < K * C) {
         wf_state_.alloc(K * C);
@@ -1037,12 +1058,12 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         wf_hits_.alloc(C);
         wf_occ_.alloc(C);
         for (int q = 0; q < 2; ++q)
-            wf_cq_[q].alloc(C);
-        wf_cnt_.alloc(8);
+            wf_cq_[q].alloc(rd::kWfQueues * C);
+        wf_cnt_.alloc(16);
         if (!wf_host_)
-            RAMLT_CUDA(cudaMallocHost(&wf_host_, sizeof(unsigned)));
+            RAMLT_CUDA(cudaMallocHost(&wf_host_, rd::kWfQueues * sizeof(unsigned)));
     }
-    auto logic = rd::k_wf_logic<R, RK>;
+    auto logic = rd::k_wf_logic<R, RK, INIT>;
     auto trace = rd::k_wf_trace<R>;
     auto trace_brute = rd::k_wf_trace_brute<R>;
     size_t lsmem = smem_;
@@ -1050,7 +1071,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     rd::StepParams<R> PL = P;   // k_wf_logic's parameters: co_stack_off = its shared-memory coroutine states
 #if RAMLT_WF_SMEM
     PL.co_stack_off = static_cast<unsigned>(tsmem);
-    lsmem = tsmem + static_cast<size_t>(128) * sizeof(rd::WfState<R, RK>);
+    lsmem = tsmem + static_cast<size_t>(128) * sizeof(rd::WfState<R, RK, INIT>);
 #endif
     P.co_stack_off = static_cast<unsigned>(tsmem);
     tsmem += static_cast<size_t>(128) * rd::BvhTrav<R>::SSTACK * sizeof(int);
@@ -1061,9 +1082,13 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
                                                 static_cast<unsigned>(std::max(lper, 1) * sms_));
     const unsigned tblocks = static_cast<unsigned>(std::max(tper, 1) * sms_);
     unsigned *cnt = wf_cnt_.p;
-    RAMLT_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned), stream_));
+    // cnt: chain-queue lengths [0..3] / [4..7] (ping-pong, one per yield point), trace work
+    // counter [8], ray-queue lengths [9] / [10]
+    constexpr int NQ = rd::kWfQueues;
+    RAMLT_CUDA(cudaMemsetAsync(cnt, 0, 16 * sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (d_.profile_kernels) {
+    const bool prof = d_.profile_kernels && !INIT;
+    if (prof) {
         if (ev_.size() + ev_trace_.size() >= 4096)
             drain_events();
         RAMLT_CUDA(cudaEventCreate(&e0));
@@ -1071,42 +1096,51 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         RAMLT_CUDA(cudaEventRecord(e0, stream_));
     }
     rd::WfParams<R> W;
-    W.trace_work = cnt + 2;
+    W.trace_work = cnt + 2 * NQ;
     W.rays = wf_rays_.p;
     W.hits = wf_hits_.p;
     W.occ = wf_occ_.p;
     W.state = wf_state_.p;
     W.pv = wf_pv_.p;
-    const bool poll = P.j1 - P.j0 > 1 || wf_poll_;
+    // chain initialisation runs until every chain found a contributing path: polled
+    const bool poll = INIT || P.j1 - P.j0 > 1 || wf_poll_;
     const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2;
     for (int r = 0;; ++r) {
         const int a = r & 1;
         W.cq_in = wf_cq_[a ^ 1].p;
-        W.n_in = cnt + (a ^ 1);
+        W.n_in = cnt + NQ * (a ^ 1);
         W.cq_out = wf_cq_[a].p;
-        W.n_out = cnt + a;
-        W.n_rays = cnt + 3 + a;
+        W.n_out = cnt + NQ * a;
+        W.n_rays = cnt + 2 * NQ + 1 + a;
         logic<<<lblocks, 128, lsmem, stream_>>>(PL, W, r == 0 ? 1 : 0);
         cudaEvent_t t0 = nullptr, t1 = nullptr;
-        if (d_.profile_kernels) {
+        if (prof) {
             RAMLT_CUDA(cudaEventCreate(&t0));
             RAMLT_CUDA(cudaEventCreate(&t1));
             RAMLT_CUDA(cudaEventRecord(t0, stream_));
         }
         // traces this round's rays; zeroes the counters the next round's logic appends to
         if (use_bvh_)
-            trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 3 + a, cnt + 2,
-                                                     cnt + (a ^ 1), cnt + 3 + (a ^ 1));
+            trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 2 * NQ + 1 + a,
+                                                     cnt + 2 * NQ, cnt + NQ * (a ^ 1), cnt + 2 * NQ + 1 + (a ^ 1));
         else
-            trace_brute<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 3 + a,
-                                                           cnt + (a ^ 1), cnt + 3 + (a ^ 1));
-        if (d_.profile_kernels) {
+            trace_brute<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p,
+                                                           cnt + 2 * NQ + 1 + a, cnt + NQ * (a ^ 1),
+                                                           cnt + 2 * NQ + 1 + (a ^ 1));
+        if (prof) {
             RAMLT_CUDA(cudaEventRecord(t1, stream_));
             ev_trace_.emplace_back(t0, t1);
         }
         launches_ += 2;
         ++wf_rounds_;
         RAMLT_CUDA(cudaGetLastError());
+        if (wf_log_) {   // RAMLT_WF_LOG=1: the round's queue lengths (ties an ncu launch to its ray count)
+            unsigned hq[16];
+            RAMLT_CUDA(cudaMemcpyAsync(hq, cnt, sizeof(hq), cudaMemcpyDeviceToHost, stream_));
+            RAMLT_CUDA(cudaStreamSynchronize(stream_));
+            std::fprintf(stderr, "wf %s round %d: rays %u, chains yielded %u %u %u %u\n", INIT ? "init" : "step", r,
+                         hq[2 * NQ + 1 + a], hq[NQ * a], hq[NQ * a + 1], hq[NQ * a + 2], hq[NQ * a + 3]);
+        }
         // A mutation yields at most max_vertices + 1 times (max_vertices - 1 closest-hit
         // rays, the eval_contribution batch, the eye_path_density batch), so a
         // one-step launch needs max_vertices + 2 logic rounds: they are enqueued
@@ -1115,13 +1149,16 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         // Multi-step launches (Fixed strategy) poll every wf_check_ rounds instead.
         const bool last_planned = !poll && r + 1 >= planned;
         if (last_planned || (poll && r % wf_check_ == wf_check_ - 1)) {
-            RAMLT_CUDA(cudaMemcpyAsync(wf_host_, cnt + a, sizeof(unsigned), cudaMemcpyDeviceToHost, stream_));
+            RAMLT_CUDA(cudaMemcpyAsync(wf_host_, cnt + NQ * a, NQ * sizeof(unsigned), cudaMemcpyDeviceToHost, stream_));
             RAMLT_CUDA(cudaStreamSynchronize(stream_));
-            if (*wf_host_ == 0)
+            unsigned left = 0;
+            for (int q = 0; q < NQ; ++q)
+                left += wf_host_[q];
+            if (left == 0)
                 break;
         }
     }
-    if (d_.profile_kernels) {
+    if (prof) {
         RAMLT_CUDA(cudaEventRecord(e1, stream_));
         ev_.emplace_back(e0, e1);
     }

@@ -46,16 +46,24 @@ template <class R> struct alignas(sizeof(R) * 2) WfHit {
 };
 
 // Coroutine state carried between rounds.
-template <class R, int RK> struct WfState {
-    StepCo<R, RK, false> co;
+template <class R, int RK, bool INIT = false> struct WfState {
+    StepCo<R, RK, INIT> co;
     int j, jend;
 };
 
+// Chain queues are kept per yield point (kWfQueues sub-queues of capacity C each:
+// retrace ray, large-step bounce, eval_contribution batch, eye_path_density batch),
+// and a round resumes them queue by queue with every queue's segment starting on a
+// warp boundary: the lanes of a warp resume at the same point of the coroutine
+// instead of at four different ones.
+constexpr int kWfQueues = 4;
+__device__ __forceinline__ int wf_queue_of(int pc) { return pc == 1 ? 0 : (pc == 2 ? 1 : (pc == 5 ? 2 : 3)); }
+
 template <class R> struct WfParams {
-    const int *cq_in;          // chains resumed this round (round > 0)
-    const unsigned *n_in;
-    int *cq_out;               // chains that yielded this round
-    unsigned *n_out;
+    const int *cq_in;          // chains resumed this round (round > 0): sub-queue q at cq_in + q * C
+    const unsigned *n_in;      // [kWfQueues]
+    int *cq_out;               // chains that yielded this round, by yield point
+    unsigned *n_out;           // [kWfQueues]
     WfRay<R> *rays;            // this round's ray queue
     unsigned *n_rays;
     unsigned *trace_work;      // zeroed here for the following k_wf_trace
@@ -182,24 +190,43 @@ template <class T> __device__ __forceinline__ void st_state(const T &v, uint4 *_
 #endif
 }
 
-template <class R, int RK>
+// INIT: chain initialisation (core/driver.cpp:219-242) instead of a step -- the
+// coroutine draws large-step eye paths from the chain's init stream until one
+// contributes and stores the chain itself; rounds run until every chain has one.
+template <class R, int RK, bool INIT = false>
 __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) k_wf_logic(StepParams<R> P, WfParams<R> W, int round0) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *W.trace_work = 0;
-    const unsigned n = round0 ? static_cast<unsigned>(P.C) : *W.n_in;
+    // round > 0: index space = the sub-queues back to back, each padded to whole warps
+    unsigned qn[kWfQueues], qstart[kWfQueues + 1];
+    qstart[0] = 0;
+#pragma unroll
+    for (int q = 0; q < kWfQueues; ++q) {
+        qn[q] = round0 ? 0u : W.n_in[q];
+        qstart[q + 1] = qstart[q] + ((qn[q] + 31u) & ~31u);
+    }
+    const unsigned n = round0 ? static_cast<unsigned>(P.C) : qstart[kWfQueues];
     RayCount rc;
     const unsigned stride = gridDim.x * blockDim.x;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
 #if RAMLT_WF_SMEM
-        WfState<R, RK> &s = reinterpret_cast<WfState<R, RK> *>(smem + P.co_stack_off)[threadIdx.x];
+        WfState<R, RK, INIT> &s = reinterpret_cast<WfState<R, RK, INIT> *>(smem + P.co_stack_off)[threadIdx.x];
 #else
-        WfState<R, RK> s;
+        WfState<R, RK, INIT> s;
 #endif
         WfSink<R> sink{W.rays, W.n_rays, W.occ, 0, 0u};
         int c;
-        if (round0) {
+        if (round0 && INIT) {
+            c = static_cast<int>(i);
+            s.co.c = c;
+            s.co.rng.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(P.chain_off + c) * 2ull);
+            s.co.pc = 0;
+            s.co.attempts = 0;
+            s.j = 0;
+            s.jend = 1;
+        } else if (round0) {
             c = static_cast<int>(i);
             co_load(s.co, P, c);
             const unsigned long long my_steps =
@@ -212,7 +239,14 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
                 continue;
             }
         } else {
-            c = W.cq_in[i];
+            int q = 0;
+#pragma unroll
+            for (int k = 1; k < kWfQueues; ++k)
+                q += i >= qstart[k] ? 1 : 0;
+            const unsigned k = i - qstart[q];
+            if (k >= qn[q])   // padding of this queue's last warp
+                continue;
+            c = W.cq_in[static_cast<size_t>(q) * P.C + k];
             ld_state(s, W.state, static_cast<size_t>(P.C), c);
             const WfHit<R> h = W.hits[c];
             s.co.res_prim = h.prim;
@@ -226,15 +260,19 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
                 P.span_start + static_cast<unsigned long long>(s.j) * P.C_total + P.chain_off + c;
             if (s.co.advance(P, S, pv, rc, index, sink) == CO_RAY_PENDING) {
                 const unsigned act = __activemask();
-                const int leader = __ffs(act) - 1;
+                const int q = wf_queue_of(s.co.pc);
+                const unsigned grp = __match_any_sync(act, q);   // the lanes yielding at the same point
+                const int leader = __ffs(grp) - 1;
                 unsigned base = 0;
                 if (static_cast<int>(threadIdx.x & 31) == leader)
-                    base = atomicAdd(W.n_out, static_cast<unsigned>(__popc(act)));
-                base = __shfl_sync(act, base, leader);
-                W.cq_out[base + __popc(act & ((1u << (threadIdx.x & 31)) - 1u))] = c;
+                    base = atomicAdd(W.n_out + q, static_cast<unsigned>(__popc(grp)));
+                base = __shfl_sync(grp, base, leader);
+                W.cq_out[static_cast<size_t>(q) * P.C + base + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u))] = c;
                 st_state(s, W.state, static_cast<size_t>(P.C), c);
                 break;
             }
+            if (INIT)   // the coroutine stored the chain
+                break;
             if (++s.j >= s.jend) {
                 co_store(s.co, P);
                 break;
@@ -274,10 +312,10 @@ k_wf_trace(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *__restr
            unsigned *__restrict__ occ, const unsigned *n_ptr, unsigned *work, unsigned *zero_a, unsigned *zero_b) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        *zero_a = 0;
+    if (blockIdx.x == 0 && threadIdx.x < kWfQueues)   // the next round's chain-queue lengths ...
+        zero_a[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)           // ... and its ray-queue length
         *zero_b = 0;
-    }
     const unsigned n = *n_ptr;
     const unsigned lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -345,10 +383,10 @@ k_wf_trace_brute(StepParams<R> P, const WfRay<R> *__restrict__ rays, WfHit<R> *_
                  unsigned *__restrict__ occ, const unsigned *n_ptr, unsigned *zero_a, unsigned *zero_b) {
     extern __shared__ __align__(16) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        *zero_a = 0;
+    if (blockIdx.x == 0 && threadIdx.x < kWfQueues)   // the next round's chain-queue lengths ...
+        zero_a[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)           // ... and its ray-queue length
         *zero_b = 0;
-    }
     const unsigned n = *n_ptr;
     const unsigned stride = gridDim.x * blockDim.x;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {

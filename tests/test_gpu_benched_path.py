@@ -65,6 +65,7 @@ def test_f64_full_scene_bvh_matches_linear_scan_oracle(launch, big_scene, full_s
     launch (small chain counts)."""
     o = full_scene_oracle
     monkeypatch.setenv("RAMLT_STEP_KERNEL", "wf" if launch == "wavefront" else "co")
+    monkeypatch.setenv("RAMLT_INIT_KERNEL", "wf" if launch == "wavefront" else "co")   # wf: k_wf_logic<INIT> rounds
     if launch != "coop":
         monkeypatch.setenv("RAMLT_COOP", "0")
     eng = _engine(big_scene, **FULL, precision="f64", rng="philox", adapt_mode="pooled", accel="bvh",
@@ -93,11 +94,12 @@ def test_f64_full_scene_bvh_matches_linear_scan_oracle(launch, big_scene, full_s
 @pytest.mark.parametrize("kernel", ["wf", "co"])
 @pytest.mark.parametrize("strategy,rng", [("fixed", "pcg32"), ("fixed", "philox"), ("ra-quadtree", "philox")])
 def test_f32_bvh_equals_f32_brute_force(strategy, rng, kernel, monkeypatch):
-    """kernel = the BVH run's step (wf: wavefront rounds, the benched default; co: the
-    fused coroutine kernel); the brute-force run always steps with the coroutine kernel."""
+    """kernel = both runs' step and chain initialisation (wf: wavefront rounds, the benched
+    default, traced by k_wf_trace over the BVH / k_wf_trace_brute over the linear scan; co:
+    the fused coroutine kernel with its BVH / shared-memory scan)."""
     from paper_2402_08273_b200 import scenes
     monkeypatch.setenv("RAMLT_STEP_KERNEL", kernel)
-    monkeypatch.setenv("RAMLT_INIT_KERNEL", "co")
+    monkeypatch.setenv("RAMLT_INIT_KERNEL", kernel)
     monkeypatch.setenv("RAMLT_COOP", "0")
     scene = scenes.cluster_room(n_tris=2000, clusters=8, seed=3)
     C, K = 2048, 24
