@@ -204,10 +204,15 @@ private:
     int co_carveout_ = -1;    // k_step_co: RAMLT_CO_CARVEOUT percent (-1: driver default)
     // wavefront step (BVH scenes, ramlt_wavefront.cuh): RAMLT_STEP_KERNEL=wf (default) | co
     bool use_wf_ = false;
-    bool use_wf_init_ = false;   // chain initialisation as wavefront rounds (RAMLT_INIT_KERNEL=wf; default with use_wf_)
+    bool use_wf_init_ = false;   // chain initialisation as wavefront rounds (RAMLT_INIT_KERNEL=wf)
     int wf_refill_ = 8;       // k_wf_trace: RAMLT_WF_REFILL idle lanes end a traversal round
     int wf_check_ = 4;        // rounds between host checks of the queue length (RAMLT_WF_CHECK)
     bool wf_log_ = false;     // RAMLT_WF_LOG=1
+    int wf_pipes_ = 1;        // RAMLT_WF_PIPES: chain ranges stepped as concurrent wavefront pipelines
+    size_t wf_pipes_min_ = size_t(1) << 18;   // RAMLT_WF_PIPES_MIN: fewest chains split into pipelines
+    int wf_lblk_ = 0, wf_tblk_ = 0;   // RAMLT_WF_LBLK / RAMLT_WF_TBLK: resident blocks per SM of a pipeline's kernels
+    cudaStream_t wf_stream2_ = nullptr;
+    cudaEvent_t wf_ev_[3] = {nullptr, nullptr, nullptr};
     bool wf_poll_ = false;    // RAMLT_WF_POLL=1: poll the queue length every wf_check_ rounds even for one-step launches
     DBuf<uint4> wf_state_;
     DBuf<rd::GV<R>> wf_pv_;
@@ -461,14 +466,30 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     // ray records carry (chain, batch ordinal) in 27 + 5 bits
     if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
         use_wf_ = false;
-    if (!std::getenv("RAMLT_INIT_KERNEL"))
-        use_wf_init_ = use_wf_ && use_co_init_ && C_ >= 65536;   // below, the fused kernel's single launch wins
+    // Chain initialisation stays with the fused kernel by default: nearly every attempt of a
+    // chain fails (c4/c5: ~37 attempts of ~11 rays before a path reaches a light), so as
+    // wavefront rounds every chain's state makes thousands of HBM round trips -- c5 init
+    // 7.4 s (wf) vs 4.5 s (co), c4 1.86 s vs 0.75 s (profiles/r02t).  RAMLT_INIT_KERNEL=wf
+    // keeps the wavefront form for the parity tests.
     if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
         use_wf_init_ = false;
     if (const char *v = std::getenv("RAMLT_WF_REFILL"))
         wf_refill_ = std::min(32, std::max(1, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_WF_LOG"))
         wf_log_ = std::string(v) == "1";
+    if (const char *v = std::getenv("RAMLT_WF_PIPES"))
+        wf_pipes_ = std::min(2, std::max(1, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_WF_PIPES_MIN"))
+        wf_pipes_min_ = static_cast<size_t>(std::max(256, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_WF_LBLK"))
+        wf_lblk_ = std::min(8, std::max(0, std::atoi(v)));
+    if (const char *v = std::getenv("RAMLT_WF_TBLK"))
+        wf_tblk_ = std::min(16, std::max(0, std::atoi(v)));
+    if (wf_pipes_ > 1) {
+        RAMLT_CUDA(cudaStreamCreateWithFlags(&wf_stream2_, cudaStreamNonBlocking));
+        for (cudaEvent_t &e : wf_ev_)
+            RAMLT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     if (const char *v = std::getenv("RAMLT_WF_POLL"))
         wf_poll_ = std::string(v) == "1";
     if (const char *v = std::getenv("RAMLT_WF_CHECK"))
@@ -595,6 +616,11 @@ template <class R> void EngineT<R>::drain_events() {
 template <class R> EngineT<R>::~EngineT() {
     if (wf_host_)
         cudaFreeHost(wf_host_);
+    if (wf_stream2_)
+        cudaStreamDestroy(wf_stream2_);
+    for (cudaEvent_t e : wf_ev_)
+        if (e)
+            cudaEventDestroy(e);
     for (auto &e : ev_trace_) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -1059,7 +1085,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         wf_occ_.alloc(C);
         for (int q = 0; q < 2; ++q)
             wf_cq_[q].alloc(rd::kWfQueues * C);
-        wf_cnt_.alloc(16);
+        wf_cnt_.alloc(32);
         if (!wf_host_)
             RAMLT_CUDA(cudaMallocHost(&wf_host_, rd::kWfQueues * sizeof(unsigned)));
     }
@@ -1078,14 +1104,38 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     const int lper = prepare(reinterpret_cast<const void *>(logic), lsmem);
     const int tper = use_bvh_ ? prepare(reinterpret_cast<const void *>(trace), tsmem)
                               : prepare(reinterpret_cast<const void *>(trace_brute), tsmem);
-    const unsigned lblocks = std::min<unsigned>(static_cast<unsigned>((C + 127) / 128),
-                                                static_cast<unsigned>(std::max(lper, 1) * sms_));
-    const unsigned tblocks = static_cast<unsigned>(std::max(tper, 1) * sms_);
-    unsigned *cnt = wf_cnt_.p;
-    // cnt: chain-queue lengths [0..3] / [4..7] (ping-pong, one per yield point), trace work
-    // counter [8], ray-queue lengths [9] / [10]
+    // chain initialisation runs until every chain found a contributing path: polled
+    const bool poll = INIT || P.j1 - P.j0 > 1 || wf_poll_;
+    const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2;
+    // Pipelines: the chains of a one-step launch are cut into wf_pipes_ contiguous ranges,
+    // each with its own queues and counters, and the ranges' rounds are enqueued on
+    // separate streams.  k_wf_trace is bound by instruction issue and k_wf_logic by
+    // memory latency, so a range in its trace kernel and another in its logic kernel
+    // share the SMs instead of taking turns; the second range starts one logic kernel
+    // late so that the two stay out of phase.  Each range's kernels get 1 / wf_pipes_
+    // of the resident blocks.  Results do not depend on the split (per-chain state;
+    // pooled adaptation and the film are order-independent sums / atomics).
+    const int npipe = (!poll && !wf_log_ && wf_pipes_ > 1 && C >= wf_pipes_min_) ? 2 : 1;
     constexpr int NQ = rd::kWfQueues;
-    RAMLT_CUDA(cudaMemsetAsync(cnt, 0, 16 * sizeof(unsigned), stream_));
+    struct Pipe {
+        size_t c0, cn;
+        cudaStream_t st;
+        unsigned *cnt;   // chain-queue lengths [0..3] / [4..7] (ping-pong, one per yield point), trace
+                         // work counter [8], ray-queue lengths [9] / [10]
+        unsigned lblocks, tblocks;
+    } pipe[2];
+    for (int p = 0; p < npipe; ++p) {
+        Pipe &pp = pipe[p];
+        pp.c0 = npipe == 1 ? 0 : (p == 0 ? 0 : ((C / 2 + 127) & ~size_t(127)));
+        pp.cn = npipe == 1 ? C : (p == 0 ? ((C / 2 + 127) & ~size_t(127)) : C - ((C / 2 + 127) & ~size_t(127)));
+        pp.st = p == 0 ? stream_ : wf_stream2_;
+        pp.cnt = wf_cnt_.p + 16 * p;
+        const int lb = npipe == 1 ? std::max(lper, 1) : std::max(1, wf_lblk_ > 0 ? wf_lblk_ : lper / 2);
+        const int tb = npipe == 1 ? std::max(tper, 1) : std::max(1, wf_tblk_ > 0 ? wf_tblk_ : tper / 2);
+        pp.lblocks = std::min<unsigned>(static_cast<unsigned>((pp.cn + 127) / 128), static_cast<unsigned>(lb * sms_));
+        pp.tblocks = static_cast<unsigned>(tb * sms_);
+    }
+    RAMLT_CUDA(cudaMemsetAsync(wf_cnt_.p, 0, 32 * sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool prof = d_.profile_kernels && !INIT;
     if (prof) {
@@ -1095,48 +1145,68 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         RAMLT_CUDA(cudaEventCreate(&e1));
         RAMLT_CUDA(cudaEventRecord(e0, stream_));
     }
-    rd::WfParams<R> W;
-    W.trace_work = cnt + 2 * NQ;
-    W.rays = wf_rays_.p;
-    W.hits = wf_hits_.p;
-    W.occ = wf_occ_.p;
-    W.state = wf_state_.p;
-    W.pv = wf_pv_.p;
-    // chain initialisation runs until every chain found a contributing path: polled
-    const bool poll = INIT || P.j1 - P.j0 > 1 || wf_poll_;
-    const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2;
+    auto fork = [&] {
+        if (npipe > 1) {
+            RAMLT_CUDA(cudaEventRecord(wf_ev_[0], stream_));
+            RAMLT_CUDA(cudaStreamWaitEvent(wf_stream2_, wf_ev_[0], 0));
+        }
+    };
+    auto join = [&] {
+        if (npipe > 1) {
+            RAMLT_CUDA(cudaEventRecord(wf_ev_[1], wf_stream2_));
+            RAMLT_CUDA(cudaStreamWaitEvent(stream_, wf_ev_[1], 0));
+        }
+    };
+    fork();
     for (int r = 0;; ++r) {
         const int a = r & 1;
-        W.cq_in = wf_cq_[a ^ 1].p;
-        W.n_in = cnt + NQ * (a ^ 1);
-        W.cq_out = wf_cq_[a].p;
-        W.n_out = cnt + NQ * a;
-        W.n_rays = cnt + 2 * NQ + 1 + a;
-        logic<<<lblocks, 128, lsmem, stream_>>>(PL, W, r == 0 ? 1 : 0);
-        cudaEvent_t t0 = nullptr, t1 = nullptr;
-        if (prof) {
-            RAMLT_CUDA(cudaEventCreate(&t0));
-            RAMLT_CUDA(cudaEventCreate(&t1));
-            RAMLT_CUDA(cudaEventRecord(t0, stream_));
+        for (int p = 0; p < npipe; ++p) {
+            const Pipe &pp = pipe[p];
+            unsigned *cnt = pp.cnt;
+            rd::WfParams<R> W;
+            W.c0 = static_cast<unsigned>(pp.c0);
+            W.cn = static_cast<unsigned>(pp.cn);
+            W.trace_work = cnt + 2 * NQ;
+            W.rays = wf_rays_.p + pp.c0 * per_chain;
+            W.hits = wf_hits_.p;
+            W.occ = wf_occ_.p;
+            W.state = wf_state_.p;
+            W.pv = wf_pv_.p;
+            W.cq_in = wf_cq_[a ^ 1].p + pp.c0;
+            W.n_in = cnt + NQ * (a ^ 1);
+            W.cq_out = wf_cq_[a].p + pp.c0;
+            W.n_out = cnt + NQ * a;
+            W.n_rays = cnt + 2 * NQ + 1 + a;
+            if (r == 0 && p == 1)   // out of phase: the second range starts after the first's first logic kernel
+                RAMLT_CUDA(cudaStreamWaitEvent(pp.st, wf_ev_[2], 0));
+            logic<<<pp.lblocks, 128, lsmem, pp.st>>>(PL, W, r == 0 ? 1 : 0);
+            if (r == 0 && p == 0 && npipe > 1)
+                RAMLT_CUDA(cudaEventRecord(wf_ev_[2], pp.st));
+            cudaEvent_t t0 = nullptr, t1 = nullptr;
+            if (prof) {
+                RAMLT_CUDA(cudaEventCreate(&t0));
+                RAMLT_CUDA(cudaEventCreate(&t1));
+                RAMLT_CUDA(cudaEventRecord(t0, pp.st));
+            }
+            // traces this round's rays; zeroes the counters the next round's logic appends to
+            if (use_bvh_)
+                trace<<<pp.tblocks, 128, tsmem, pp.st>>>(P, W.rays, wf_hits_.p, wf_occ_.p, cnt + 2 * NQ + 1 + a,
+                                                          cnt + 2 * NQ, cnt + NQ * (a ^ 1), cnt + 2 * NQ + 1 + (a ^ 1));
+            else
+                trace_brute<<<pp.tblocks, 128, tsmem, pp.st>>>(P, W.rays, wf_hits_.p, wf_occ_.p,
+                                                                cnt + 2 * NQ + 1 + a, cnt + NQ * (a ^ 1),
+                                                                cnt + 2 * NQ + 1 + (a ^ 1));
+            if (prof) {
+                RAMLT_CUDA(cudaEventRecord(t1, pp.st));
+                ev_trace_.emplace_back(t0, t1);
+            }
+            launches_ += 2;
         }
-        // traces this round's rays; zeroes the counters the next round's logic appends to
-        if (use_bvh_)
-            trace<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p, cnt + 2 * NQ + 1 + a,
-                                                     cnt + 2 * NQ, cnt + NQ * (a ^ 1), cnt + 2 * NQ + 1 + (a ^ 1));
-        else
-            trace_brute<<<tblocks, 128, tsmem, stream_>>>(P, wf_rays_.p, wf_hits_.p, wf_occ_.p,
-                                                           cnt + 2 * NQ + 1 + a, cnt + NQ * (a ^ 1),
-                                                           cnt + 2 * NQ + 1 + (a ^ 1));
-        if (prof) {
-            RAMLT_CUDA(cudaEventRecord(t1, stream_));
-            ev_trace_.emplace_back(t0, t1);
-        }
-        launches_ += 2;
         ++wf_rounds_;
         RAMLT_CUDA(cudaGetLastError());
         if (wf_log_) {   // RAMLT_WF_LOG=1: the round's queue lengths (ties an ncu launch to its ray count)
             unsigned hq[16];
-            RAMLT_CUDA(cudaMemcpyAsync(hq, cnt, sizeof(hq), cudaMemcpyDeviceToHost, stream_));
+            RAMLT_CUDA(cudaMemcpyAsync(hq, wf_cnt_.p, sizeof(hq), cudaMemcpyDeviceToHost, stream_));
             RAMLT_CUDA(cudaStreamSynchronize(stream_));
             std::fprintf(stderr, "wf %s round %d: rays %u, chains yielded %u %u %u %u\n", INIT ? "init" : "step", r,
                          hq[2 * NQ + 1 + a], hq[NQ * a], hq[NQ * a + 1], hq[NQ * a + 2], hq[NQ * a + 3]);
@@ -1146,16 +1216,22 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         // one-step launch needs max_vertices + 2 logic rounds: they are enqueued
         // without a host round trip and the queue length is read back once, after
         // the last (a nonzero length -- never seen -- just continues the loop).
-        // Multi-step launches (Fixed strategy) poll every wf_check_ rounds instead.
+        // Multi-step launches (Fixed strategy) and chain initialisation poll every
+        // wf_check_ rounds instead.
         const bool last_planned = !poll && r + 1 >= planned;
         if (last_planned || (poll && r % wf_check_ == wf_check_ - 1)) {
-            RAMLT_CUDA(cudaMemcpyAsync(wf_host_, cnt + NQ * a, NQ * sizeof(unsigned), cudaMemcpyDeviceToHost, stream_));
-            RAMLT_CUDA(cudaStreamSynchronize(stream_));
+            join();
             unsigned left = 0;
-            for (int q = 0; q < NQ; ++q)
-                left += wf_host_[q];
+            for (int p = 0; p < npipe; ++p) {
+                RAMLT_CUDA(cudaMemcpyAsync(wf_host_, pipe[p].cnt + NQ * a, NQ * sizeof(unsigned),
+                                           cudaMemcpyDeviceToHost, stream_));
+                RAMLT_CUDA(cudaStreamSynchronize(stream_));
+                for (int q = 0; q < NQ; ++q)
+                    left += wf_host_[q];
+            }
             if (left == 0)
                 break;
+            fork();
         }
     }
     if (prof) {

@@ -60,6 +60,7 @@ constexpr int kWfQueues = 4;
 __device__ __forceinline__ int wf_queue_of(int pc) { return pc == 1 ? 0 : (pc == 2 ? 1 : (pc == 5 ? 2 : 3)); }
 
 template <class R> struct WfParams {
+    unsigned c0, cn;           // this pipeline's chain range [c0, c0 + cn) (round 0)
     const int *cq_in;          // chains resumed this round (round > 0): sub-queue q at cq_in + q * C
     const unsigned *n_in;      // [kWfQueues]
     int *cq_out;               // chains that yielded this round, by yield point
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
         qn[q] = round0 ? 0u : W.n_in[q];
         qstart[q + 1] = qstart[q] + ((qn[q] + 31u) & ~31u);
     }
-    const unsigned n = round0 ? static_cast<unsigned>(P.C) : qstart[kWfQueues];
+    const unsigned n = round0 ? W.cn : qstart[kWfQueues];
     RayCount rc;
     const unsigned stride = gridDim.x * blockDim.x;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
         WfSink<R> sink{W.rays, W.n_rays, W.occ, 0, 0u};
         int c;
         if (round0 && INIT) {
-            c = static_cast<int>(i);
+            c = static_cast<int>(W.c0 + i);
             s.co.c = c;
             s.co.rng.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(P.chain_off + c) * 2ull);
             s.co.pc = 0;
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
             s.j = 0;
             s.jend = 1;
         } else if (round0) {
-            c = static_cast<int>(i);
+            c = static_cast<int>(W.c0 + i);
             co_load(s.co, P, c);
             const unsigned long long my_steps =
                 P.per + (static_cast<unsigned long long>(P.chain_off + c) < P.rem ? 1ull : 0ull);

@@ -125,6 +125,42 @@ def test_f32_bvh_equals_f32_brute_force(strategy, rng, kernel, monkeypatch):
     np.testing.assert_allclose(iv, ib, rtol=1e-5, atol=1e-6 * float(np.abs(ib).max()))
 
 
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_wavefront_pipelines_equal_single_range(precision, monkeypatch):
+    """RAMLT_WF_PIPES=2: the chains stepped as two wavefront pipelines on two streams
+    (their k_wf_trace / k_wf_logic kernels sharing the SMs) make the decisions of the
+    single pipeline -- per-chain state, order-independent pooled adaptation; with refines."""
+    from paper_2402_08273_b200 import scenes
+    monkeypatch.setenv("RAMLT_STEP_KERNEL", "wf")
+    monkeypatch.setenv("RAMLT_COOP", "0")
+    monkeypatch.setenv("RAMLT_WF_PIPES_MIN", "256")
+    scene = scenes.cluster_room(n_tris=2000, clusters=8, seed=3)
+    C, K = 4096 + 640, 24   # ranges of unequal size
+    out = []
+    for pipes in ("1", "2"):
+        monkeypatch.setenv("RAMLT_WF_PIPES", pipes)
+        eng = _engine(scene, strategy="ra-quadtree", perturbation="lens", chains=C, mutations=C * K, width=128,
+                      height=128, max_vertices=13, b_samples=4096, seed=7, precision=precision, rng="philox",
+                      log_steps=K, adapt_mode="pooled", m_refine=C * 6, m_split=200, accel="bvh",
+                      dump_partition=True)
+        eng.set_b(1.0)
+        eng.init_chains()
+        eng.run(C * K)
+        a, f = eng.decisions(K)
+        out.append((a, f, eng.image(), eng.trace(), eng.partition_dump(), eng.stats()))
+        eng.close()
+    (a1, f1, i1, t1, d1, s1), (a2, f2, i2, t2, d2, s2) = out
+    assert np.array_equal(f1, f2), np.argwhere(f1 != f2)[:5]
+    np.testing.assert_array_equal(a1, a2)
+    np.testing.assert_array_equal(t1, t2)
+    assert d1 == d2
+    assert s1.region_count == s2.region_count > 1
+    assert s1.rays_closest + s1.rays_visibility == s2.rays_closest + s2.rays_visibility
+    # the film is a sum of atomics (fp32 staging in the f32 build): order-dependent rounding only
+    np.testing.assert_allclose(i2, i1, rtol=1e-4 if precision == "f32" else 1e-9,
+                               atol=1e-6 * float(np.abs(i1).max()))
+
+
 def _bench_like(scene, seed, precision, chains, steps, b):
     """bench.py's c4 configuration (f32 default; f64 = parity build) at 1024^2."""
     eng = _engine(scene, strategy="ra-quadtree", perturbation="lens", chains=chains, mutations=chains * steps,
