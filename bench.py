@@ -651,8 +651,14 @@ def main():
         # algorithmic bytes are this rank's device rays x B_ray over its summed
         # launch time (the chain-state traffic belongs to k_wf_logic)
         ach = res["rays_local"] * b_ray / (res["trace_ms"] / 1e3) / 1e9
+        rays_per_launch = res["rays_local"] / max(res["trace_launches"], 1)
+        wf_traffic = None
+        try:   # ncu --set full of one k_wf_trace launch with a known ray count (profiles/traffic_<workload>.json)
+            wf_traffic = json.load(open(tpath))["k_wf_trace"]["dram_bytes_per_ray"] * rays_per_launch
+        except Exception:
+            wf_traffic = None
         roofline.update({
-            "achieved": ach, "frac": ach / peak,
+            "achieved": ach, "frac": ach / peak, "traffic": wf_traffic,
             "work_per_unit": f"B_ray = {levels} BVH levels x 64 B + 4 x 48 B = {b_ray:.0f} B per device ray "
                              f"(SURVEY.md §8(d) per-ray term); {res['rays_local'] / max(res['trace_launches'], 1):.0f} "
                              f"rays per launch on average",

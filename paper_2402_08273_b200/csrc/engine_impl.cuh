@@ -1093,7 +1093,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     auto trace = rd::k_wf_trace<R>;
     auto trace_brute = rd::k_wf_trace_brute<R>;
     size_t lsmem = smem_;
-    size_t tsmem = (smem_ + 15) & ~size_t(15);
+    size_t tsmem = (smem_ + 31) & ~size_t(31);   // the coroutine states are moved as 32 B sectors
     rd::StepParams<R> PL = P;   // k_wf_logic's parameters: co_stack_off = its shared-memory coroutine states
 #if RAMLT_WF_SMEM
     PL.co_stack_off = static_cast<unsigned>(tsmem);

@@ -137,6 +137,7 @@ struct NoSink {
     __device__ __forceinline__ void null(unsigned) const {}
     __device__ __forceinline__ void begin_batch() const {}
     __device__ __forceinline__ bool occluded(int) const { return false; }
+    __device__ __forceinline__ void cold() const {}
 };
 
 #define CO_RAY(O, D, LIM, N)                                                                       \
@@ -166,21 +167,28 @@ template <class R> struct ChainCo {
 };
 
 template <class R, int RK, bool INIT = false> struct StepCo {
-    // ---- chain (persists over the chain's steps) ----
+    // ---- hot: everything the large-step bounce loop (yield point 2) reads or writes.
+    // The wavefront step (ramlt_wavefront.cuh) moves only these leading sectors for a
+    // chain resumed in that loop and fetches the rest when the chain leaves it.
     int c;
-    ChainCo<R> cs;
-    Rng<RK> rng;
-    // ---- coroutine ----
     int pc;
+    int wf_j, wf_jend;              // wavefront: the chain's step cursor within the launch
+    Rng<RK> rng;
     RayReq<R> ray;
     int res_prim;   // -1 miss / visible
     R res_t;
-    // ---- per-step state ----
+    R dpdf;
+    int kp;
+    unsigned smp;
+    double tf;                      // transition densities and acceptance: fp64 in every build
     bool choose, ok, accepted, pert_rec;
-    R s_pert, dpdf;
-    double tf, tr, a;   // transition densities and acceptance: fp64 in every build
-    int endpoint, first, idx, next, i, region, kp, head_end;
-    unsigned pmask, m, smp;
+    unsigned attempts;              // INIT (init_attempts < 2^32)
+    // ---- cold (32-byte aligned: no sector holds both hot and cold fields) ----
+    alignas(32) ChainCo<R> cs;      // chain state that persists over the chain's steps
+    R s_pert;
+    double tr, a;
+    int endpoint, first, idx, next, i, region, head_end;
+    unsigned pmask, m;
     V3<R> o, d;
     Contrib<R> pcb;
     // evaluate / eye density sub-state
@@ -188,7 +196,6 @@ template <class R, int RK, bool INIT = false> struct StepCo {
     double ep;
     R eseg;
     int ek, ei;
-    unsigned attempts;             // INIT (init_attempts < 2^32)
 
     template <class Sink = NoSink>
     __device__ __forceinline__ int advance(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
@@ -436,6 +443,8 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
         while (kp < P.maxv) {
             ++rc.c;
             CO_RAY(o, d, M<R>::inf(), 2);
+            o = ray.o;   // o, d are cold: a chain resumed here may hold the hot fields only
+            d = ray.d;
             {
                 if (res_prim < 0)
                     break;
@@ -477,6 +486,7 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
                 dpdf = bs.pdf;
             }
         }
+        sink.cold();   // leaving the bounce loop: the rest of the state is needed from here on
         if (!ok)
             goto finish;
         head_end = kp - 1;

@@ -46,9 +46,11 @@ template <class R> struct alignas(sizeof(R) * 2) WfHit {
 };
 
 // Coroutine state carried between rounds.
-template <class R, int RK, bool INIT = false> struct WfState {
-    StepCo<R, RK, INIT> co;
-    int j, jend;
+template <class R, int RK, bool INIT = false> struct alignas(32) WfState {
+    StepCo<R, RK, INIT> co;   // its step cursor: co.wf_j, co.wf_jend
+    // Sectors [0, HOT) hold the fields the large-step bounce loop uses (StepCo's
+    // leading members); a chain resumed in that loop moves only those.
+    static constexpr int HOT = static_cast<int>((__builtin_offsetof(StepCo<R, RK, INIT>, cs) + 31) / 32);
 };
 
 // Chain queues are kept per yield point (kWfQueues sub-queues of capacity C each:
@@ -82,6 +84,13 @@ template <class R> struct WfSink {
     unsigned *occ_g;
     int c;
     unsigned occ;   // answers of the batch this chain is resumed from
+    // hot/cold state: where the chain's cold sectors are and whether they are resident
+    const uint4 *state;
+    size_t C;
+    char *resident;      // the thread's coroutine state (shared memory)
+    int *full;           // != 0: every sector is resident
+    int hot, total;      // sectors
+    __device__ __forceinline__ void cold() const;
     // n slots per calling lane: one atomic for the lanes converged here
     __device__ __forceinline__ unsigned reserve(unsigned n) const {
         const unsigned act = __activemask();
@@ -119,6 +128,13 @@ template <class R> struct WfSink {
     __device__ __forceinline__ void begin_batch() const { occ_g[c] = 0u; }
     __device__ __forceinline__ bool occluded(int k) const { return (occ >> k) & 1u; }
 };
+
+// RAMLT_WF_HOTCOLD=1 (default): chains resumed in the large-step bounce loop -- half of
+// all mutations, ~11 rounds each, nearly all of them ending without a contribution --
+// load and store only the hot sectors of their state (4 of 10 in fp32).
+#ifndef RAMLT_WF_HOTCOLD
+#define RAMLT_WF_HOTCOLD 1
+#endif
 
 // State chunks are whole 32 B sectors moved with 256-bit evict-first loads / stores
 // (LDG/STG.E.EF.ENL2.256): a chain's chunk never shares a sector with its neighbour's,
@@ -191,12 +207,30 @@ template <class T> __device__ __forceinline__ void st_state(const T &v, uint4 *_
 #endif
 }
 
+// Sectors [k0, k1) of a state image (32 B aligned, a whole number of sectors long).
+__device__ __forceinline__ void ld_sectors(char *dst, const uint4 *__restrict__ base, size_t C, int c, int k0, int k1) {
+    const Sector *p = reinterpret_cast<const Sector *>(base);
+    for (int k = k0; k < k1; ++k)
+        *reinterpret_cast<Sector *>(dst + 32 * k) = ld_sector_cs(p + static_cast<size_t>(k) * C + c);
+}
+__device__ __forceinline__ void st_sectors(const char *src, uint4 *__restrict__ base, size_t C, int c, int k0, int k1) {
+    Sector *p = reinterpret_cast<Sector *>(base);
+    for (int k = k0; k < k1; ++k)
+        st_sector_cs(p + static_cast<size_t>(k) * C + c, *reinterpret_cast<const Sector *>(src + 32 * k));
+}
+template <class R> __device__ __forceinline__ void WfSink<R>::cold() const {
+    if (!*full) {
+        ld_sectors(resident, state, C, c, hot, total);
+        *full = 1;
+    }
+}
+
 // INIT: chain initialisation (core/driver.cpp:219-242) instead of a step -- the
 // coroutine draws large-step eye paths from the chain's init stream until one
 // contributes and stores the chain itself; rounds run until every chain has one.
 template <class R, int RK, bool INIT = false>
 __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) k_wf_logic(StepParams<R> P, WfParams<R> W, int round0) {
-    extern __shared__ __align__(16) char smem[];
+    extern __shared__ __align__(32) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         *W.trace_work = 0;
@@ -217,7 +251,11 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
 #else
         WfState<R, RK, INIT> s;
 #endif
-        WfSink<R> sink{W.rays, W.n_rays, W.occ, 0, 0u};
+        using St = WfState<R, RK, INIT>;
+        constexpr int TOTAL = static_cast<int>(sizeof(St) / 32);
+        int full = 1;   // every sector of the state is resident
+        WfSink<R> sink{W.rays, W.n_rays, W.occ, 0, 0u, W.state, static_cast<size_t>(P.C),
+                       reinterpret_cast<char *>(&s), &full, St::HOT, TOTAL};
         int c;
         if (round0 && INIT) {
             c = static_cast<int>(W.c0 + i);
@@ -225,16 +263,16 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
             s.co.rng.reseed(P.seed, kStreamInit + static_cast<unsigned long long>(P.chain_off + c) * 2ull);
             s.co.pc = 0;
             s.co.attempts = 0;
-            s.j = 0;
-            s.jend = 1;
+            s.co.wf_j = 0;
+            s.co.wf_jend = 1;
         } else if (round0) {
             c = static_cast<int>(W.c0 + i);
             co_load(s.co, P, c);
             const unsigned long long my_steps =
                 P.per + (static_cast<unsigned long long>(P.chain_off + c) < P.rem ? 1ull : 0ull);
-            s.j = P.j0;
-            s.jend = static_cast<int>(min(static_cast<unsigned long long>(P.j1), my_steps));
-            if (s.j >= s.jend) {   // inactive for this launch
+            s.co.wf_j = P.j0;
+            s.co.wf_jend = static_cast<int>(min(static_cast<unsigned long long>(P.j1), my_steps));
+            if (s.co.wf_j >= s.co.wf_jend) {   // inactive for this launch
                 if (P.record_visits)
                     P.ch.vreg[c] = -1;
                 continue;
@@ -248,17 +286,28 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
             if (k >= qn[q])   // padding of this queue's last warp
                 continue;
             c = W.cq_in[static_cast<size_t>(q) * P.C + k];
+#if RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32
+            if (q == 1) {   // in the large-step bounce loop: the hot sectors only
+                ld_sectors(reinterpret_cast<char *>(&s), W.state, static_cast<size_t>(P.C), c, 0, St::HOT);
+                full = 0;
+            } else {
+                ld_sectors(reinterpret_cast<char *>(&s), W.state, static_cast<size_t>(P.C), c, 0, TOTAL);
+            }
+#else
             ld_state(s, W.state, static_cast<size_t>(P.C), c);
-            const WfHit<R> h = W.hits[c];
-            s.co.res_prim = h.prim;
-            s.co.res_t = h.t;
-            sink.occ = W.occ[c];
+#endif
+            if (q < 2) {   // a closest-hit yield: its answer
+                const WfHit<R> h = W.hits[c];
+                s.co.res_prim = h.prim;
+                s.co.res_t = h.t;
+            }
+            sink.occ = q >= 2 ? W.occ[c] : 0u;   // only the batch yields have occlusion answers
         }
         sink.c = c;
         const PvSmem<R> pv{W.pv + c, P.C};
         for (;;) {
             const unsigned long long index =
-                P.span_start + static_cast<unsigned long long>(s.j) * P.C_total + P.chain_off + c;
+                P.span_start + static_cast<unsigned long long>(s.co.wf_j) * P.C_total + P.chain_off + c;
             if (s.co.advance(P, S, pv, rc, index, sink) == CO_RAY_PENDING) {
                 const unsigned act = __activemask();
                 const int q = wf_queue_of(s.co.pc);
@@ -269,12 +318,18 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
                     base = atomicAdd(W.n_out + q, static_cast<unsigned>(__popc(grp)));
                 base = __shfl_sync(grp, base, leader);
                 W.cq_out[static_cast<size_t>(q) * P.C + base + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u))] = c;
+#if RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32
+                // still in the bounce loop it was resumed in: the cold sectors in HBM are current
+                st_sectors(reinterpret_cast<const char *>(&s), W.state, static_cast<size_t>(P.C), c, 0,
+                           full ? TOTAL : St::HOT);
+#else
                 st_state(s, W.state, static_cast<size_t>(P.C), c);
+#endif
                 break;
             }
             if (INIT)   // the coroutine stored the chain
                 break;
-            if (++s.j >= s.jend) {
+            if (++s.co.wf_j >= s.co.wf_jend) {
                 co_store(s.co, P);
                 break;
             }
