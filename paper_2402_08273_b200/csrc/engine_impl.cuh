@@ -208,6 +208,7 @@ private:
     int wf_refill_ = 8;       // k_wf_trace: RAMLT_WF_REFILL idle lanes end a traversal round
     int wf_check_ = 4;        // rounds between host checks of the queue length (RAMLT_WF_CHECK)
     bool wf_log_ = false;     // RAMLT_WF_LOG=1
+    bool wf_bounce_ = false;  // RAMLT_WF_BOUNCE=1: the large-step bounce loop in its own kernel (k_wf_bounce)
     int wf_pipes_ = 1;        // RAMLT_WF_PIPES: chain ranges stepped as concurrent wavefront pipelines
     size_t wf_pipes_min_ = size_t(1) << 18;   // RAMLT_WF_PIPES_MIN: fewest chains split into pipelines
     int wf_lblk_ = 0, wf_tblk_ = 0;   // RAMLT_WF_LBLK / RAMLT_WF_TBLK: resident blocks per SM of a pipeline's kernels
@@ -477,6 +478,8 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
         wf_refill_ = std::min(32, std::max(1, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_WF_LOG"))
         wf_log_ = std::string(v) == "1";
+    if (const char *v = std::getenv("RAMLT_WF_BOUNCE"))
+        wf_bounce_ = std::string(v) == "1";
     if (const char *v = std::getenv("RAMLT_WF_PIPES"))
         wf_pipes_ = std::min(2, std::max(1, std::atoi(v)));
     if (const char *v = std::getenv("RAMLT_WF_PIPES_MIN"))
@@ -1106,7 +1109,10 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
                               : prepare(reinterpret_cast<const void *>(trace_brute), tsmem);
     // chain initialisation runs until every chain found a contributing path: polled
     const bool poll = INIT || P.j1 - P.j0 > 1 || wf_poll_;
-    const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2;
+    // RAMLT_WF_BOUNCE=1: the bounce queue is resumed by k_wf_bounce (one more round: the
+    // chains it takes out of the loop pass through the post-loop queue)
+    const bool bounce_sep = !INIT && wf_bounce_ && rd::WfCompact<R, RK, INIT>::OK;
+    const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2 + (bounce_sep ? 1 : 0);
     // Pipelines: the chains of a one-step launch are cut into wf_pipes_ contiguous ranges,
     // each with its own queues and counters, and the ranges' rounds are enqueued on
     // separate streams.  k_wf_trace is bound by instruction issue and k_wf_logic by
@@ -1122,8 +1128,14 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         cudaStream_t st;
         unsigned *cnt;   // chain-queue lengths [0..3] / [4..7] (ping-pong, one per yield point), trace
                          // work counter [8], ray-queue lengths [9] / [10]
-        unsigned lblocks, tblocks;
+        unsigned lblocks, tblocks, bblocks;
     } pipe[2];
+    const size_t bsmem = (smem_ + 31) & ~size_t(31);
+    int bper = 1;
+    if constexpr (!INIT) {
+        if (bounce_sep)
+            bper = prepare(reinterpret_cast<const void *>(rd::k_wf_bounce<R, RK>), bsmem);
+    }
     for (int p = 0; p < npipe; ++p) {
         Pipe &pp = pipe[p];
         pp.c0 = npipe == 1 ? 0 : (p == 0 ? 0 : ((C / 2 + 127) & ~size_t(127)));
@@ -1134,6 +1146,8 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         const int tb = npipe == 1 ? std::max(tper, 1) : std::max(1, wf_tblk_ > 0 ? wf_tblk_ : tper / 2);
         pp.lblocks = std::min<unsigned>(static_cast<unsigned>((pp.cn + 127) / 128), static_cast<unsigned>(lb * sms_));
         pp.tblocks = static_cast<unsigned>(tb * sms_);
+        pp.bblocks = std::min<unsigned>(static_cast<unsigned>((pp.cn + 127) / 128),
+                                        static_cast<unsigned>(std::max(1, npipe == 1 ? bper : bper / 2) * sms_));
     }
     RAMLT_CUDA(cudaMemsetAsync(wf_cnt_.p, 0, 32 * sizeof(unsigned), stream_));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1164,6 +1178,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
             const Pipe &pp = pipe[p];
             unsigned *cnt = pp.cnt;
             rd::WfParams<R> W;
+            W.bounce_sep = bounce_sep ? 1 : 0;
             W.c0 = static_cast<unsigned>(pp.c0);
             W.cn = static_cast<unsigned>(pp.cn);
             W.trace_work = cnt + 2 * NQ;
@@ -1180,6 +1195,12 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
             if (r == 0 && p == 1)   // out of phase: the second range starts after the first's first logic kernel
                 RAMLT_CUDA(cudaStreamWaitEvent(pp.st, wf_ev_[2], 0));
             logic<<<pp.lblocks, 128, lsmem, pp.st>>>(PL, W, r == 0 ? 1 : 0);
+            if constexpr (!INIT) {
+                if (bounce_sep && r > 0) {
+                    rd::k_wf_bounce<R, RK><<<pp.bblocks, 128, bsmem, pp.st>>>(P, W);
+                    ++launches_;
+                }
+            }
             if (r == 0 && p == 0 && npipe > 1)
                 RAMLT_CUDA(cudaEventRecord(wf_ev_[2], pp.st));
             cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -1208,8 +1229,8 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
             unsigned hq[16];
             RAMLT_CUDA(cudaMemcpyAsync(hq, wf_cnt_.p, sizeof(hq), cudaMemcpyDeviceToHost, stream_));
             RAMLT_CUDA(cudaStreamSynchronize(stream_));
-            std::fprintf(stderr, "wf %s round %d: rays %u, chains yielded %u %u %u %u\n", INIT ? "init" : "step", r,
-                         hq[2 * NQ + 1 + a], hq[NQ * a], hq[NQ * a + 1], hq[NQ * a + 2], hq[NQ * a + 3]);
+            std::fprintf(stderr, "wf %s round %d: rays %u, chains yielded %u %u %u %u %u\n", INIT ? "init" : "step", r,
+                         hq[2 * NQ + 1 + a], hq[NQ * a], hq[NQ * a + 1], hq[NQ * a + 2], hq[NQ * a + 3], hq[NQ * a + 4]);
         }
         // A mutation yields at most max_vertices + 1 times (max_vertices - 1 closest-hit
         // rays, the eval_contribution batch, the eye_path_density batch), so a

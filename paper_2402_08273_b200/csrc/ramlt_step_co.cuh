@@ -152,6 +152,57 @@ struct NoSink {
     case (N):;                                                                                     \
     } while (0)
 
+// One iteration of trace_eye_subpath's loop (path.cpp:84-142) once the closest hit of the
+// pending ray is known: record the vertex, extend the transition density, sample the
+// continuation.  Returns true when the path continues with the ray (o, d); false when the
+// loop ends (miss, emitter reached -- ok --, path capacity, no continuation).  Shared by the
+// coroutine (StepCo::advance) and the wavefront's bounce kernel (k_wf_bounce).
+template <class R, int RK>
+__device__ __forceinline__ bool bounce_body(const StepParams<R> &P, const SceneView<R> &S, const PvSmem<R> &pv,
+                                            const RayReq<R> &ray, int res_prim, R res_t, Rng<RK> &rng, R &dpdf,
+                                            int &kp, unsigned &smp, double &tf, bool &ok, V3<R> &o, V3<R> &d) {
+    d = ray.d;
+    if (res_prim < 0)
+        return false;
+    Hit<R> h;
+    hit_record(S, ray, res_prim, res_t, h);
+    const MatD<R> mt = S.mat[h.mat];
+    Vx<R> x;
+    x.p = h.p;
+    x.n = h.n;
+    x.mat = h.mat;
+    x.emi = h.emi;
+    x.spec = h.emi < 0 && (mt.kind == MAT_MIRROR || mt.kind == MAT_DIELECTRIC);
+    x.ev = EV_NONE;
+    tf *= static_cast<double>(dpdf * (M<R>::abs(dot(h.n, d)) / (h.t * h.t)));
+    if (x.spec)
+        smp |= 1u << kp;
+    if (h.emi >= 0) {
+        pv.set(kp, x);
+        ++kp;
+        ok = true;
+        return false;
+    }
+    if (kp + 1 >= P.maxv) {
+        pv.set(kp, x);
+        ++kp;
+        return false;
+    }
+    BS<R> bs;
+    if (!bsdf_sample(mt, neg(d), h.n, rng, bs) || bs.zero_thr) {
+        pv.set(kp, x);
+        ++kp;
+        return false;
+    }
+    x.ev = bs.ev;
+    pv.set(kp, x);
+    ++kp;
+    o = h.p;
+    d = bs.dir;
+    dpdf = bs.pdf;
+    return true;
+}
+
 // INIT: the same coroutine runs chain initialisation (core/driver.cpp:219-242):
 // large-step eye paths from the chain's init stream until one has a nonzero
 // contribution, then the chain's state is written (as init_chain does).
@@ -443,49 +494,12 @@ __device__ __forceinline__ int StepCo<R, RK, INIT>::advance(const StepParams<R> 
         while (kp < P.maxv) {
             ++rc.c;
             CO_RAY(o, d, M<R>::inf(), 2);
-            o = ray.o;   // o, d are cold: a chain resumed here may hold the hot fields only
-            d = ray.d;
-            {
-                if (res_prim < 0)
-                    break;
-                Hit<R> h;
-                hit_record(S, ray, res_prim, res_t, h);
-                const MatD<R> mt = S.mat[h.mat];
-                Vx<R> x;
-                x.p = h.p;
-                x.n = h.n;
-                x.mat = h.mat;
-                x.emi = h.emi;
-                x.spec = h.emi < 0 && (mt.kind == MAT_MIRROR || mt.kind == MAT_DIELECTRIC);
-                x.ev = EV_NONE;
-                tf *= static_cast<double>(dpdf * (M<R>::abs(dot(h.n, d)) / (h.t * h.t)));
-                if (x.spec)
-                    smp |= 1u << kp;
-                if (h.emi >= 0) {
-                    pv.set(kp, x);
-                    ++kp;
-                    ok = true;
-                    break;
-                }
-                if (kp + 1 >= P.maxv) {
-                    pv.set(kp, x);
-                    ++kp;
-                    break;
-                }
-                BS<R> bs;
-                if (!bsdf_sample(mt, neg(d), h.n, rng, bs) || bs.zero_thr) {
-                    pv.set(kp, x);
-                    ++kp;
-                    break;
-                }
-                x.ev = bs.ev;
-                pv.set(kp, x);
-                ++kp;
-                o = h.p;
-                d = bs.dir;
-                dpdf = bs.pdf;
-            }
+            // (o, d are cold: a chain resumed here may hold the hot fields only; the body
+            // takes the incoming direction from the ray)
+            if (!bounce_body<R, RK>(P, S, pv, ray, res_prim, res_t, rng, dpdf, kp, smp, tf, ok, o, d))
+                break;
         }
+    case 7:   // wavefront: the loop ran in k_wf_bounce, the chain resumes behind it
         sink.cold();   // leaving the bounce loop: the rest of the state is needed from here on
         if (!ok)
             goto finish;

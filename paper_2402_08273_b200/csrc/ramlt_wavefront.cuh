@@ -1,30 +1,39 @@
-// ramlt_wavefront.cuh -- the chain step as a wavefront (BVH scenes).
+// ramlt_wavefront.cuh -- the chain step as a wavefront (the default for BVH scenes).
 //
 // The mutation of core/driver.cpp:113-171 is the resumable coroutine StepCo
 // (ramlt_step_co.cuh).  Instead of tracing inside the coroutine kernel, a
-// lockstep step alternates two kernels until no chain has a ray pending:
+// lockstep step alternates kernels until no chain has a ray pending:
 //
-//   k_wf_logic  one thread per chain that yielded (compacted chain queue):
-//               resume the coroutine with its answer, advance it to its next
-//               yield (or the end of its step); its rays go into the round's
-//               ray queue and the chain into the next chain queue, both with
-//               warp-aggregated atomics.  A yield is one closest-hit ray
-//               (retrace, large-step bounce) or ALL the visibility rays of
-//               eval_contribution / eye_path_density at once (they do not
-//               depend on each other), so a mutation takes ~closest-hit rays
-//               + 2 rounds instead of one round per ray;
+//   k_wf_logic  one thread per chain that yielded: resume the coroutine with
+//               its answer, advance it to its next yield (or the end of its
+//               step); its rays go into the round's ray queue and the chain
+//               into the next round's chain queue, with warp-aggregated
+//               atomics.  A yield is one closest-hit ray (retrace, large-step
+//               bounce) or ALL the visibility rays of eval_contribution /
+//               eye_path_density at once (they do not depend on each other),
+//               so a mutation takes ~closest-hit rays + 2 rounds.  Chains are
+//               queued per yield point and every queue is resumed from a warp
+//               boundary: a warp's lanes resume at the same point;
+//   k_wf_bounce (RAMLT_WF_BOUNCE=1) the large-step bounce loop -- half of all
+//               mutations, ~11 rounds each -- resumed by a small kernel from
+//               the chain's compact image (bounce_body, the coroutine's own
+//               loop body);
 //   k_wf_trace  persistent, one ray per lane, dynamic ray fetch and
 //               while-while BVH rounds over the queue, writing (t, prim) by
 //               chain for closest hits and OR-ing bit k of the chain's
-//               occlusion mask for an occluded visibility ray k.
+//               occlusion mask for an occluded visibility ray k
+//               (k_wf_trace_brute: the shared-memory linear scan instead).
 //
-// Between rounds the coroutine state lives in HBM as 16-byte chunks indexed
-// [chunk][chain] (coalesced vectorised loads/stores); the proposal vertices
-// live in a [vertex][chain] array.  The trace kernel carries no mutation
-// state, so it runs with far fewer registers and more warps than the fused
-// coroutine kernel, and every warp of it holds rays, whatever phase each
-// chain is in.  Arithmetic and RNG consumption are the coroutine's, so the
-// results equal k_step_co's (and the fp64/PCG build the reference's).
+// Between rounds the coroutine state lives in HBM as whole 32-byte sectors
+// indexed [sector][chain] (256-bit evict-first loads / stores); a chain inside
+// the bounce loop moves only a compact image of the loop's live values (2
+// sectors in fp32 / Philox) and fetches the cold sectors when it leaves the
+// loop.  The proposal vertices live in a [vertex][chain] array.  The trace
+// kernel carries no mutation state, so it runs with far fewer registers and
+// more warps than the fused coroutine kernel, and every warp of it holds rays,
+// whatever phase each chain is in.  Arithmetic and RNG consumption are the
+// coroutine's, so the results equal k_step_co's (and the fp64/PCG build the
+// reference's).
 #pragma once
 
 #include "ramlt_step_co.cuh"
@@ -58,11 +67,16 @@ template <class R, int RK, bool INIT = false> struct alignas(32) WfState {
 // and a round resumes them queue by queue with every queue's segment starting on a
 // warp boundary: the lanes of a warp resume at the same point of the coroutine
 // instead of at four different ones.
-constexpr int kWfQueues = 4;
-__device__ __forceinline__ int wf_queue_of(int pc) { return pc == 1 ? 0 : (pc == 2 ? 1 : (pc == 5 ? 2 : 3)); }
+// A fifth queue holds the chains k_wf_bounce took out of the bounce loop: k_wf_logic resumes
+// them behind the loop (yield point 7) in the next round.
+constexpr int kWfQueues = 5;
+__device__ __forceinline__ int wf_queue_of(int pc) {
+    return pc == 1 ? 0 : (pc == 2 ? 1 : (pc == 5 ? 2 : (pc == 6 ? 3 : 4)));
+}
 
 template <class R> struct WfParams {
     unsigned c0, cn;           // this pipeline's chain range [c0, c0 + cn) (round 0)
+    int bounce_sep;            // != 0: the bounce queue (1) belongs to k_wf_bounce, not to k_wf_logic
     const int *cq_in;          // chains resumed this round (round > 0): sub-queue q at cq_in + q * C
     const unsigned *n_in;      // [kWfQueues]
     int *cq_out;               // chains that yielded this round, by yield point
@@ -225,6 +239,110 @@ template <class R> __device__ __forceinline__ void WfSink<R>::cold() const {
     }
 }
 
+// Compact image of a chain inside the large-step bounce loop (steps, not INIT): the
+// loop's live values in 2 sectors (fp32 / Philox) instead of the 4 hot ones -- the pending ray (its lim is
+// +inf), the Philox draw counter (key and stream follow from the seed and the chain id; the
+// cached block is recomputed from the counter, the same words), tf, dpdf, the specular mask,
+// kp, the four flags and the step cursor.  It lives in sectors 0-1 of the chain's state; the
+// cold sectors keep their place.  RAMLT_WF_COMPACT=0: the 4 raw hot sectors.
+#ifndef RAMLT_WF_COMPACT
+#define RAMLT_WF_COMPACT 1
+#endif
+template <int RK> struct WfRngSave;
+template <> struct WfRngSave<RNG_PHILOX> {
+    unsigned long long draw;
+    __device__ __forceinline__ void save(const Rng<RNG_PHILOX> &r) { draw = r.draw; }
+    template <class R> __device__ __forceinline__ void restore(Rng<RNG_PHILOX> &r, const StepParams<R> &P, int c) const {
+        r.reseed(P.seed, static_cast<unsigned long long>(P.chain_off + c));
+        r.draw = draw;
+    }
+};
+template <> struct WfRngSave<RNG_PCG> {
+    unsigned long long state, inc;
+    __device__ __forceinline__ void save(const Rng<RNG_PCG> &r) { state = r.state, inc = r.inc; }
+    template <class R> __device__ __forceinline__ void restore(Rng<RNG_PCG> &r, const StepParams<R> &, int) const {
+        r.state = state, r.inc = inc;
+    }
+};
+// The image: 64 B (2 sectors) in fp32 / Philox, 72 B (3) in fp32 / PCG, 96-104 B (3-4) in fp64.
+template <class R, int RK> struct WfBounceImage {
+    double tf;
+    WfRngSave<RK> rng;
+    R o[3], d[3];
+    R dpdf;
+    unsigned smp;
+    unsigned kp_flags;   // kp | choose << 8 | ok << 9 | accepted << 10 | pert_rec << 11
+    int j, jend;
+};
+// The members of StepCo the image restores, for k_wf_bounce (no cold part, no coroutine).
+template <class R, int RK> struct WfBounceRegs {
+    int c, pc, wf_j, wf_jend;
+    Rng<RK> rng;
+    RayReq<R> ray;
+    R dpdf;
+    int kp;
+    unsigned smp;
+    double tf;
+    bool choose, ok, accepted, pert_rec;
+    unsigned attempts;
+};
+template <class R, int RK, bool INIT> struct WfCompact {
+    static constexpr bool OK = !INIT && RAMLT_WF_COMPACT && RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32;
+    using Img = WfBounceImage<R, RK>;
+    static constexpr int N = static_cast<int>((sizeof(Img) + 31) / 32);   // sectors
+    struct alignas(32) Buf {
+        Sector w[N];
+    };
+    template <class CoT> static __device__ __forceinline__ void pack(const CoT &co, Buf &buf) {
+        Img im;
+        im.tf = co.tf;
+        im.rng.save(co.rng);
+        im.o[0] = co.ray.o.x, im.o[1] = co.ray.o.y, im.o[2] = co.ray.o.z;
+        im.d[0] = co.ray.d.x, im.d[1] = co.ray.d.y, im.d[2] = co.ray.d.z;
+        im.dpdf = co.dpdf;
+        im.smp = co.smp;
+        im.kp_flags = static_cast<unsigned>(co.kp) | (co.choose ? 0x100u : 0u) | (co.ok ? 0x200u : 0u) |
+                      (co.accepted ? 0x400u : 0u) | (co.pert_rec ? 0x800u : 0u);
+        im.j = co.wf_j;
+        im.jend = co.wf_jend;
+        memcpy(&buf, &im, sizeof(Img));
+    }
+    template <class CoT>
+    static __device__ __forceinline__ void unpack(CoT &co, const Buf &buf, int c, const StepParams<R> &P) {
+        Img im;
+        memcpy(&im, &buf, sizeof(Img));
+        co.c = c;
+        co.pc = 2;
+        co.ray.o = mk(im.o[0], im.o[1], im.o[2]);
+        co.ray.d = mk(im.d[0], im.d[1], im.d[2]);
+        co.ray.lim = M<R>::inf();
+        im.rng.restore(co.rng, P, c);
+        co.tf = im.tf;
+        co.dpdf = im.dpdf;
+        co.smp = im.smp;
+        co.kp = static_cast<int>(im.kp_flags & 0xffu);
+        co.choose = (im.kp_flags & 0x100u) != 0;
+        co.ok = (im.kp_flags & 0x200u) != 0;
+        co.accepted = (im.kp_flags & 0x400u) != 0;
+        co.pert_rec = (im.kp_flags & 0x800u) != 0;
+        co.wf_j = im.j;
+        co.wf_jend = im.jend;
+        co.attempts = 0;
+    }
+    static __device__ __forceinline__ void load(Buf &buf, const uint4 *__restrict__ state, size_t C, int c) {
+        const Sector *sp = reinterpret_cast<const Sector *>(state);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            buf.w[k] = ld_sector_cs(sp + static_cast<size_t>(k) * C + c);
+    }
+    static __device__ __forceinline__ void store(const Buf &buf, uint4 *__restrict__ state, size_t C, int c) {
+        Sector *sp = reinterpret_cast<Sector *>(state);
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            st_sector_cs(sp + static_cast<size_t>(k) * C + c, buf.w[k]);
+    }
+};
+
 // INIT: chain initialisation (core/driver.cpp:219-242) instead of a step -- the
 // coroutine draws large-step eye paths from the chain's init stream until one
 // contributes and stores the chain itself; rounds run until every chain has one.
@@ -239,7 +357,7 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
     qstart[0] = 0;
 #pragma unroll
     for (int q = 0; q < kWfQueues; ++q) {
-        qn[q] = round0 ? 0u : W.n_in[q];
+        qn[q] = (round0 || (q == 1 && W.bounce_sep)) ? 0u : W.n_in[q];
         qstart[q + 1] = qstart[q] + ((qn[q] + 31u) & ~31u);
     }
     const unsigned n = round0 ? W.cn : qstart[kWfQueues];
@@ -253,6 +371,7 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
 #endif
         using St = WfState<R, RK, INIT>;
         constexpr int TOTAL = static_cast<int>(sizeof(St) / 32);
+        static_assert(WfCompact<R, RK, INIT>::N <= St::HOT, "the compact image must not reach the cold sectors");
         int full = 1;   // every sector of the state is resident
         WfSink<R> sink{W.rays, W.n_rays, W.occ, 0, 0u, W.state, static_cast<size_t>(P.C),
                        reinterpret_cast<char *>(&s), &full, St::HOT, TOTAL};
@@ -287,7 +406,14 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
                 continue;
             c = W.cq_in[static_cast<size_t>(q) * P.C + k];
 #if RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32
-            if (q == 1) {   // in the large-step bounce loop: the hot sectors only
+            if ((q == 1 || q == 4) && WfCompact<R, RK, INIT>::OK) {   // in (4: just behind) the large-step bounce loop: the compact image
+                typename WfCompact<R, RK, INIT>::Buf buf;
+                WfCompact<R, RK, INIT>::load(buf, W.state, static_cast<size_t>(P.C), c);
+                WfCompact<R, RK, INIT>::unpack(s.co, buf, c, P);
+                if (q == 4)
+                    s.co.pc = 7;
+                full = 0;
+            } else if (q == 1) {   // ... or the hot sectors only
                 ld_sectors(reinterpret_cast<char *>(&s), W.state, static_cast<size_t>(P.C), c, 0, St::HOT);
                 full = 0;
             } else {
@@ -320,8 +446,18 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
                 W.cq_out[static_cast<size_t>(q) * P.C + base + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u))] = c;
 #if RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32
                 // still in the bounce loop it was resumed in: the cold sectors in HBM are current
-                st_sectors(reinterpret_cast<const char *>(&s), W.state, static_cast<size_t>(P.C), c, 0,
-                           full ? TOTAL : St::HOT);
+                if (q == 1 && WfCompact<R, RK, INIT>::OK) {
+                    // entering the loop (full): the cold sectors too; the raw hot sectors are never read back
+                    typename WfCompact<R, RK, INIT>::Buf buf;
+                    WfCompact<R, RK, INIT>::pack(s.co, buf);
+                    WfCompact<R, RK, INIT>::store(buf, W.state, static_cast<size_t>(P.C), c);
+                    if (full)
+                        st_sectors(reinterpret_cast<const char *>(&s), W.state, static_cast<size_t>(P.C), c, St::HOT,
+                                   TOTAL);
+                } else {
+                    st_sectors(reinterpret_cast<const char *>(&s), W.state, static_cast<size_t>(P.C), c, 0,
+                               full ? TOTAL : St::HOT);
+                }
 #else
                 st_state(s, W.state, static_cast<size_t>(P.C), c);
 #endif
@@ -342,6 +478,78 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
         atomicAdd(&P.ch.rays[0], static_cast<unsigned long long>(sc));
         atomicAdd(&P.ch.rays[1], static_cast<unsigned long long>(sv));
     }
+}
+
+// The large-step bounce loop as its own kernel: half of all mutations spend ~11 rounds in
+// it and its live state is the compact image, so those resumes run here -- a few dozen
+// registers, no shared-memory coroutine, a small instruction footprint -- instead of in
+// k_wf_logic.  One thread per chain of the bounce queue: unpack, bounce_body (the
+// coroutine's own loop body), then either the next ray and the bounce queue again, or the
+// post-loop queue, from which k_wf_logic resumes the chain behind the loop next round.
+template <class R, int RK>
+__global__ void __launch_bounds__(128, sizeof(R) == 4 ? 8 : 1) k_wf_bounce(StepParams<R> P, WfParams<R> W) {
+    extern __shared__ __align__(32) char smem[];
+    SceneView<R> S = stage_scene(P.scene, smem);
+    using Cp = WfCompact<R, RK, false>;
+    const unsigned n = W.n_in[1];
+    const unsigned stride = gridDim.x * blockDim.x;
+    unsigned cast = 0;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31u) & ~31u); i += stride) {
+        const bool live = i < n;
+        bool cont = false;
+        int c = 0;
+        WfBounceRegs<R, RK> co;
+        V3<R> o, d;
+        if (live) {
+            c = W.cq_in[static_cast<size_t>(P.C) + i];
+            typename Cp::Buf buf;
+            Cp::load(buf, W.state, static_cast<size_t>(P.C), c);
+            Cp::unpack(co, buf, c, P);
+            const WfHit<R> h = W.hits[c];
+            const PvSmem<R> pv{W.pv + c, P.C};
+            cont = bounce_body<R, RK>(P, S, pv, co.ray, h.prim, h.t, co.rng, co.dpdf, co.kp, co.smp, co.tf, co.ok, o, d);
+        }
+        // warp-aggregated appends: continuing chains -> a ray and the bounce queue, the others -> post-loop queue
+        const unsigned lane = threadIdx.x & 31;
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned mc = __ballot_sync(0xffffffffu, live && cont);
+        const unsigned me = __ballot_sync(0xffffffffu, live && !cont);
+        unsigned base_c = 0, base_r = 0, base_e = 0;
+        if (lane == 0) {
+            if (mc) {
+                base_c = atomicAdd(W.n_out + 1, static_cast<unsigned>(__popc(mc)));
+                base_r = atomicAdd(W.n_rays, static_cast<unsigned>(__popc(mc)));
+            }
+            if (me)
+                base_e = atomicAdd(W.n_out + 4, static_cast<unsigned>(__popc(me)));
+        }
+        base_c = __shfl_sync(0xffffffffu, base_c, 0);
+        base_r = __shfl_sync(0xffffffffu, base_r, 0);
+        base_e = __shfl_sync(0xffffffffu, base_e, 0);
+        if (live) {
+            if (cont) {
+                co.ray.o = o;
+                co.ray.d = d;
+                ++cast;
+                const unsigned k = static_cast<unsigned>(__popc(mc & lt));
+                WfRay<R> r;
+                r.o[0] = o.x, r.o[1] = o.y, r.o[2] = o.z;
+                r.lim = M<R>::inf();
+                r.d[0] = d.x, r.d[1] = d.y, r.d[2] = d.z;
+                r.ck = c;
+                W.rays[base_r + k] = r;
+                W.cq_out[static_cast<size_t>(P.C) + base_c + k] = c;
+            } else {
+                W.cq_out[static_cast<size_t>(4) * P.C + base_e + __popc(me & lt)] = c;
+            }
+            typename Cp::Buf buf;
+            Cp::pack(co, buf);
+            Cp::store(buf, W.state, static_cast<size_t>(P.C), c);
+        }
+    }
+    cast = __reduce_add_sync(0xffffffffu, cast);
+    if (cast && (threadIdx.x & 31) == 0)
+        atomicAdd(&P.ch.rays[0], static_cast<unsigned long long>(cast));
 }
 
 template <class R> __device__ __forceinline__ WfRay<R> ld_ray(const WfRay<R> *p) { return *p; }

@@ -125,6 +125,41 @@ def test_f32_bvh_equals_f32_brute_force(strategy, rng, kernel, monkeypatch):
     np.testing.assert_allclose(iv, ib, rtol=1e-5, atol=1e-6 * float(np.abs(ib).max()))
 
 
+@pytest.mark.parametrize("rng", ["philox", "pcg32"])
+@pytest.mark.parametrize("strategy", ["fixed", "ra-quadtree"])
+def test_f32_wavefront_equals_fused_coroutine_kernel(strategy, rng, monkeypatch):
+    """The production build's wavefront step (queues per yield point, compact bounce-loop
+    state, hot / cold sectors) against the fused coroutine kernel k_step_co on the same BVH:
+    the same coroutine and arithmetic, so identical decisions, a, ray counts, lambda trace
+    and partition.  (The f64 wavefront is pinned to the reference by test_gpu_parity.)"""
+    from paper_2402_08273_b200 import scenes
+    monkeypatch.setenv("RAMLT_COOP", "0")
+    monkeypatch.setenv("RAMLT_INIT_KERNEL", "co")
+    scene = scenes.cluster_room(n_tris=2000, clusters=8, seed=3)
+    C, K = 3000, 24
+    out = []
+    for kernel in ("co", "wf"):
+        monkeypatch.setenv("RAMLT_STEP_KERNEL", kernel)
+        eng = _engine(scene, strategy=strategy, perturbation="lens", chains=C, mutations=C * K, width=128,
+                      height=128, max_vertices=13, b_samples=4096, seed=11, precision="f32", rng=rng,
+                      log_steps=K, adapt_mode="pooled", m_refine=C * 6, m_split=200, accel="bvh",
+                      dump_partition=True)
+        eng.set_b(1.0)
+        eng.init_chains()
+        eng.run(C * K)
+        a, f = eng.decisions(K)
+        s = eng.stats()
+        out.append((a, f, eng.image(), eng.trace(), eng.partition_dump(), s.rays_closest + s.rays_visibility))
+        eng.close()
+    (a1, f1, i1, t1, d1, r1), (a2, f2, i2, t2, d2, r2) = out
+    assert np.array_equal(f1, f2), np.argwhere(f1 != f2)[:5]
+    np.testing.assert_array_equal(a1, a2)
+    assert r1 == r2
+    np.testing.assert_array_equal(t1, t2)
+    assert d1 == d2
+    np.testing.assert_allclose(i2, i1, rtol=1e-4, atol=1e-6 * float(np.abs(i1).max()))
+
+
 @pytest.mark.parametrize("precision", ["f64", "f32"])
 def test_wavefront_pipelines_equal_single_range(precision, monkeypatch):
     """RAMLT_WF_PIPES=2: the chains stepped as two wavefront pipelines on two streams

@@ -39,3 +39,5 @@ timeout 600 python tools/e2e_phases.py c5 128 2>&1 | tail -1 | tee $OUT/e2e_phas
 RAMLT_WF_LOG=1 timeout 600 python tools/ncu_case.py clusters ra-quadtree lens 8388608 2 13 2048 > $OUT/wf_log_c5.txt 2>&1
 du -sh $OUT
 echo done
+timeout 1500 python tools/ab.py c5 "" hc "@RAMLT_WF_REFILL=4" "@RAMLT_WF_REFILL=12" "@RAMLT_WF_REFILL=16" 2>&1 | tail -5 | tee $OUT/ab_c5_refill.txt
+echo done2
