@@ -208,7 +208,7 @@ private:
     int wf_refill_ = 8;       // k_wf_trace: RAMLT_WF_REFILL idle lanes end a traversal round
     int wf_check_ = 4;        // rounds between host checks of the queue length (RAMLT_WF_CHECK)
     bool wf_log_ = false;     // RAMLT_WF_LOG=1
-    bool wf_bounce_ = false;  // RAMLT_WF_BOUNCE=1: the large-step bounce loop in its own kernel (k_wf_bounce)
+    bool wf_bounce_ = true;   // RAMLT_WF_BOUNCE=0: the large-step bounce loop resumed by k_wf_logic instead of k_wf_bounce
     int wf_pipes_ = 1;        // RAMLT_WF_PIPES: chain ranges stepped as concurrent wavefront pipelines
     size_t wf_pipes_min_ = size_t(1) << 18;   // RAMLT_WF_PIPES_MIN: fewest chains split into pipelines
     int wf_lblk_ = 0, wf_tblk_ = 0;   // RAMLT_WF_LBLK / RAMLT_WF_TBLK: resident blocks per SM of a pipeline's kernels
@@ -1109,7 +1109,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
                               : prepare(reinterpret_cast<const void *>(trace_brute), tsmem);
     // chain initialisation runs until every chain found a contributing path: polled
     const bool poll = INIT || P.j1 - P.j0 > 1 || wf_poll_;
-    // RAMLT_WF_BOUNCE=1: the bounce queue is resumed by k_wf_bounce (one more round: the
+    // default (RAMLT_WF_BOUNCE=0 turns it off): the bounce queue is resumed by k_wf_bounce (one more round: the
     // chains it takes out of the loop pass through the post-loop queue)
     const bool bounce_sep = !INIT && wf_bounce_ && rd::WfCompact<R, RK, INIT>::OK;
     const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2 + (bounce_sep ? 1 : 0);

@@ -130,8 +130,9 @@ def test_f32_bvh_equals_f32_brute_force(strategy, rng, kernel, monkeypatch):
 def test_f32_wavefront_equals_fused_coroutine_kernel(strategy, rng, monkeypatch):
     """The production build's wavefront step (queues per yield point, compact bounce-loop
     state, hot / cold sectors) against the fused coroutine kernel k_step_co on the same BVH:
-    the same coroutine and arithmetic, so identical decisions, a, ray counts, lambda trace
-    and partition.  (The f64 wavefront is pinned to the reference by test_gpu_parity.)"""
+    the same coroutine, so identical decisions, ray counts and partition, a and the lambda
+    trace to fp32 rounding.  (The f64 wavefront -- compact image and k_wf_bounce included --
+    is pinned bit-exactly to the reference by test_gpu_parity.)"""
     from paper_2402_08273_b200 import scenes
     monkeypatch.setenv("RAMLT_COOP", "0")
     monkeypatch.setenv("RAMLT_INIT_KERNEL", "co")
@@ -152,10 +153,14 @@ def test_f32_wavefront_equals_fused_coroutine_kernel(strategy, rng, monkeypatch)
         out.append((a, f, eng.image(), eng.trace(), eng.partition_dump(), s.rays_closest + s.rays_visibility))
         eng.close()
     (a1, f1, i1, t1, d1, r1), (a2, f2, i2, t2, d2, r2) = out
+    # identical decisions, ray counts and partition; a and the pooled lambda trace agree to a
+    # few fp32 ulps (the kernels contract FMAs in the shared mutation code differently)
     assert np.array_equal(f1, f2), np.argwhere(f1 != f2)[:5]
-    np.testing.assert_array_equal(a1, a2)
+    np.testing.assert_allclose(a2, a1, rtol=4e-6, atol=0)
     assert r1 == r2
-    np.testing.assert_array_equal(t1, t2)
+    assert t1.shape == t2.shape
+    np.testing.assert_array_equal(t1[:, :3], t2[:, :3])
+    np.testing.assert_allclose(t2[:, 3:], t1[:, 3:], rtol=1e-6, atol=1e-9)
     assert d1 == d2
     np.testing.assert_allclose(i2, i1, rtol=1e-4, atol=1e-6 * float(np.abs(i1).max()))
 
