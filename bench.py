@@ -674,9 +674,12 @@ def main():
         roofline["traversal_ceiling"] = {
             "k_trace_bench_rays_per_s": res["ceiling"], "in_step_rays_per_s_per_gpu": dev_rays,
             "frac": dev_rays / res["ceiling"],
-            "note": "the step kernel's BVH traversal loop alone on incoherent closest-hit rays, same BVH, "
-                    "same GPU (latency-bound: ncu long-scoreboard on node loads); the measured ceiling the "
-                    "in-step ray rate is compared with"}
+            "in_trace_kernel_rays_per_s": (res["rays_local"] / (res["trace_ms"] / 1e3)) if res.get("trace_ms") else None,
+            "note": "k_trace_bench: the fused coroutine kernel's BVH traversal loop alone on seeded incoherent "
+                    "closest-hit rays, same BVH, same GPU -- a traversal-only probe of this BVH; the whole-step "
+                    "ray rate (rays / step time, logic kernels included) is compared with it, and "
+                    "in_trace_kernel_rays_per_s is the rate inside the wavefront's k_wf_trace launches (its "
+                    "mix has camera rays and any-hit visibility rays, so it can exceed the probe)"}
     cpu = None
     if not args.no_cpu_baseline and res["world"] == 1:
         sample = args.cpu_sample or wl["cpu_sample"]

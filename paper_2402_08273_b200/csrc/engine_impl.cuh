@@ -1111,7 +1111,7 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     const bool poll = INIT || P.j1 - P.j0 > 1 || wf_poll_;
     // default (RAMLT_WF_BOUNCE=0 turns it off): the bounce queue is resumed by k_wf_bounce (one more round: the
     // chains it takes out of the loop pass through the post-loop queue)
-    const bool bounce_sep = !INIT && wf_bounce_ && rd::WfCompact<R, RK, INIT>::OK;
+    const bool bounce_sep = wf_bounce_ && rd::WfCompact<R, RK, INIT>::OK;
     const int planned = poll ? 0 : static_cast<int>(d_.max_vertices) + 2 + (bounce_sep ? 1 : 0);
     // Pipelines: the chains of a one-step launch are cut into wf_pipes_ contiguous ranges,
     // each with its own queues and counters, and the ranges' rounds are enqueued on
@@ -1132,10 +1132,8 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
     } pipe[2];
     const size_t bsmem = (smem_ + 31) & ~size_t(31);
     int bper = 1;
-    if constexpr (!INIT) {
-        if (bounce_sep)
-            bper = prepare(reinterpret_cast<const void *>(rd::k_wf_bounce<R, RK>), bsmem);
-    }
+    if (bounce_sep)
+        bper = prepare(reinterpret_cast<const void *>(rd::k_wf_bounce<R, RK, INIT>), bsmem);
     for (int p = 0; p < npipe; ++p) {
         Pipe &pp = pipe[p];
         pp.c0 = npipe == 1 ? 0 : (p == 0 ? 0 : ((C / 2 + 127) & ~size_t(127)));
@@ -1195,11 +1193,9 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
             if (r == 0 && p == 1)   // out of phase: the second range starts after the first's first logic kernel
                 RAMLT_CUDA(cudaStreamWaitEvent(pp.st, wf_ev_[2], 0));
             logic<<<pp.lblocks, 128, lsmem, pp.st>>>(PL, W, r == 0 ? 1 : 0);
-            if constexpr (!INIT) {
-                if (bounce_sep && r > 0) {
-                    rd::k_wf_bounce<R, RK><<<pp.bblocks, 128, bsmem, pp.st>>>(P, W);
-                    ++launches_;
-                }
+            if (bounce_sep && r > 0) {
+                rd::k_wf_bounce<R, RK, INIT><<<pp.bblocks, 128, bsmem, pp.st>>>(P, W);
+                ++launches_;
             }
             if (r == 0 && p == 0 && npipe > 1)
                 RAMLT_CUDA(cudaEventRecord(wf_ev_[2], pp.st));
@@ -1240,7 +1236,8 @@ void EngineT<R>::launch_step_wf(rd::StepParams<R> P) {
         // Multi-step launches (Fixed strategy) and chain initialisation poll every
         // wf_check_ rounds instead.
         const bool last_planned = !poll && r + 1 >= planned;
-        if (last_planned || (poll && r % wf_check_ == wf_check_ - 1)) {
+        const int check = INIT ? 8 * wf_check_ : wf_check_;   // initialisation runs thousands of short rounds
+        if (last_planned || (poll && r % check == check - 1)) {
             join();
             unsigned left = 0;
             for (int p = 0; p < npipe; ++p) {

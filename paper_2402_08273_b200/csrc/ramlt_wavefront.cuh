@@ -239,7 +239,7 @@ template <class R> __device__ __forceinline__ void WfSink<R>::cold() const {
     }
 }
 
-// Compact image of a chain inside the large-step bounce loop (steps, not INIT): the
+// Compact image of a chain inside the large-step bounce loop (steps and INIT): the
 // loop's live values in 2 sectors (fp32 / Philox) instead of the 4 hot ones -- the pending ray (its lim is
 // +inf), the Philox draw counter (key and stream follow from the seed and the chain id; the
 // cached block is recomputed from the counter, the same words), tf, dpdf, the specular mask,
@@ -252,15 +252,18 @@ template <int RK> struct WfRngSave;
 template <> struct WfRngSave<RNG_PHILOX> {
     unsigned long long draw;
     __device__ __forceinline__ void save(const Rng<RNG_PHILOX> &r) { draw = r.draw; }
-    template <class R> __device__ __forceinline__ void restore(Rng<RNG_PHILOX> &r, const StepParams<R> &P, int c) const {
-        r.reseed(P.seed, static_cast<unsigned long long>(P.chain_off + c));
+    template <bool INIT, class R>
+    __device__ __forceinline__ void restore(Rng<RNG_PHILOX> &r, const StepParams<R> &P, int c) const {
+        const unsigned long long gc = static_cast<unsigned long long>(P.chain_off + c);
+        r.reseed(P.seed, INIT ? kStreamInit + gc * 2ull : gc);   // the chain's init / step stream
         r.draw = draw;
     }
 };
 template <> struct WfRngSave<RNG_PCG> {
     unsigned long long state, inc;
     __device__ __forceinline__ void save(const Rng<RNG_PCG> &r) { state = r.state, inc = r.inc; }
-    template <class R> __device__ __forceinline__ void restore(Rng<RNG_PCG> &r, const StepParams<R> &, int) const {
+    template <bool INIT, class R>
+    __device__ __forceinline__ void restore(Rng<RNG_PCG> &r, const StepParams<R> &, int) const {
         r.state = state, r.inc = inc;
     }
 };
@@ -273,6 +276,7 @@ template <class R, int RK> struct WfBounceImage {
     unsigned smp;
     unsigned kp_flags;   // kp | choose << 8 | ok << 9 | accepted << 10 | pert_rec << 11
     int j, jend;
+    unsigned attempts;   // INIT
 };
 // The members of StepCo the image restores, for k_wf_bounce (no cold part, no coroutine).
 template <class R, int RK> struct WfBounceRegs {
@@ -287,7 +291,7 @@ template <class R, int RK> struct WfBounceRegs {
     unsigned attempts;
 };
 template <class R, int RK, bool INIT> struct WfCompact {
-    static constexpr bool OK = !INIT && RAMLT_WF_COMPACT && RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32;
+    static constexpr bool OK = RAMLT_WF_COMPACT && RAMLT_WF_HOTCOLD && RAMLT_WF_CHUNK32;
     using Img = WfBounceImage<R, RK>;
     static constexpr int N = static_cast<int>((sizeof(Img) + 31) / 32);   // sectors
     struct alignas(32) Buf {
@@ -305,6 +309,7 @@ template <class R, int RK, bool INIT> struct WfCompact {
                       (co.accepted ? 0x400u : 0u) | (co.pert_rec ? 0x800u : 0u);
         im.j = co.wf_j;
         im.jend = co.wf_jend;
+        im.attempts = co.attempts;
         memcpy(&buf, &im, sizeof(Img));
     }
     template <class CoT>
@@ -316,7 +321,7 @@ template <class R, int RK, bool INIT> struct WfCompact {
         co.ray.o = mk(im.o[0], im.o[1], im.o[2]);
         co.ray.d = mk(im.d[0], im.d[1], im.d[2]);
         co.ray.lim = M<R>::inf();
-        im.rng.restore(co.rng, P, c);
+        im.rng.template restore<INIT>(co.rng, P, c);
         co.tf = im.tf;
         co.dpdf = im.dpdf;
         co.smp = im.smp;
@@ -327,7 +332,7 @@ template <class R, int RK, bool INIT> struct WfCompact {
         co.pert_rec = (im.kp_flags & 0x800u) != 0;
         co.wf_j = im.j;
         co.wf_jend = im.jend;
-        co.attempts = 0;
+        co.attempts = im.attempts;
     }
     static __device__ __forceinline__ void load(Buf &buf, const uint4 *__restrict__ state, size_t C, int c) {
         const Sector *sp = reinterpret_cast<const Sector *>(state);
@@ -486,11 +491,11 @@ __global__ void __launch_bounds__(128, RAMLT_WF_SMEM && sizeof(R) == 4 ? 5 : 1) 
 // k_wf_logic.  One thread per chain of the bounce queue: unpack, bounce_body (the
 // coroutine's own loop body), then either the next ray and the bounce queue again, or the
 // post-loop queue, from which k_wf_logic resumes the chain behind the loop next round.
-template <class R, int RK>
+template <class R, int RK, bool INIT = false>
 __global__ void __launch_bounds__(128, sizeof(R) == 4 ? 8 : 1) k_wf_bounce(StepParams<R> P, WfParams<R> W) {
     extern __shared__ __align__(32) char smem[];
     SceneView<R> S = stage_scene(P.scene, smem);
-    using Cp = WfCompact<R, RK, false>;
+    using Cp = WfCompact<R, RK, INIT>;
     const unsigned n = W.n_in[1];
     const unsigned stride = gridDim.x * blockDim.x;
     unsigned cast = 0;
