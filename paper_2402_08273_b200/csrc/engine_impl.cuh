@@ -470,8 +470,9 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
     // Chain initialisation stays with the fused kernel by default: nearly every attempt of a
     // chain fails (c4/c5: ~37 attempts of ~11 rays before a path reaches a light), so as
     // wavefront rounds every chain's state makes thousands of HBM round trips -- c5 init
-    // 7.4 s (wf) vs 4.5 s (co), c4 1.86 s vs 0.75 s (profiles/r02t).  RAMLT_INIT_KERNEL=wf
-    // keeps the wavefront form for the parity tests.
+    // 7.4 s (wf) vs 4.5 s (co), c4 1.86 s vs 0.75 s (profiles/r02t); 5.7 s vs 4.5 s with the compact
+    // image and k_wf_bounce<INIT> (profiles/r02z: the ~7,000 nearly empty rounds of the unluckiest
+    // chains).  RAMLT_INIT_KERNEL=wf keeps the wavefront form for the parity tests.
     if (static_cast<unsigned long long>(C_) >= (1ull << rd::kWfChainBits) || d.max_vertices > 32)
         use_wf_init_ = false;
     if (const char *v = std::getenv("RAMLT_WF_REFILL"))
