@@ -370,7 +370,9 @@ EngineT<R>::EngineT(const HostScene &scene, const ramlt_render_desc &d) : d_(d),
             std::memcpy(&coords[9 * i + 3], hs_.tri[i].b, 3 * sizeof(double));
             std::memcpy(&coords[9 * i + 6], hs_.tri[i].c, 3 * sizeof(double));
         }
-        int leaf_max = 4;
+        // leaves of at most 2 triangles: c5 on the wavefront build 121.2 (4) / 124.4 (3) / 125.1 (2) /
+        // 117.5 (6) M mutations/s (profiles/r03a): 66 vs 59 node visits but 13 vs 27 triangle tests per ray
+        int leaf_max = 2;
         if (const char *v = std::getenv("RAMLT_BVH_LEAF"))
             leaf_max = std::max(1, std::min(15, std::atoi(v)));
         BvhBuild bb = build_bvh(coords.data(), hs_.tri.size(), leaf_max);
